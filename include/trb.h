@@ -1,0 +1,216 @@
+/*
+ * trb.h — C ABI of the B200-native video front end (motion -> 3x3 morphology
+ * -> connected components -> blob statistics -> mean-shift tracking).
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * ("teamrec", arXiv 1310.3322).  Every entry point replaces one reference
+ * C++ call; the reference file:line is cited beside it (paths relative to
+ * /root/reference/proj/include/teamrec/).  Plain pointers and sizes only:
+ * no torch or C++ types cross this boundary.
+ *
+ * Conventions
+ *   - Every function returns a trb_status; 0 is success.  On failure the
+ *     message is available from trb_last_error() (thread-local), with the
+ *     reference's own wording where the reference throws
+ *     (e.g. "motion detector expects grayscale frames", motion.hpp:165).
+ *   - The caller owns every buffer.  There is no cross-ABI free.
+ *   - Handles are not internally synchronised (same as the reference
+ *     objects, which are touched by one pipeline stage thread each,
+ *     pipeline.hpp:259-286).  Each handle owns a CUDA stream.
+ *   - There is no CPU fallback: without a usable sm_100 device every call
+ *     that computes returns TRB_CUDA_ERROR.
+ */
+#ifndef TRB_H_
+#define TRB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum trb_status {
+  TRB_OK = 0,
+  TRB_INVALID_ARGUMENT = 1, /* teamrec::InvalidArgument (error.hpp:15-18) */
+  TRB_CONFIG_ERROR = 2,     /* teamrec::ConfigError (error.hpp:27-30)     */
+  TRB_IO_ERROR = 3,         /* teamrec::IoError (error.hpp:21-24)         */
+  TRB_CUDA_ERROR = 4,       /* device missing / kernel fault              */
+  TRB_OUT_OF_MEMORY = 5,
+  TRB_CAPACITY = 6          /* caller buffer too small; *n holds the need */
+} trb_status;
+
+/* ---- configuration structs (field-for-field the reference structs) ---- */
+
+enum { TRB_BG_MEAN = 0, TRB_BG_MODE = 1 };       /* BackgroundMethod, motion.hpp:18 */
+enum { TRB_CONN_FOUR = 0, TRB_CONN_EIGHT = 1 };   /* Connectivity, segmentation.hpp:15 */
+enum { TRB_TRACK_ACTIVE = 0, TRB_TRACK_LOST = 1 }; /* TrackStatus, tracking.hpp:36 */
+/* 3x3 morphology is NOT in the reference; default OFF keeps parity. */
+enum { TRB_MORPH_NONE = 0, TRB_MORPH_ERODE = 1, TRB_MORPH_DILATE = 2, TRB_MORPH_OPEN = 3, TRB_MORPH_CLOSE = 4 };
+
+/* MotionConfig (motion.hpp:44-56).  warp must be 0 (identity). */
+typedef struct trb_motion_config {
+  int32_t method;    /* TRB_BG_MEAN | TRB_BG_MODE, default mean */
+  int32_t window;    /* default 91 */
+  int32_t threshold; /* default 25 */
+  int32_t bins;      /* default 32 */
+  int32_t warp;      /* 0 = identity */
+  int32_t morph;     /* extension: TRB_MORPH_*, default none */
+} trb_motion_config;
+
+/* SegmentationConfig (segmentation.hpp:25-34). */
+typedef struct trb_seg_config {
+  int32_t n_blocks;     /* default 4; validated, never changes the output */
+  int32_t connectivity; /* default eight */
+  int32_t min_area;     /* default 4 */
+} trb_seg_config;
+
+/* TrackerConfig (tracking.hpp:21-34). */
+typedef struct trb_tracker_config {
+  int32_t k_clusters;   /* default 16 */
+  int32_t max_iters;    /* default 20 */
+  double eps;           /* default 0.5 */
+  int32_t kmeans_iters; /* default 20 */
+  int32_t _pad;
+  uint64_t seed;        /* default 0 */
+} trb_tracker_config;
+
+/* Blob (segmentation.hpp:36-45) without the pixel list. */
+typedef struct trb_blob {
+  int32_t label, area, x_min, y_min, x_max, y_max;
+  double cx, cy;
+} trb_blob;
+
+/* TrackLogEntry (tracking.hpp:159-165). */
+typedef struct trb_track_log_entry {
+  int32_t frame, track_id;
+  double x, y;
+  int32_t w, h, status, _pad;
+} trb_track_log_entry;
+
+/* Track (tracking.hpp:40-50) scalar part; quantizer centres and the
+ * target histogram are read with trb_tracker_track_model(). */
+typedef struct trb_track {
+  int32_t track_id, w, h, status, lost_frames, k;
+  double cx, cy;
+} trb_track;
+
+/* ---- process-wide ---- */
+const char* trb_last_error(void);
+const char* trb_version(void);
+int trb_device_count(int* n);
+void trb_default_motion_config(trb_motion_config* c);
+void trb_default_seg_config(trb_seg_config* c);
+void trb_default_tracker_config(trb_tracker_config* c);
+/* validate() of each config: MotionConfig::validate motion.hpp:51-55,
+ * SegmentationConfig::validate segmentation.hpp:30-33,
+ * TrackerConfig::validate tracking.hpp:28-33. */
+int trb_motion_config_validate(const trb_motion_config* c);
+int trb_seg_config_validate(const trb_seg_config* c);
+int trb_tracker_config_validate(const trb_tracker_config* c);
+
+/* ---- MotionDetector (motion.hpp:149-212) ---- */
+typedef struct trb_motion trb_motion;
+/* MotionDetector(cfg, w, h), motion.hpp:151-157 */
+int trb_motion_create(const trb_motion_config* cfg, int width, int height, int device, trb_motion** out);
+int trb_motion_destroy(trb_motion* m);
+/* push(gray), motion.hpp:164-193.  gray: width*height bytes on the host,
+ * channels must be 1.  *has_mask = 0 until `window` frames arrived
+ * (std::nullopt), then mask_out (host, width*height bytes of 0/1) is
+ * written. */
+int trb_motion_push(trb_motion* m, const uint8_t* gray, int width, int height, int channels, int64_t frame_index,
+                    uint8_t* mask_out, int* has_mask);
+/* background(), motion.hpp:196-203 */
+int trb_motion_background(trb_motion* m, uint8_t* out);
+int trb_motion_frames_seen(const trb_motion* m, int* n);
+
+/* ---- label_blocked / label_sequential (segmentation.hpp:183-264) ----
+ * mask: host, w*h bytes (nonzero = foreground).  labels_out: host, w*h
+ * int32 (nullable).  blobs_out: host, blob_cap entries (nullable); the
+ * number of blobs is always written to *n_blobs; TRB_CAPACITY when
+ * blob_cap is too small.  pixels_out (nullable) receives the per-blob
+ * raster pixel lists (Blob::pixels, segmentation.hpp:141) concatenated in
+ * label order: sum(area) int64 entries. */
+int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* cfg, int device, int32_t* labels_out,
+              trb_blob* blobs_out, int blob_cap, int* n_blobs, int64_t* pixels_out, int64_t pixels_cap);
+
+/* ---- Tracker (tracking.hpp:170-241) ---- */
+typedef struct trb_tracker trb_tracker;
+int trb_tracker_create(const trb_tracker_config* cfg, int device, trb_tracker** out);
+int trb_tracker_destroy(trb_tracker* t);
+/* process(frame, blobs), tracking.hpp:179-205.  frame: host, w*h*channels. */
+int trb_tracker_process(trb_tracker* t, const uint8_t* frame, int width, int height, int channels,
+                        const trb_blob* blobs, int n_blobs);
+int trb_tracker_num_tracks(const trb_tracker* t, int* n);
+int trb_tracker_tracks(const trb_tracker* t, trb_track* out, int cap);
+/* centers: k*3 doubles, target_hist: k doubles, for track i (list order) */
+int trb_tracker_track_model(const trb_tracker* t, int i, double* centers, double* target_hist);
+int trb_tracker_log_size(const trb_tracker* t, int64_t* n);
+int trb_tracker_log(const trb_tracker* t, trb_track_log_entry* out, int64_t cap);
+int trb_tracker_frames_processed(const trb_tracker* t, int* n);
+
+/* ---- batched device-resident front end (run_vision, harness.hpp:412-450) ----
+ * n_streams independent camera streams of one geometry advance one frame
+ * per step: motion -> (morph) -> CCL -> blob stats -> tracking, each stage
+ * one launch for all streams.  Outputs stay in HBM until downloaded. */
+typedef struct trb_streams trb_streams;
+int trb_streams_create(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
+                       const trb_seg_config* sc, const trb_tracker_config* tc, int device, trb_streams** out);
+int trb_streams_destroy(trb_streams* s);
+/* frames: host array of n_streams DEVICE pointers (w*h*channels bytes each).
+ * cuda_stream: cudaStream_t to launch on (NULL = the handle's own). */
+int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* cuda_stream);
+/* frames: host array of n_streams HOST pointers (pinned for best speed);
+ * the H2D copy is part of the call.  If result_host is not NULL it
+ * receives n_streams int32 blob counts (the D2H read of the step). */
+int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t* result_host, void* cuda_stream);
+int trb_streams_synchronize(trb_streams* s);
+int trb_streams_frames_seen(const trb_streams* s, int* n);
+/* 1 once the window is full (a mask/labels/blobs exist for the last step) */
+int trb_streams_has_output(const trb_streams* s, int* has);
+int trb_streams_download_mask(trb_streams* s, int stream, uint8_t* out);
+int trb_streams_download_labels(trb_streams* s, int stream, int32_t* out);
+int trb_streams_download_blobs(trb_streams* s, int stream, trb_blob* out, int cap, int* n);
+int trb_streams_log_size(trb_streams* s, int stream, int64_t* n);
+int trb_streams_download_log(trb_streams* s, int stream, trb_track_log_entry* out, int64_t cap);
+int trb_streams_num_tracks(trb_streams* s, int stream, int* n);
+/* Kernel launches issued by the last step (for the bench's gpu_launches). */
+int trb_streams_last_step_launches(const trb_streams* s, int* n);
+/* Device pointers of the per-stream output planes (for device consumers). */
+int trb_streams_device_planes(trb_streams* s, int stream, uint8_t** mask, int32_t** labels);
+
+/* ---- synthetic input (synth.hpp:45-101), device rasteriser ----
+ * rects: n_shapes * 4 int32 (ix, iy, w, h) already rounded with lround on
+ * the host (synth.hpp:313-314); colors: n_shapes * 3 bytes.  Later shapes
+ * overwrite earlier ones.  out: DEVICE buffer w*h*channels. */
+int trb_synth_raster(uint8_t* out_device, int width, int height, int channels, uint8_t background,
+                     const int32_t* rects, const uint8_t* colors, int n_shapes, void* cuda_stream);
+
+
+/* ---- standalone tracker operations (public reference functions) ----
+ * frame: host, w*h*channels bytes.  Device-computed, bit-exact. */
+/* meanshift_step(frame, track, cfg), tracking.hpp:125-157.  *status is
+ * TRB_TRACK_ACTIVE / TRB_TRACK_LOST, in and out. */
+int trb_meanshift_step(const uint8_t* frame, int width, int height, int channels, double* cx, double* cy, int w,
+                       int h, const double* centers, const double* target_hist, int k, int max_iters, double eps,
+                       int* status, int device);
+/* histogram(frame, cx, cy, w, h, q, kernel), tracking.hpp:106-112
+ * (epanechnikov = 1, uniform = 0).  Errors as the reference:
+ * "histogram window must be >= 3x3", "histogram window does not intersect
+ * the frame". */
+int trb_histogram(const uint8_t* frame, int width, int height, int channels, double cx, double cy, int w, int h,
+                  const double* centers, int k, int epanechnikov, double* hist_out, int device);
+/* quantize_colors(pixels, k, iters, seed), quantize.hpp:43-118; samples must
+ * be integer-valued in [0, 65535] (as rgb_at produces). */
+int trb_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint64_t seed, double* centers_out,
+                        int device);
+
+/* ---- self tests of the exact-arithmetic replicas (host build of the same
+ * header the kernels use; on_device = 1 runs the device build) ---- */
+int trb_selftest_hypot(const double* x, const double* y, int64_t n, double* out, int on_device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRB_H_ */

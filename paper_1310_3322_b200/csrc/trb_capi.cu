@@ -1,0 +1,664 @@
+// trb_capi.cu — the extern "C" boundary (include/trb.h).  Converts
+// trb::Error exceptions into status codes + thread-local messages, owns the
+// per-handle device buffers and CUDA streams.  No computation happens on
+// the host: every result comes from the sm_100a kernels.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "trb_engine.cuh"
+#include "trb_exact.cuh"
+#include "trb_track.cuh"
+
+using trb::DevBuf;
+using trb::Error;
+using trb::PinnedBuf;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TRB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return TRB_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TRB_INVALID_ARGUMENT;
+  }
+}
+
+void need(bool cond, const char* msg, trb_status code = TRB_INVALID_ARGUMENT) {
+  if (!cond) throw Error(code, msg);
+}
+
+// Binds the calling thread to `device`, failing loudly when no sm_100
+// device exists (there is no CPU fallback).
+void use_device(int device) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw Error(TRB_CUDA_ERROR, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) throw Error(TRB_INVALID_ARGUMENT, "device index out of range");
+  TRB_CUDA(cudaSetDevice(device));
+}
+
+trb_motion_config default_motion() { return trb_motion_config{TRB_BG_MEAN, 91, 25, 32, 0, TRB_MORPH_NONE}; }
+}  // namespace
+
+// ---------------------------------------------------------------- handles
+struct trb_motion {
+  int device;
+  int w, h;
+  std::unique_ptr<trb::MotionState> m;
+  DevBuf frame, mask, tmp, ptrs;
+  cudaStream_t st = nullptr;
+  ~trb_motion() {
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+struct trb_tracker {
+  int device;
+  trb_tracker_config cfg;
+  std::unique_ptr<trb::TrackerState> t;
+  DevBuf frame, ptrs, blobs, nblobs;
+  size_t frame_bytes = 0;
+  int64_t blob_cap = 0;
+  cudaStream_t st = nullptr;
+  ~trb_tracker() {
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+struct trb_streams {
+  int device;
+  std::unique_ptr<trb::Streams> s;
+};
+
+extern "C" {
+
+const char* trb_last_error(void) { return g_last_error.c_str(); }
+const char* trb_version(void) { return "trb 0.1 (sm_100a)"; }
+
+int trb_device_count(int* n) {
+  return guard([&] {
+    need(n != nullptr, "null output");
+    *n = 0;
+    const cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) *n = 0;
+  });
+}
+
+void trb_default_motion_config(trb_motion_config* c) { *c = default_motion(); }
+void trb_default_seg_config(trb_seg_config* c) { *c = trb_seg_config{4, TRB_CONN_EIGHT, 4}; }
+void trb_default_tracker_config(trb_tracker_config* c) { *c = trb_tracker_config{16, 20, 0.5, 20, 0, 0}; }
+
+int trb_motion_config_validate(const trb_motion_config* c) {
+  return guard([&] { trb::validate_motion(*c); });
+}
+int trb_seg_config_validate(const trb_seg_config* c) {
+  return guard([&] { trb::validate_seg(*c, 0, 0); });
+}
+int trb_tracker_config_validate(const trb_tracker_config* c) {
+  return guard([&] { trb::validate_tracker(*c); });
+}
+
+// ------------------------------------------------------------- motion
+int trb_motion_create(const trb_motion_config* cfg, int width, int height, int device, trb_motion** out) {
+  return guard([&] {
+    need(cfg && out, "null argument");
+    *out = nullptr;
+    trb::validate_motion(*cfg);
+    if (width < 1 || height < 1) throw Error(TRB_INVALID_ARGUMENT, "motion detector needs positive frame dimensions");
+    use_device(device);
+    auto m = std::make_unique<trb_motion>();
+    m->device = device;
+    m->w = width;
+    m->h = height;
+    m->m = std::make_unique<trb::MotionState>(*cfg, 1, width, height, 1);
+    const size_t px = static_cast<size_t>(width) * height;
+    m->frame.alloc(px, false);
+    m->mask.alloc(px);
+    if (cfg->morph != TRB_MORPH_NONE) m->tmp.alloc(px);
+    m->ptrs.alloc(sizeof(void*), false);
+    const void* fp = m->frame.p;
+    TRB_CUDA(cudaMemcpy(m->ptrs.p, &fp, sizeof(void*), cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+    *out = m.release();
+  });
+}
+
+int trb_motion_destroy(trb_motion* m) {
+  return guard([&] {
+    if (m) {
+      cudaSetDevice(m->device);
+      delete m;
+    }
+  });
+}
+
+int trb_motion_push(trb_motion* m, const uint8_t* gray, int width, int height, int channels, int64_t frame_index,
+                    uint8_t* mask_out, int* has_mask) {
+  return guard([&] {
+    need(m && gray && has_mask, "null argument");
+    // MotionDetector::push checks, motion.hpp:165-167
+    if (channels != 1) throw Error(TRB_INVALID_ARGUMENT, "motion detector expects grayscale frames");
+    if (width != m->w || height != m->h)
+      throw Error(TRB_INVALID_ARGUMENT,
+                  "frame " + std::to_string(frame_index) + " dimensions do not match detector");
+    TRB_CUDA(cudaSetDevice(m->device));
+    const size_t px = static_cast<size_t>(width) * height;
+    TRB_CUDA(cudaMemcpyAsync(m->frame.p, gray, px, cudaMemcpyHostToDevice, m->st));
+    int launches = 0;
+    const bool emitted = m->m->push(m->ptrs.as<const uint8_t* const>(), m->mask.as<uint8_t>(), m->tmp.as<uint8_t>(),
+                                    m->st, &launches);
+    *has_mask = emitted ? 1 : 0;
+    if (emitted && mask_out) TRB_CUDA(cudaMemcpyAsync(mask_out, m->mask.p, px, cudaMemcpyDeviceToHost, m->st));
+    TRB_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+int trb_motion_background(trb_motion* m, uint8_t* out) {
+  return guard([&] {
+    need(m && out, "null argument");
+    TRB_CUDA(cudaSetDevice(m->device));
+    const size_t px = static_cast<size_t>(m->w) * m->h;
+    DevBuf bg;
+    bg.alloc(px, false);
+    m->m->background(bg.as<uint8_t>(), m->st);
+    TRB_CUDA(cudaMemcpyAsync(out, bg.p, px, cudaMemcpyDeviceToHost, m->st));
+    TRB_CUDA(cudaStreamSynchronize(m->st));
+  });
+}
+
+int trb_motion_frames_seen(const trb_motion* m, int* n) {
+  return guard([&] {
+    need(m && n, "null argument");
+    *n = m->m->frames_seen();
+  });
+}
+
+// ------------------------------------------------------------ labelling
+namespace {
+struct LabelWs {
+  std::unique_ptr<trb::CclState> ccl;
+  DevBuf mask;
+  cudaStream_t st = nullptr;
+  ~LabelWs() {
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+LabelWs& label_ws(int device, int w, int h, const trb_seg_config& cfg) {
+  thread_local std::map<std::tuple<int, int, int, int, int>, std::unique_ptr<LabelWs>> cache;
+  auto key = std::make_tuple(device, w, h, cfg.connectivity, cfg.min_area);
+  auto& slot = cache[key];
+  if (!slot) {
+    if (cache.size() > 8) {  // keep the cache small
+      for (auto it = cache.begin(); it != cache.end();)
+        if (it->first != key) it = cache.erase(it);
+        else ++it;
+    }
+    auto ws = std::make_unique<LabelWs>();
+    trb_seg_config c = cfg;
+    c.n_blocks = 1;
+    ws->ccl = std::make_unique<trb::CclState>(1, w, h, c);
+    ws->mask.alloc(static_cast<size_t>(w) * h, false);
+    TRB_CUDA(cudaStreamCreateWithFlags(&ws->st, cudaStreamNonBlocking));
+    slot = std::move(ws);
+  }
+  return *cache[key];
+}
+
+__global__ void mask_normalize_kernel(uint8_t* m, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) m[i] = m[i] != 0;
+}
+
+__global__ void iota_kernel(int64_t* v, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+struct NonZero {
+  __host__ __device__ bool operator()(const int32_t& x) const { return x != 0; }
+};
+
+// Blob::pixels: stable sort of the foreground pixel indices (already in
+// raster order) by label, on the device.
+void pixel_lists(const int32_t* labels, int64_t px, int64_t n_fg, int64_t* out_host, cudaStream_t st) {
+  DevBuf idx, keys, sel_idx, sel_keys, sorted_idx, sorted_keys, nsel, tmp;
+  idx.alloc(sizeof(int64_t) * px, false);
+  sel_idx.alloc(sizeof(int64_t) * (n_fg + 1), false);
+  sel_keys.alloc(sizeof(int32_t) * (n_fg + 1), false);
+  sorted_idx.alloc(sizeof(int64_t) * (n_fg + 1), false);
+  sorted_keys.alloc(sizeof(int32_t) * (n_fg + 1), false);
+  nsel.alloc(sizeof(int64_t), false);
+  iota_kernel<<<static_cast<unsigned>(trb::ceil_div64(px, 256)), 256, 0, st>>>(idx.as<int64_t>(), px);
+  size_t tb1 = 0, tb2 = 0, tb3 = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb1, idx.as<int64_t>(), labels, sel_idx.as<int64_t>(), nsel.as<int64_t>(), px,
+                             st);
+  cub::DeviceSelect::If(nullptr, tb2, labels, sel_keys.as<int32_t>(), nsel.as<int64_t>(), px, NonZero(), st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb3, sel_keys.as<int32_t>(), sorted_keys.as<int32_t>(),
+                                  sel_idx.as<int64_t>(), sorted_idx.as<int64_t>(), n_fg, 0, 32, st);
+  tmp.alloc(std::max(tb1, std::max(tb2, tb3)), false);
+  size_t t1 = tmp.n;
+  cub::DeviceSelect::Flagged(tmp.p, t1, idx.as<int64_t>(), labels, sel_idx.as<int64_t>(), nsel.as<int64_t>(), px, st);
+  size_t t2 = tmp.n;
+  cub::DeviceSelect::If(tmp.p, t2, labels, sel_keys.as<int32_t>(), nsel.as<int64_t>(), px, NonZero(), st);
+  size_t t3 = tmp.n;
+  cub::DeviceRadixSort::SortPairs(tmp.p, t3, sel_keys.as<int32_t>(), sorted_keys.as<int32_t>(), sel_idx.as<int64_t>(),
+                                  sorted_idx.as<int64_t>(), n_fg, 0, 32, st);
+  TRB_LAUNCH_CHECK("pixel_lists");
+  TRB_CUDA(cudaMemcpyAsync(out_host, sorted_idx.p, sizeof(int64_t) * n_fg, cudaMemcpyDeviceToHost, st));
+}
+}  // namespace
+
+int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* cfg, int device, int32_t* labels_out,
+              trb_blob* blobs_out, int blob_cap, int* n_blobs, int64_t* pixels_out, int64_t pixels_cap) {
+  return guard([&] {
+    need(mask && cfg && n_blobs, "null argument");
+    need(width >= 1 && height >= 1, "mask dimensions must be >= 1");
+    trb::validate_seg(*cfg, width, height);
+    use_device(device);
+    LabelWs& ws = label_ws(device, width, height, *cfg);
+    const int64_t px = static_cast<int64_t>(width) * height;
+    TRB_CUDA(cudaMemcpyAsync(ws.mask.p, mask, px, cudaMemcpyHostToDevice, ws.st));
+    mask_normalize_kernel<<<static_cast<unsigned>(trb::ceil_div64(px, 256)), 256, 0, ws.st>>>(ws.mask.as<uint8_t>(),
+                                                                                              px);
+    int launches = 0;
+    ws.ccl->run(ws.mask.as<uint8_t>(), ws.st, &launches);
+    int32_t nb = 0;
+    TRB_CUDA(cudaMemcpyAsync(&nb, ws.ccl->nblobs(), sizeof(int32_t), cudaMemcpyDeviceToHost, ws.st));
+    if (labels_out)
+      TRB_CUDA(cudaMemcpyAsync(labels_out, ws.ccl->labels(), sizeof(int32_t) * px, cudaMemcpyDeviceToHost, ws.st));
+    TRB_CUDA(cudaStreamSynchronize(ws.st));
+    *n_blobs = nb;
+    if (blobs_out && nb > 0)
+      TRB_CUDA(cudaMemcpyAsync(blobs_out, ws.ccl->blobs(), sizeof(trb_blob) * std::min(nb, blob_cap),
+                               cudaMemcpyDeviceToHost, ws.st));
+    if (pixels_out) {
+      // foreground pixels that survived min_area = sum of blob areas
+      std::vector<trb_blob> bl(nb);
+      if (nb > 0)
+        TRB_CUDA(cudaMemcpyAsync(bl.data(), ws.ccl->blobs(), sizeof(trb_blob) * nb, cudaMemcpyDeviceToHost, ws.st));
+      TRB_CUDA(cudaStreamSynchronize(ws.st));
+      int64_t n_fg = 0;
+      for (const auto& b : bl) n_fg += b.area;
+      if (n_fg > pixels_cap) throw Error(TRB_CAPACITY, "pixel list buffer too small");
+      if (n_fg > 0) pixel_lists(ws.ccl->labels(), px, n_fg, pixels_out, ws.st);
+    }
+    TRB_CUDA(cudaStreamSynchronize(ws.st));
+    if (blobs_out && nb > blob_cap) throw Error(TRB_CAPACITY, "blob buffer too small");
+  });
+}
+
+// ------------------------------------------------------------- tracker
+int trb_tracker_create(const trb_tracker_config* cfg, int device, trb_tracker** out) {
+  return guard([&] {
+    need(cfg && out, "null argument");
+    *out = nullptr;
+    trb::validate_tracker(*cfg);
+    use_device(device);
+    auto t = std::make_unique<trb_tracker>();
+    t->device = device;
+    t->cfg = *cfg;
+    t->t = std::make_unique<trb::TrackerState>(*cfg, 1, 4096, 1 << 20);
+    t->ptrs.alloc(sizeof(void*), false);
+    t->nblobs.alloc(sizeof(int32_t));
+    TRB_CUDA(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
+    *out = t.release();
+  });
+}
+
+int trb_tracker_destroy(trb_tracker* t) {
+  return guard([&] {
+    if (t) {
+      cudaSetDevice(t->device);
+      delete t;
+    }
+  });
+}
+
+int trb_tracker_process(trb_tracker* t, const uint8_t* frame, int width, int height, int channels,
+                        const trb_blob* blobs, int n_blobs) {
+  return guard([&] {
+    need(t && frame, "null argument");
+    need(width >= 1 && height >= 1, "frame dimensions must be >= 1");
+    need(channels == 1 || channels == 3, "frame channels must be 1 or 3");
+    need(n_blobs >= 0 && (n_blobs == 0 || blobs), "bad blob list");
+    TRB_CUDA(cudaSetDevice(t->device));
+    const size_t fb = static_cast<size_t>(width) * height * channels;
+    if (fb > t->frame_bytes) {
+      t->frame.alloc(fb, false);
+      t->frame_bytes = fb;
+      const void* fp = t->frame.p;
+      TRB_CUDA(cudaMemcpy(t->ptrs.p, &fp, sizeof(void*), cudaMemcpyHostToDevice));
+    }
+    if (n_blobs > t->blob_cap) {
+      t->blob_cap = std::max<int64_t>(n_blobs, 2 * t->blob_cap);
+      t->blobs.alloc(sizeof(trb_blob) * t->blob_cap, false);
+    }
+    if (t->blob_cap == 0) {
+      t->blob_cap = 16;
+      t->blobs.alloc(sizeof(trb_blob) * 16, false);
+    }
+    TRB_CUDA(cudaMemcpyAsync(t->frame.p, frame, fb, cudaMemcpyHostToDevice, t->st));
+    if (n_blobs > 0)
+      TRB_CUDA(cudaMemcpyAsync(t->blobs.p, blobs, sizeof(trb_blob) * n_blobs, cudaMemcpyHostToDevice, t->st));
+    const int32_t nb = n_blobs;
+    TRB_CUDA(cudaMemcpyAsync(t->nblobs.p, &nb, sizeof(int32_t), cudaMemcpyHostToDevice, t->st));
+    int launches = 0;
+    t->t->process(t->ptrs.as<const uint8_t* const>(), width, height, channels, t->blobs.as<trb_blob>(), t->blob_cap,
+                  t->nblobs.as<int32_t>(), t->st, &launches);
+    t->t->check_errors(t->st);
+  });
+}
+
+int trb_tracker_num_tracks(const trb_tracker* t, int* n) {
+  return guard([&] {
+    need(t && n, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    *n = t->t->num_tracks(0, t->st);
+  });
+}
+
+int trb_tracker_tracks(const trb_tracker* t, trb_track* out, int cap) {
+  return guard([&] {
+    need(t && out, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    t->t->tracks(0, out, cap, t->st);
+  });
+}
+
+int trb_tracker_track_model(const trb_tracker* t, int i, double* centers, double* target_hist) {
+  return guard([&] {
+    need(t != nullptr, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    need(i >= 0 && i < t->t->num_tracks(0, t->st), "track index out of range");
+    t->t->track_model(0, i, centers, target_hist, t->st);
+  });
+}
+
+int trb_tracker_log_size(const trb_tracker* t, int64_t* n) {
+  return guard([&] {
+    need(t && n, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    *n = t->t->log_size(0, t->st);
+  });
+}
+
+int trb_tracker_log(const trb_tracker* t, trb_track_log_entry* out, int64_t cap) {
+  return guard([&] {
+    need(t && out, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    t->t->log(0, out, cap, t->st);
+  });
+}
+
+int trb_tracker_frames_processed(const trb_tracker* t, int* n) {
+  return guard([&] {
+    need(t && n, "null argument");
+    TRB_CUDA(cudaSetDevice(t->device));
+    *n = t->t->frames_processed(0, t->st);
+  });
+}
+
+// ------------------------------------------------------------- streams
+int trb_streams_create(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
+                       const trb_seg_config* sc, const trb_tracker_config* tc, int device, trb_streams** out) {
+  return guard([&] {
+    need(out != nullptr, "null argument");
+    *out = nullptr;
+    use_device(device);
+    const trb_motion_config m = mc ? *mc : default_motion();
+    const trb_seg_config s = sc ? *sc : trb_seg_config{4, TRB_CONN_EIGHT, 4};
+    trb_tracker_config t{16, 20, 0.5, 20, 0, 0};
+    if (tc) t = *tc;
+    auto h = std::make_unique<trb_streams>();
+    h->device = device;
+    h->s = std::make_unique<trb::Streams>(n_streams, width, height, channels, m, s, t, tc != nullptr);
+    *out = h.release();
+  });
+}
+
+int trb_streams_destroy(trb_streams* s) {
+  return guard([&] {
+    if (s) {
+      cudaSetDevice(s->device);
+      delete s;
+    }
+  });
+}
+
+int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* cuda_stream) {
+  return guard([&] {
+    need(s && frames, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->step_device(frames, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t* result_host, void* cuda_stream) {
+  return guard([&] {
+    need(s && frames, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->step_host(frames, result_host, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int trb_streams_synchronize(trb_streams* s) {
+  return guard([&] {
+    need(s != nullptr, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    if (s->s->tracker()) s->s->tracker()->check_errors(s->s->stream());
+  });
+}
+
+int trb_streams_frames_seen(const trb_streams* s, int* n) {
+  return guard([&] {
+    need(s && n, "null argument");
+    *n = s->s->frames_seen();
+  });
+}
+
+int trb_streams_has_output(const trb_streams* s, int* has) {
+  return guard([&] {
+    need(s && has, "null argument");
+    *has = s->s->has_output() ? 1 : 0;
+  });
+}
+
+int trb_streams_download_mask(trb_streams* s, int stream, uint8_t* out) {
+  return guard([&] {
+    need(s && out, "null argument");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    TRB_CUDA(cudaMemcpy(out, s->s->mask(stream), s->s->px(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int trb_streams_download_labels(trb_streams* s, int stream, int32_t* out) {
+  return guard([&] {
+    need(s && out, "null argument");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    TRB_CUDA(cudaMemcpy(out, s->s->ccl().labels() + s->s->px() * stream, sizeof(int32_t) * s->s->px(),
+                        cudaMemcpyDeviceToHost));
+  });
+}
+
+int trb_streams_download_blobs(trb_streams* s, int stream, trb_blob* out, int cap, int* n) {
+  return guard([&] {
+    need(s && n, "null argument");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    int32_t nb = 0;
+    TRB_CUDA(cudaMemcpy(&nb, s->s->ccl().nblobs() + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    *n = nb;
+    if (out && nb > 0)
+      TRB_CUDA(cudaMemcpy(out, s->s->ccl().blobs() + s->s->ccl().blob_cap() * stream,
+                          sizeof(trb_blob) * std::min(nb, cap), cudaMemcpyDeviceToHost));
+    if (out && nb > cap) throw Error(TRB_CAPACITY, "blob buffer too small");
+  });
+}
+
+int trb_streams_log_size(trb_streams* s, int stream, int64_t* n) {
+  return guard([&] {
+    need(s && n, "null argument");
+    need(s->s->tracker() != nullptr, "streams were created without a tracker");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    *n = s->s->tracker()->log_size(stream, s->s->stream());
+  });
+}
+
+int trb_streams_download_log(trb_streams* s, int stream, trb_track_log_entry* out, int64_t cap) {
+  return guard([&] {
+    need(s && out, "null argument");
+    need(s->s->tracker() != nullptr, "streams were created without a tracker");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    s->s->tracker()->check_errors(s->s->stream());
+    s->s->tracker()->log(stream, out, cap, s->s->stream());
+  });
+}
+
+int trb_streams_num_tracks(trb_streams* s, int stream, int* n) {
+  return guard([&] {
+    need(s && n, "null argument");
+    need(s->s->tracker() != nullptr, "streams were created without a tracker");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    *n = s->s->tracker()->num_tracks(stream, s->s->stream());
+  });
+}
+
+int trb_streams_last_step_launches(const trb_streams* s, int* n) {
+  return guard([&] {
+    need(s && n, "null argument");
+    *n = s->s->last_launches();
+  });
+}
+
+int trb_streams_device_planes(trb_streams* s, int stream, uint8_t** mask, int32_t** labels) {
+  return guard([&] {
+    need(s != nullptr, "null argument");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    if (mask) *mask = s->s->mask(stream);
+    if (labels) *labels = s->s->ccl().labels() + s->s->px() * stream;
+  });
+}
+
+int trb_synth_raster(uint8_t* out_device, int width, int height, int channels, uint8_t background,
+                     const int32_t* rects, const uint8_t* colors, int n_shapes, void* cuda_stream) {
+  return guard([&] {
+    need(out_device != nullptr, "null argument");
+    need(channels == 1 || channels == 3, "clip channels must be 1 or 3");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    DevBuf d;
+    d.alloc(sizeof(int32_t) * 4 * n_shapes + 3 * n_shapes + 16, false);
+    int32_t* dr = d.as<int32_t>();
+    uint8_t* dc = reinterpret_cast<uint8_t*>(dr + 4 * n_shapes);
+    if (n_shapes > 0) {
+      TRB_CUDA(cudaMemcpyAsync(dr, rects, sizeof(int32_t) * 4 * n_shapes, cudaMemcpyHostToDevice, st));
+      TRB_CUDA(cudaMemcpyAsync(dc, colors, 3 * n_shapes, cudaMemcpyHostToDevice, st));
+    }
+    trb::launch_synth_raster(out_device, width, height, channels, background, dr, dc, n_shapes, st);
+    TRB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// ----------------------------------------------------- standalone ops
+int trb_meanshift_step(const uint8_t* frame, int width, int height, int channels, double* cx, double* cy, int w,
+                       int h, const double* centers, const double* target_hist, int k, int max_iters, double eps,
+                       int* status, int device) {
+  return guard([&] {
+    need(frame && cx && cy && centers && target_hist && status, "null argument");
+    need(channels == 1 || channels == 3, "frame channels must be 1 or 3");
+    need(k >= 1, "quantizer needs at least one centre");
+    if (*status != TRB_TRACK_ACTIVE) return;  // meanshift_step, tracking.hpp:126
+    use_device(device);
+    const size_t fb = static_cast<size_t>(width) * height * channels;
+    DevBuf f;
+    f.alloc(fb, false);
+    TRB_CUDA(cudaMemcpy(f.p, frame, fb, cudaMemcpyHostToDevice));
+    trb::device_meanshift_step(f.as<uint8_t>(), width, height, channels, cx, cy, w, h, centers, target_hist, k,
+                               max_iters, eps, status, nullptr);
+  });
+}
+
+int trb_histogram(const uint8_t* frame, int width, int height, int channels, double cx, double cy, int w, int h,
+                  const double* centers, int k, int epanechnikov, double* hist_out, int device) {
+  return guard([&] {
+    need(frame && centers && hist_out, "null argument");
+    // histogram(), tracking.hpp:108-110
+    if (w < 3 || h < 3) throw Error(TRB_INVALID_ARGUMENT, "histogram window must be >= 3x3");
+    use_device(device);
+    const size_t fb = static_cast<size_t>(width) * height * channels;
+    DevBuf f;
+    f.alloc(fb, false);
+    TRB_CUDA(cudaMemcpy(f.p, frame, fb, cudaMemcpyHostToDevice));
+    if (!trb::device_histogram(f.as<uint8_t>(), width, height, channels, cx, cy, w, h, centers, k, epanechnikov,
+                               hist_out, nullptr))
+      throw Error(TRB_INVALID_ARGUMENT, "histogram window does not intersect the frame");
+  });
+}
+
+int trb_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint64_t seed, double* centers_out,
+                        int device) {
+  return guard([&] {
+    need(pixels && centers_out, "null argument");
+    use_device(device);
+    trb::device_quantize_colors(pixels, n, k, iters, seed, centers_out, nullptr);
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ self tests
+namespace {
+__global__ void hypot_kernel(const double* x, const double* y, int64_t n, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = trb::glibc_hypot(x[i], y[i]);
+}
+}  // namespace
+
+extern "C" int trb_selftest_hypot(const double* x, const double* y, int64_t n, double* out, int on_device) {
+  return guard([&] {
+    need(x && y && out, "null argument");
+    if (!on_device) {
+      for (int64_t i = 0; i < n; ++i) out[i] = trb::glibc_hypot(x[i], y[i]);
+      return;
+    }
+    use_device(0);
+    DevBuf dx, dy, dout;
+    dx.alloc(sizeof(double) * n, false);
+    dy.alloc(sizeof(double) * n, false);
+    dout.alloc(sizeof(double) * n, false);
+    TRB_CUDA(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaMemcpy(dy.p, y, sizeof(double) * n, cudaMemcpyHostToDevice));
+    hypot_kernel<<<static_cast<unsigned>(trb::ceil_div64(n, 256)), 256>>>(dx.as<double>(), dy.as<double>(), n,
+                                                                         dout.as<double>());
+    TRB_LAUNCH_CHECK("hypot_kernel");
+    TRB_CUDA(cudaMemcpy(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  });
+}

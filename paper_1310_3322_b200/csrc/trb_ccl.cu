@@ -1,0 +1,423 @@
+// trb_ccl.cu — north-star kernels (3) and (4): connected-component
+// labelling as tile-local union-find + a boundary-merge pass + canonical
+// relabelling, and per-blob area/bbox/centroid reduction.
+//
+// Reference: label_blocked / label_sequential (segmentation.hpp:183-264),
+// label_window + UnionFind (:154-178, :58-75), finalize_labels (:88-149).
+//
+// Canonical output (segmentation.hpp:193-197): labels are dense 1..k in
+// raster order of each component's first pixel, components with
+// area < min_area dropped and the survivors compacted.  So the final label
+// of a component is 1 + the number of surviving components whose minimum
+// linear pixel index is smaller — computed here from a per-row survivor
+// count (exclusive scan over rows) plus a per-row survivor bitmap
+// (popcount of the bits to the left).  `n_blocks` never changes the output.
+//
+// Kernels (grid.z or grid.y = stream):
+//   ccl_local    32x32 tile in shared memory: union-find (atomicMin, root =
+//                smallest local index = raster-first pixel), per tile
+//                component stats (area, bbox, sum x, sum y), one global slot
+//                per tile component; labg[p] = slot for foreground pixels
+//   ccl_merge    unions across tile seams on the slot union-find
+//   ccl_resolve  slot -> set root; stats of non-root slots atomically
+//                folded into their root
+//   ccl_mark     surviving roots: bitmap bit + per-row count
+//   ccl_scan     exclusive scan of the row counts (one CTA per stream)
+//   ccl_assign   rank of every slot's component; Blob record per survivor
+//   ccl_final    labels[p] = dense[labg[p]] (16 pixels per thread)
+#include "trb_kernels.cuh"
+
+namespace trb {
+
+namespace {
+
+__device__ __forceinline__ int sfind(const int* lab, int i) {
+  int p = lab[i];
+  while (p != i) {
+    i = p;
+    p = lab[i];
+  }
+  return i;
+}
+
+// Playne & Hawick style lock-free union in shared memory: the larger root
+// is pointed at the smaller with atomicMin until one attempt lands on a
+// root.
+__device__ __forceinline__ void sunion(int* lab, int a, int b) {
+  bool done;
+  do {
+    a = sfind(lab, a);
+    b = sfind(lab, b);
+    if (a < b) {
+      const int old = atomicMin(&lab[b], a);
+      done = (old == b);
+      b = old;
+    } else if (b < a) {
+      const int old = atomicMin(&lab[a], b);
+      done = (old == a);
+      a = old;
+    } else {
+      done = true;
+    }
+  } while (!done);
+}
+
+__device__ __forceinline__ int gfind(int* parent, int s) {
+  int p = *reinterpret_cast<volatile int*>(&parent[s]);
+  while (p != s) {
+    const int gp = *reinterpret_cast<volatile int*>(&parent[p]);
+    if (gp != p) atomicMin(&parent[s], gp);  // path halving; monotone, ancestors only
+    s = p;
+    p = gp;
+  }
+  return s;
+}
+
+__device__ __forceinline__ void gunion(int* parent, int a, int b) {
+  bool done;
+  do {
+    a = gfind(parent, a);
+    b = gfind(parent, b);
+    if (a < b) {
+      const int old = atomicMin(&parent[b], a);
+      done = (old == b);
+      b = old;
+    } else if (b < a) {
+      const int old = atomicMin(&parent[a], b);
+      done = (old == a);
+      a = old;
+    } else {
+      done = true;
+    }
+  } while (!done);
+}
+
+__device__ __forceinline__ SlotTable slot_base(const CclArgs& a, int s) {
+  SlotTable t = a.slots;
+  const int64_t o = static_cast<int64_t>(s) * a.slot_cap;
+  t.parent += o, t.root += o, t.area += o, t.x0 += o, t.y0 += o, t.x1 += o, t.y1 += o;
+  t.sx += o, t.sy += o, t.minpix += o, t.dense += o;
+  return t;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ local
+__global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
+  __shared__ int lab[kTilePx];
+  __shared__ int cid[kTilePx];  // compact component id of each local root
+  __shared__ int st_area[kMaxTileComps], st_x0[kMaxTileComps], st_y0[kMaxTileComps], st_x1[kMaxTileComps],
+      st_y1[kMaxTileComps], st_sx[kMaxTileComps], st_sy[kMaxTileComps];
+  __shared__ int n_comp, slot_base_id;
+
+  const int s = blockIdx.z;
+  const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
+  int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
+  const int tx0 = blockIdx.x * kTileW, ty0 = blockIdx.y * kTileH;
+  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  const int gx = tx0 + c;
+  if (threadIdx.x == 0) n_comp = 0;
+
+  // 1. load: every foreground pixel starts as its own root
+  bool fg[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = r0 + 8 * k, gy = ty0 + r;
+    const int i = r * kTileW + c;
+    fg[k] = gx < a.w && gy < a.h && mask[static_cast<int64_t>(gy) * a.w + gx] != 0;
+    lab[i] = fg[k] ? i : -1;
+  }
+  __syncthreads();
+
+  // 2. merge with the already-visited neighbours inside the tile
+  //    (label_window's left / up / up-left / up-right, segmentation.hpp:169-174)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!fg[k]) continue;
+    const int r = r0 + 8 * k, i = r * kTileW + c;
+    if (c > 0 && lab[i - 1] >= 0) sunion(lab, i, i - 1);
+    if (r > 0) {
+      if (lab[i - kTileW] >= 0) {
+        sunion(lab, i, i - kTileW);
+      } else if (a.conn == TRB_CONN_EIGHT) {
+        if (c > 0 && lab[i - kTileW - 1] >= 0) sunion(lab, i, i - kTileW - 1);
+        if (c < kTileW - 1 && lab[i - kTileW + 1] >= 0) sunion(lab, i, i - kTileW + 1);
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3. flatten; number the local roots
+  int root[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = (r0 + 8 * k) * kTileW + c;
+    root[k] = fg[k] ? sfind(lab, i) : -1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = (r0 + 8 * k) * kTileW + c;
+    if (fg[k]) lab[i] = root[k];
+    if (fg[k] && root[k] == i) {
+      const int id = atomicAdd(&n_comp, 1);
+      cid[i] = id;
+      st_area[id] = 0;
+      st_x0[id] = INT_MAX, st_y0[id] = INT_MAX, st_x1[id] = -1, st_y1[id] = -1;
+      st_sx[id] = 0, st_sy[id] = 0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && n_comp > 0) slot_base_id = atomicAdd(&a.nslots[s], n_comp);
+
+  // 4. tile-component statistics (integer, order-free)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!fg[k]) continue;
+    const int gy = ty0 + r0 + 8 * k;
+    const int id = cid[root[k]];
+    atomicAdd(&st_area[id], 1);
+    atomicMin(&st_x0[id], gx);
+    atomicMin(&st_y0[id], gy);
+    atomicMax(&st_x1[id], gx);
+    atomicMax(&st_y1[id], gy);
+    atomicAdd(&st_sx[id], gx);
+    atomicAdd(&st_sy[id], gy);
+  }
+  __syncthreads();
+  if (n_comp == 0) return;
+  const int base = slot_base_id;
+
+  // 5. slot id per foreground pixel; slot records per tile component
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!fg[k]) continue;
+    const int gy = ty0 + r0 + 8 * k;
+    labg[static_cast<int64_t>(gy) * a.w + gx] = base + cid[root[k]];
+  }
+  SlotTable t = slot_base(a, s);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = (r0 + 8 * k) * kTileW + c;
+    if (!fg[k] || root[k] != i) continue;
+    const int id = cid[i];
+    const int slot = base + id;
+    const int gy = ty0 + r0 + 8 * k;
+    t.parent[slot] = slot;
+    t.area[slot] = st_area[id];
+    t.x0[slot] = st_x0[id];
+    t.y0[slot] = st_y0[id];
+    t.x1[slot] = st_x1[id];
+    t.y1[slot] = st_y1[id];
+    t.sx[slot] = static_cast<unsigned long long>(st_sx[id]);
+    t.sy[slot] = static_cast<unsigned long long>(st_sy[id]);
+    t.minpix[slot] = gy * a.w + gx;
+  }
+}
+
+// ------------------------------------------------------------------ merge
+// One thread per tile-seam pixel: 32 top-seam + 32 left-seam per tile.
+__global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
+  const int s = blockIdx.y;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n_tiles = static_cast<int64_t>(a.tiles_x) * a.tiles_y;
+  if (gid >= n_tiles * 64) return;
+  const int tile = static_cast<int>(gid >> 6), j = static_cast<int>(gid & 63);
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
+  const int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
+  int* parent = a.slots.parent + static_cast<int64_t>(s) * a.slot_cap;
+  const int w = a.w, h = a.h;
+  auto fgat = [&](int x, int y) { return mask[static_cast<int64_t>(y) * w + x] != 0; };
+  auto sl = [&](int x, int y) { return labg[static_cast<int64_t>(y) * w + x]; };
+  if (j < 32) {  // top seam: (x, y) against row y-1
+    if (ty == 0) return;
+    const int x = tx * kTileW + j, y = ty * kTileH;
+    if (x >= w || y >= h || !fgat(x, y)) return;
+    const int me = sl(x, y);
+    if (fgat(x, y - 1)) {
+      gunion(parent, me, sl(x, y - 1));
+    } else if (a.conn == TRB_CONN_EIGHT) {
+      if (x > 0 && fgat(x - 1, y - 1)) gunion(parent, me, sl(x - 1, y - 1));
+      if (x + 1 < w && fgat(x + 1, y - 1)) gunion(parent, me, sl(x + 1, y - 1));
+    }
+  } else {  // left seam: (x, y) against column x-1
+    if (tx == 0) return;
+    const int x = tx * kTileW, y = ty * kTileH + (j - 32);
+    if (x >= w || y >= h || !fgat(x, y)) return;
+    const int me = sl(x, y);
+    if (fgat(x - 1, y)) gunion(parent, me, sl(x - 1, y));
+    if (a.conn == TRB_CONN_EIGHT) {
+      if (y > 0 && fgat(x - 1, y - 1)) gunion(parent, me, sl(x - 1, y - 1));
+      if (y + 1 < h && fgat(x - 1, y + 1)) gunion(parent, me, sl(x - 1, y + 1));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- resolve
+__global__ void __launch_bounds__(256) ccl_resolve_kernel(CclArgs a) {
+  const int s = blockIdx.y;
+  const int n = a.nslots[s];
+  SlotTable t = slot_base(a, s);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = gfind(t.parent, i);
+    t.root[i] = r;
+    if (r == i) continue;
+    atomicAdd(&t.area[r], t.area[i]);
+    atomicMin(&t.x0[r], t.x0[i]);
+    atomicMin(&t.y0[r], t.y0[i]);
+    atomicMax(&t.x1[r], t.x1[i]);
+    atomicMax(&t.y1[r], t.y1[i]);
+    atomicAdd(&t.sx[r], t.sx[i]);
+    atomicAdd(&t.sy[r], t.sy[i]);
+    atomicMin(&t.minpix[r], t.minpix[i]);
+  }
+}
+
+// ------------------------------------------------------------------- mark
+__global__ void __launch_bounds__(256) ccl_mark_kernel(CclArgs a) {
+  const int s = blockIdx.y;
+  const int n = a.nslots[s];
+  SlotTable t = slot_base(a, s);
+  int32_t* rowcount = a.rowcount + static_cast<int64_t>(s) * a.h;
+  uint32_t* bitmap = a.bitmap + static_cast<int64_t>(s) * a.h * a.wpr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (t.root[i] != i || t.area[i] < a.min_area) continue;
+    const int pos = t.minpix[i];
+    const int y = pos / a.w, x = pos - y * a.w;
+    atomicOr(&bitmap[static_cast<int64_t>(y) * a.wpr + (x >> 5)], 1u << (x & 31));
+    atomicAdd(&rowcount[y], 1);
+  }
+}
+
+// ------------------------------------------------------------------- scan
+// Exclusive scan of the per-row survivor counts; one 1024-thread CTA per
+// stream, rows processed in chunks of 1024.
+__global__ void __launch_bounds__(1024) ccl_scan_kernel(CclArgs a) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  const int s = blockIdx.x;
+  int32_t* rc = a.rowcount + static_cast<int64_t>(s) * a.h;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < a.h; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < a.h ? rc[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int ws = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += y;
+      }
+      warp_sums[lane] = ws;
+    }
+    __syncthreads();
+    const int incl = x + (wid > 0 ? warp_sums[wid - 1] : 0) + carry;
+    if (i < a.h) rc[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.nblobs[s] = carry;
+}
+
+// ----------------------------------------------------------------- assign
+__global__ void __launch_bounds__(256) ccl_assign_kernel(CclArgs a) {
+  const int s = blockIdx.y;
+  const int n = a.nslots[s];
+  SlotTable t = slot_base(a, s);
+  const int32_t* rowpre = a.rowcount + static_cast<int64_t>(s) * a.h;
+  const uint32_t* bitmap = a.bitmap + static_cast<int64_t>(s) * a.h * a.wpr;
+  trb_blob* blobs = a.blobs + static_cast<int64_t>(s) * a.blob_cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = t.root[i];
+    const int area = t.area[r];
+    if (area < a.min_area) {
+      t.dense[i] = 0;
+      continue;
+    }
+    const int pos = t.minpix[r];
+    const int y = pos / a.w, x = pos - y * a.w;
+    const uint32_t* row = bitmap + static_cast<int64_t>(y) * a.wpr;
+    int rank = rowpre[y];
+    for (int k = 0; k < (x >> 5); ++k) rank += __popc(row[k]);
+    rank += __popc(row[x >> 5] & ((1u << (x & 31)) - 1u));
+    const int label = rank + 1;
+    t.dense[i] = label;
+    if (r != i) continue;
+    trb_blob b;
+    b.label = label;
+    b.area = area;
+    b.x_min = t.x0[r];
+    b.y_min = t.y0[r];
+    b.x_max = t.x1[r];
+    b.y_max = t.y1[r];
+    // exact: integer sums < 2^53 converted to double, one IEEE division
+    // (segmentation.hpp:139-147 accumulates the same integers in a double)
+    b.cx = static_cast<double>(t.sx[r]) / static_cast<double>(area);
+    b.cy = static_cast<double>(t.sy[r]) / static_cast<double>(area);
+    blobs[rank] = b;
+  }
+}
+
+// ------------------------------------------------------------------ final
+__global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a, int vec_ok) {
+  const int s = blockIdx.y;
+  const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
+  const int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
+  int32_t* labels = a.labels + static_cast<int64_t>(s) * a.px;
+  const int32_t* dense = a.slots.dense + static_cast<int64_t>(s) * a.slot_cap;
+  const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
+  if (p0 >= a.px) return;
+  if (vec_ok && p0 + 16 <= a.px) {
+    const uint4 mq = *reinterpret_cast<const uint4*>(mask + p0);
+    const uint8_t* m = reinterpret_cast<const uint8_t*>(&mq);
+    int4 out[4];
+    int* o = reinterpret_cast<int*>(out);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = m[i] ? dense[labg[p0 + i]] : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) __stcs(reinterpret_cast<int4*>(labels + p0) + j, out[j]);
+  } else {
+    const int64_t p1 = min(p0 + 16, a.px);
+    for (int64_t p = p0; p < p1; ++p) labels[p] = mask[p] ? dense[labg[p]] : 0;
+  }
+}
+
+int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
+  const int64_t n_tiles = static_cast<int64_t>(a.tiles_x) * a.tiles_y;
+  // per-frame resets: slot counters, row counts and survivor bitmap
+  TRB_CUDA(cudaMemsetAsync(a.nslots, 0, sizeof(int32_t) * S, st));
+  TRB_CUDA(cudaMemsetAsync(a.rowcount, 0, sizeof(int32_t) * static_cast<size_t>(a.h) * S, st));
+  TRB_CUDA(cudaMemsetAsync(a.bitmap, 0, sizeof(uint32_t) * static_cast<size_t>(a.h) * a.wpr * S, st));
+  ccl_local_kernel<<<dim3(a.tiles_x, a.tiles_y, S), 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_local_kernel");
+  ccl_merge_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 64, 256)), S), 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_merge_kernel");
+  // slot kernels: enough CTAs to cover a typical frame, grid-stride beyond
+  const unsigned slot_blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div64(a.slot_cap, 256), 64));
+  ccl_resolve_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_resolve_kernel");
+  ccl_mark_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_mark_kernel");
+  ccl_scan_kernel<<<S, 1024, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_scan_kernel");
+  ccl_assign_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("ccl_assign_kernel");
+  const int vec_ok = (a.px % 16 == 0);
+  ccl_final_kernel<<<dim3(static_cast<unsigned>(ceil_div64(ceil_div64(a.px, 16), 256)), S), 256, 0, st>>>(a, vec_ok);
+  TRB_LAUNCH_CHECK("ccl_final_kernel");
+  return 7;
+}
+
+}  // namespace trb

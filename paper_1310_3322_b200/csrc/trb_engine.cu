@@ -1,0 +1,253 @@
+// trb_engine.cu — host state machines (see trb_engine.cuh).
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "trb_engine.cuh"
+#include "trb_track.cuh"
+
+namespace trb {
+
+// ---------------------------------------------------------------- validate
+// MotionConfig::validate (motion.hpp:51-55); morph is this build's extension.
+void validate_motion(const trb_motion_config& c) {
+  if (c.window < 2) throw Error(TRB_CONFIG_ERROR, "motion window_w must be >= 2");
+  if (c.threshold <= 0 || c.threshold >= 255) throw Error(TRB_CONFIG_ERROR, "motion threshold must be in (0,255)");
+  if (c.bins < 2 || c.bins > 256) throw Error(TRB_CONFIG_ERROR, "motion histogram_bins must be in [2,256]");
+  if (c.method != TRB_BG_MEAN && c.method != TRB_BG_MODE)
+    throw Error(TRB_INVALID_ARGUMENT, "unknown background method (expected mean|mode)");
+  if (c.morph < TRB_MORPH_NONE || c.morph > TRB_MORPH_CLOSE)
+    throw Error(TRB_CONFIG_ERROR, "motion morph must be none|erode|dilate|open|close");
+}
+
+// block_grid (segmentation.hpp:79-84): most-square factorisation.
+static std::pair<int, int> block_grid(int n) {
+  int rows = 1;
+  for (int r = 1; r * r <= n; ++r)
+    if (n % r == 0) rows = r;
+  return {rows, n / rows};
+}
+
+// SegmentationConfig::validate (segmentation.hpp:30-33) + label_blocked's
+// grid check (segmentation.hpp:201-205).
+void validate_seg(const trb_seg_config& c, int w, int h) {
+  if (c.n_blocks < 1) throw Error(TRB_CONFIG_ERROR, "n_blocks must be >= 1");
+  if (c.min_area < 1) throw Error(TRB_CONFIG_ERROR, "min_area must be >= 1");
+  if (c.connectivity != TRB_CONN_FOUR && c.connectivity != TRB_CONN_EIGHT)
+    throw Error(TRB_INVALID_ARGUMENT, "unknown connectivity (expected four|eight)");
+  if (w < 1 || h < 1) return;
+  const auto [rows, cols] = block_grid(c.n_blocks);
+  if (rows > h || cols > w)
+    throw Error(TRB_CONFIG_ERROR, "n_blocks=" + std::to_string(c.n_blocks) + " does not tile a " + std::to_string(w) +
+                                      "x" + std::to_string(h) + " image (grid " + std::to_string(rows) + "x" +
+                                      std::to_string(cols) + ")");
+}
+
+// TrackerConfig::validate (tracking.hpp:28-33)
+void validate_tracker(const trb_tracker_config& c) {
+  if (c.k_clusters < 2) throw Error(TRB_CONFIG_ERROR, "tracker k_clusters must be >= 2");
+  if (!(c.eps > 0.0)) throw Error(TRB_CONFIG_ERROR, "tracker eps must be > 0");
+  if (c.max_iters < 1) throw Error(TRB_CONFIG_ERROR, "tracker max_iters must be >= 1");
+  if (c.kmeans_iters < 1) throw Error(TRB_CONFIG_ERROR, "tracker kmeans_iters must be >= 1");
+}
+
+// ------------------------------------------------------------------ motion
+MotionState::MotionState(const trb_motion_config& cfg, int S, int w, int h, int ch)
+    : cfg_(cfg), S_(S), w_(w), h_(h), ch_(ch) {
+  validate_motion(cfg);
+  if (w < 1 || h < 1) throw Error(TRB_INVALID_ARGUMENT, "motion detector needs positive frame dimensions");
+  px_ = static_cast<int64_t>(w) * h;
+  wide_ = cfg.window > 257;  // 255*257 < 2^16
+  ring_.alloc(static_cast<size_t>(px_) * cfg.window * S);
+  sums_.alloc(static_cast<size_t>(px_) * S * (wide_ ? 4 : 2));
+}
+
+bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st,
+                       int* launches) {
+  const int W = cfg_.window;
+  MotionArgs a{};
+  a.frames = frames_dev;
+  a.ring = ring_.as<uint8_t>();
+  a.ring_stride = px_ * W;
+  a.sums = sums_.p;
+  a.mask = mask;
+  a.px = px_;
+  a.slot = frames_seen_ % W;
+  a.full_before = frames_seen_ >= W;
+  a.emit = frames_seen_ + 1 >= W;
+  a.threshold = cfg_.threshold;
+  a.W = static_cast<uint32_t>(W);
+  a.div = FastDiv::make(2u * static_cast<uint32_t>(W));
+  a.vec_ok = (px_ % 16 == 0);
+  if (cfg_.method == TRB_BG_MEAN) {
+    launch_motion_mean(a, ch_, wide_, S_, st);
+    ++*launches;
+  } else {
+    launch_ring_update(a, ch_, wide_, S_, st);
+    ++*launches;
+    if (a.emit) {
+      ModeArgs m{};
+      m.ring = ring_.as<uint8_t>();
+      m.ring_stride = px_ * W;
+      m.px = px_;
+      m.W = W;
+      m.bins = cfg_.bins;
+      m.threshold = cfg_.threshold;
+      m.newest = a.slot;
+      m.mask = mask;
+      launch_motion_mode(m, S_, st);
+      ++*launches;
+    }
+  }
+  ++frames_seen_;
+  if (!a.emit) return false;
+  if (cfg_.morph != TRB_MORPH_NONE) *launches += launch_morph(mask, tmp, w_, h_, S_, cfg_.morph, st);
+  return true;
+}
+
+void MotionState::background(uint8_t* out_dev, cudaStream_t st) {
+  if (frames_seen_ < cfg_.window)
+    throw Error(TRB_INVALID_ARGUMENT, "background not available before the window fills");
+  if (cfg_.method == TRB_BG_MEAN) {
+    launch_mean_background(sums_.p, px_, cfg_.window, wide_, out_dev, st);
+  } else {
+    ModeArgs m{};
+    m.ring = ring_.as<uint8_t>();
+    m.ring_stride = px_ * cfg_.window;
+    m.px = px_;
+    m.W = cfg_.window;
+    m.bins = cfg_.bins;
+    m.threshold = cfg_.threshold;
+    m.bg_out = out_dev;
+    launch_motion_mode(m, 1, st);
+  }
+}
+
+// --------------------------------------------------------------------- CCL
+CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w), h_(h) {
+  validate_seg(cfg, w, h);
+  px_ = static_cast<int64_t>(w) * h;
+  const int tx = ceil_div(w, kTileW), ty = ceil_div(h, kTileH);
+  slot_cap_ = static_cast<int64_t>(tx) * ty * kMaxTileComps;
+  blob_cap_ = px_ / 2 + 1;
+  const int wpr = ceil_div(w, 32);
+  labg_.alloc(sizeof(int32_t) * px_ * S, false);
+  labels_.alloc(sizeof(int32_t) * px_ * S);
+  // 11 per-slot arrays: 9 x int32 + 2 x u64
+  slots_.alloc(static_cast<size_t>(slot_cap_) * S * (9 * 4 + 2 * 8), false);
+  nslots_.alloc(sizeof(int32_t) * S);
+  rowcount_.alloc(sizeof(int32_t) * h * S);
+  bitmap_.alloc(sizeof(uint32_t) * static_cast<size_t>(h) * wpr * S);
+  blobs_.alloc(sizeof(trb_blob) * blob_cap_ * S, false);
+  nblobs_.alloc(sizeof(int32_t) * S);
+
+  CclArgs& a = args_;
+  a.labg = labg_.as<int32_t>();
+  a.labels = labels_.as<int32_t>();
+  a.w = w;
+  a.h = h;
+  a.px = px_;
+  a.conn = cfg.connectivity;
+  a.min_area = cfg.min_area;
+  a.tiles_x = tx;
+  a.tiles_y = ty;
+  const size_t n = static_cast<size_t>(slot_cap_) * S;
+  char* base = slots_.as<char>();
+  // u64 arrays first for alignment
+  a.slots.sx = reinterpret_cast<unsigned long long*>(base);
+  a.slots.sy = a.slots.sx + n;
+  int32_t* i32 = reinterpret_cast<int32_t*>(a.slots.sy + n);
+  a.slots.parent = i32 + 0 * n;
+  a.slots.root = i32 + 1 * n;
+  a.slots.area = i32 + 2 * n;
+  a.slots.x0 = i32 + 3 * n;
+  a.slots.y0 = i32 + 4 * n;
+  a.slots.x1 = i32 + 5 * n;
+  a.slots.y1 = i32 + 6 * n;
+  a.slots.minpix = i32 + 7 * n;
+  a.slots.dense = i32 + 8 * n;
+  a.slot_cap = slot_cap_;
+  a.nslots = nslots_.as<int32_t>();
+  a.rowcount = rowcount_.as<int32_t>();
+  a.bitmap = bitmap_.as<uint32_t>();
+  a.wpr = wpr;
+  a.blobs = blobs_.as<trb_blob>();
+  a.blob_cap = blob_cap_;
+  a.nblobs = nblobs_.as<int32_t>();
+}
+
+void CclState::run(const uint8_t* mask, cudaStream_t st, int* launches) {
+  args_.mask = mask;
+  *launches += launch_ccl(args_, S_, st);
+}
+
+// ----------------------------------------------------------------- streams
+Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const trb_seg_config& sc,
+                 const trb_tracker_config& tc, bool with_tracker)
+    : S_(S), w_(w), h_(h), ch_(ch), mc_(mc) {
+  if (S < 1) throw Error(TRB_INVALID_ARGUMENT, "need at least one stream");
+  if (ch != 1 && ch != 3) throw Error(TRB_INVALID_ARGUMENT, "frame channels must be 1 or 3");
+  if (w < 1 || h < 1) throw Error(TRB_INVALID_ARGUMENT, "frame dimensions must be >= 1");
+  if (with_tracker) validate_tracker(tc);
+  px_ = static_cast<int64_t>(w) * h;
+  motion_ = std::make_unique<MotionState>(mc, S, w, h, ch);
+  ccl_ = std::make_unique<CclState>(S, w, h, sc);
+  if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S);
+  mask_.alloc(static_cast<size_t>(px_) * S);
+  if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S);
+  frame_ptrs_.alloc(sizeof(void*) * S);
+  ptrs_host_.alloc(sizeof(void*) * S);
+  TRB_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
+}
+
+Streams::~Streams() {
+  if (own_) cudaStreamDestroy(own_);
+}
+
+void Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st) {
+  int launches = 0;
+  const bool emitted = motion_->push(frames_dev, mask_.as<uint8_t>(), mask_tmp_.as<uint8_t>(), st, &launches);
+  if (emitted) {
+    ccl_->run(mask_.as<uint8_t>(), st, &launches);
+    if (tracker_)
+      tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches);
+  }
+  has_output_ = emitted;
+  last_launches_ = launches;
+}
+
+void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
+  if (!st) st = own_;
+  // the kernels read the per-stream frame pointers from device memory
+  // (pinned staging must not be overwritten while a previous copy is in flight)
+  TRB_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(ptrs_host_.p, frames, sizeof(void*) * S_);
+  TRB_CUDA(cudaMemcpyAsync(frame_ptrs_.p, ptrs_host_.p, sizeof(void*) * S_, cudaMemcpyHostToDevice, st));
+  ptrs_staging_ = false;
+  run_(frame_ptrs_.as<const uint8_t* const>(), st);
+}
+
+void Streams::step_host(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
+  if (!st) st = own_;
+  const size_t fb = static_cast<size_t>(px_) * ch_;
+  if (!staging_.p) staging_.alloc(fb * S_, false);
+  if (!ptrs_staging_) {
+    TRB_CUDA(cudaStreamSynchronize(st));
+    ptrs_staging_ = true;
+    const uint8_t** hp = ptrs_host_.as<const uint8_t*>();
+    for (int s = 0; s < S_; ++s) hp[s] = staging_.as<uint8_t>() + fb * s;
+    TRB_CUDA(cudaMemcpyAsync(frame_ptrs_.p, ptrs_host_.p, sizeof(void*) * S_, cudaMemcpyHostToDevice, st));
+  }
+  for (int s = 0; s < S_; ++s)
+    TRB_CUDA(cudaMemcpyAsync(staging_.as<uint8_t>() + fb * s, frames[s], fb, cudaMemcpyHostToDevice, st));
+  run_(frame_ptrs_.as<const uint8_t* const>(), st);
+  if (result_host) {
+    if (has_output_)
+      TRB_CUDA(cudaMemcpyAsync(result_host, ccl_->nblobs(), sizeof(int32_t) * S_, cudaMemcpyDeviceToHost, st));
+    else
+      std::memset(result_host, 0, sizeof(int32_t) * S_);
+    TRB_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+}  // namespace trb

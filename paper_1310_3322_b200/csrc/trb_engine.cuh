@@ -1,0 +1,141 @@
+// trb_engine.cuh — host-side state machines over the kernels.  One object
+// per reference object: MotionState ~ MotionDetector (motion.hpp:149-212),
+// CclState ~ label_blocked's workspace (segmentation.hpp:198-264),
+// TrackerState ~ Tracker (tracking.hpp:170-241).  Each holds a batch of
+// S independent streams so one launch serves every stream of a GPU.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "trb_kernels.cuh"
+
+namespace trb {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t bytes, bool zero = true) {
+    if (bytes <= n && p) return;
+    release();
+    TRB_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    n = bytes;
+    if (zero) TRB_CUDA(cudaMemset(p, 0, bytes ? bytes : 16));
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t bytes) {
+    if (bytes <= n && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    TRB_CUDA(cudaMallocHost(&p, bytes ? bytes : 16));
+    n = bytes;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+void validate_motion(const trb_motion_config& c);
+void validate_seg(const trb_seg_config& c, int w, int h);
+void validate_tracker(const trb_tracker_config& c);
+
+class MotionState {
+ public:
+  MotionState(const trb_motion_config& cfg, int S, int w, int h, int ch);
+  // frames_dev: device array [S] of device frame pointers.  Writes the
+  // masks (device, S*px) when the window is full; returns true then.
+  bool push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st, int* launches);
+  void background(uint8_t* out_dev, cudaStream_t st);  // stream 0 only
+  int frames_seen() const { return frames_seen_; }
+  const trb_motion_config& cfg() const { return cfg_; }
+
+ private:
+  trb_motion_config cfg_;
+  int S_, w_, h_, ch_;
+  int64_t px_;
+  bool wide_;
+  int frames_seen_ = 0;
+  DevBuf ring_, sums_;
+};
+
+class CclState {
+ public:
+  CclState(int S, int w, int h, const trb_seg_config& cfg);
+  // mask: device [S][px].  Labels, blobs and counts stay on the device.
+  void run(const uint8_t* mask, cudaStream_t st, int* launches);
+  int32_t* labels() const { return labels_.as<int32_t>(); }
+  trb_blob* blobs() const { return blobs_.as<trb_blob>(); }
+  int32_t* nblobs() const { return nblobs_.as<int32_t>(); }
+  int64_t blob_cap() const { return blob_cap_; }
+  int64_t px() const { return px_; }
+
+ private:
+  CclArgs args_{};
+  int S_, w_, h_;
+  int64_t px_, slot_cap_, blob_cap_;
+  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_, nblobs_;
+};
+
+class TrackerState;  // trb_track.cu
+
+// The batched front end: motion -> morph -> CCL -> tracking for S streams.
+class Streams {
+ public:
+  Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const trb_seg_config& sc,
+          const trb_tracker_config& tc, bool with_tracker);
+  ~Streams();
+  void step_device(const uint8_t* const* frames_host_array_of_dev_ptrs, cudaStream_t st);
+  void step_host(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
+  cudaStream_t stream() const { return own_; }
+  int S() const { return S_; }
+  int w() const { return w_; }
+  int h() const { return h_; }
+  int ch() const { return ch_; }
+  int64_t px() const { return px_; }
+  int frames_seen() const { return motion_->frames_seen(); }
+  bool has_output() const { return has_output_; }
+  int last_launches() const { return last_launches_; }
+  uint8_t* mask(int s) const { return mask_.as<uint8_t>() + px_ * s; }
+  CclState& ccl() { return *ccl_; }
+  TrackerState* tracker() { return tracker_.get(); }
+
+ private:
+  void run_(const uint8_t* const* frames_dev, cudaStream_t st);
+  int S_, w_, h_, ch_;
+  int64_t px_;
+  trb_motion_config mc_;
+  std::unique_ptr<MotionState> motion_;
+  std::unique_ptr<CclState> ccl_;
+  std::unique_ptr<TrackerState> tracker_;
+  DevBuf mask_, mask_tmp_, frame_ptrs_, staging_;
+  PinnedBuf ptrs_host_;
+  cudaStream_t own_ = nullptr;
+  bool has_output_ = false;
+  bool ptrs_staging_ = false;
+  int last_launches_ = 0;
+};
+
+}  // namespace trb

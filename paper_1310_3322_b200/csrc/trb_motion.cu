@@ -1,0 +1,302 @@
+// trb_motion.cu — north-star kernel (1): fused background-model update,
+// frame differencing and thresholding; plus the Mode estimator, the 3x3
+// morphology stage (north-star (2)) and the synthetic-frame rasteriser.
+//
+// Reference: MotionDetector::push (motion.hpp:164-193), window_background
+// (motion.hpp:127-144), luma (frame.hpp:91-93).
+//
+// HBM layout (per stream, all frame-major so every access is a coalesced
+// 16-byte vector stream):
+//   ring  [W][px] u8   slot = frames_seen % W (the reference keeps the same
+//                      samples pixel-major, ring_[p*W+slot], motion.hpp:173)
+//   sums  [px]    u16 when W <= 257 (255*257 < 2^16), else u32
+//   mask  [px]    u8 0/1
+// Algorithmic bytes per pixel per frame (Mean, gray): frame 1 + evicted
+// sample 1 + new sample 1 + sum 2+2 + mask 1 = 8.
+#include "trb_kernels.cuh"
+
+namespace trb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t luma3(uint32_t r, uint32_t g, uint32_t b) {
+  return (77u * r + 150u * g + 29u * b + 128u) >> 8;  // frame.hpp:92
+}
+
+// Load 16 consecutive pixels of the input frame as gray bytes.
+template <int CH>
+__device__ __forceinline__ void load16(const uint8_t* __restrict__ f, int64_t p0, uint8_t (&v)[16]) {
+  if constexpr (CH == 1) {
+    const uint4 q = __ldcs(reinterpret_cast<const uint4*>(f + p0));
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = b[i];
+  } else {
+    uint4 q[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) q[j] = __ldcs(reinterpret_cast<const uint4*>(f + 3 * p0) + j);
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = static_cast<uint8_t>(luma3(b[3 * i], b[3 * i + 1], b[3 * i + 2]));
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ uint8_t load1(const uint8_t* __restrict__ f, int64_t p) {
+  if constexpr (CH == 1) return f[p];
+  return static_cast<uint8_t>(luma3(f[3 * p], f[3 * p + 1], f[3 * p + 2]));
+}
+
+__device__ __forceinline__ uint8_t thr_mask(uint32_t v, uint32_t bg, int thr) {
+  const int diff = static_cast<int>(v) - static_cast<int>(bg);
+  return (diff > thr || -diff > thr) ? 1 : 0;  // motion.hpp:189-190, strict
+}
+
+}  // namespace
+
+// One thread = 16 pixels.  grid.y = stream.
+template <int CH, typename SumT>
+__global__ void __launch_bounds__(256) motion_mean_kernel(MotionArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t* __restrict__ frame = a.frames[s];
+  uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * a.px;
+  SumT* __restrict__ sums = reinterpret_cast<SumT*>(a.sums) + static_cast<int64_t>(s) * a.px;
+  uint8_t* __restrict__ mask = a.mask + static_cast<int64_t>(s) * a.px;
+  const int64_t chunk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p0 = chunk * 16;
+  if (p0 >= a.px) return;
+  if (p0 + 16 <= a.px && a.vec_ok) {
+    uint8_t v[16];
+    load16<CH>(frame, p0, v);
+    uint4 old_q = make_uint4(0, 0, 0, 0);
+    if (a.full_before) old_q = __ldcs(reinterpret_cast<const uint4*>(ring + p0));
+    const uint8_t* old = reinterpret_cast<const uint8_t*>(&old_q);
+    uint4 new_q;
+    uint8_t* nb = reinterpret_cast<uint8_t*>(&new_q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) nb[i] = v[i];
+    __stcs(reinterpret_cast<uint4*>(ring + p0), new_q);
+    constexpr int kSumVec = 16 * sizeof(SumT) / 16;
+    uint4 sq[kSumVec];
+#pragma unroll
+    for (int j = 0; j < kSumVec; ++j) sq[j] = __ldcs(reinterpret_cast<const uint4*>(sums + p0) + j);
+    SumT* sv = reinterpret_cast<SumT*>(sq);
+    uint4 mq;
+    uint8_t* mb = reinterpret_cast<uint8_t*>(&mq);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t sum = static_cast<uint32_t>(sv[i]) - old[i] + v[i];
+      sv[i] = static_cast<SumT>(sum);
+      uint32_t bg;
+      if constexpr (sizeof(SumT) == 2) bg = a.div.div(2u * sum + a.W);
+      else bg = static_cast<uint32_t>((2ull * sum + a.W) / (2ull * a.W));
+      mb[i] = thr_mask(v[i], bg, a.threshold);
+    }
+#pragma unroll
+    for (int j = 0; j < kSumVec; ++j) __stcs(reinterpret_cast<uint4*>(sums + p0) + j, sq[j]);
+    if (a.emit) __stcs(reinterpret_cast<uint4*>(mask + p0), mq);
+  } else {
+    const int64_t p1 = min(p0 + 16, a.px);
+    for (int64_t p = p0; p < p1; ++p) {
+      const uint8_t v = load1<CH>(frame, p);
+      const uint8_t old = a.full_before ? ring[p] : 0;
+      ring[p] = v;
+      const uint32_t sum = static_cast<uint32_t>(sums[p]) - old + v;
+      sums[p] = static_cast<SumT>(sum);
+      if (a.emit) {
+        const uint32_t bg = static_cast<uint32_t>((2ull * sum + a.W) / (2ull * a.W));
+        mask[p] = thr_mask(v, bg, a.threshold);
+      }
+    }
+  }
+}
+
+// Mode estimator (window_background Mode path, motion.hpp:134-143): per
+// pixel histogram of the W ring samples into `bins` equal bins, most
+// populated bin (strict >, lower bin wins ties), rounded mean of that bin's
+// samples.  Per-thread bin counters live in shared memory ([bin][thread]
+// so lanes never conflict).  One thread = one pixel.
+__global__ void __launch_bounds__(64) motion_mode_kernel(ModeArgs a) {
+  extern __shared__ uint16_t counts[];  // [bins][64]
+  const int s = blockIdx.y;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint8_t* ring = a.ring + static_cast<int64_t>(s) * a.ring_stride;
+  const int t = threadIdx.x;
+  for (int b = 0; b < a.bins; ++b) counts[b * 64 + t] = 0;
+  if (p >= a.px) return;
+  for (int i = 0; i < a.W; ++i) {
+    const uint32_t v = ring[static_cast<int64_t>(i) * a.px + p];
+    counts[((v * a.bins) >> 8) * 64 + t] += 1;
+  }
+  int best = 0;
+  uint32_t bestc = counts[t];
+  for (int b = 1; b < a.bins; ++b) {
+    const uint32_t c = counts[b * 64 + t];
+    if (c > bestc) bestc = c, best = b;
+  }
+  uint64_t sum = 0, cnt = 0;
+  for (int i = 0; i < a.W; ++i) {
+    const uint32_t v = ring[static_cast<int64_t>(i) * a.px + p];
+    if (static_cast<int>((v * a.bins) >> 8) == best) sum += v, ++cnt;
+  }
+  const uint32_t bg = static_cast<uint32_t>((2 * sum + cnt) / (2 * cnt));
+  if (a.bg_out) {
+    a.bg_out[static_cast<int64_t>(s) * a.px + p] = static_cast<uint8_t>(bg);
+    return;
+  }
+  // the newest sample sits in slot a.newest
+  const uint32_t v = ring[static_cast<int64_t>(a.newest) * a.px + p];
+  a.mask[static_cast<int64_t>(s) * a.px + p] = thr_mask(v, bg, a.threshold);
+}
+
+// Ring update only (Mode path): write the new sample, keep the sums.
+template <int CH, typename SumT>
+__global__ void __launch_bounds__(256) ring_update_kernel(MotionArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t* __restrict__ frame = a.frames[s];
+  uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * a.px;
+  SumT* __restrict__ sums = reinterpret_cast<SumT*>(a.sums) + static_cast<int64_t>(s) * a.px;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= a.px) return;
+  const uint8_t v = load1<CH>(frame, p);
+  const uint8_t old = a.full_before ? ring[p] : 0;
+  ring[p] = v;
+  sums[p] = static_cast<SumT>(static_cast<uint32_t>(sums[p]) - old + v);
+}
+
+// Mean background image from the sums (MotionDetector::background, :196-203).
+template <typename SumT>
+__global__ void mean_background_kernel(const void* sums_v, int64_t px, int W, uint8_t* out) {
+  const SumT* sums = reinterpret_cast<const SumT*>(sums_v);
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= px) return;
+  out[p] = static_cast<uint8_t>((2ull * sums[p] + W) / (2ull * W));
+}
+
+// 3x3 binary erosion / dilation (north-star kernel (2); not in the
+// reference).  Out-of-image neighbours are ignored.  One CTA = 32x8 output
+// pixels; the (32+2)x(8+2) input tile with halo is staged in shared memory.
+__global__ void __launch_bounds__(256) morph3x3_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                      int w, int h, int64_t stride, int dilate) {
+  __shared__ uint8_t tile[10][34];
+  const int s = blockIdx.z;
+  in += static_cast<int64_t>(s) * stride;
+  out += static_cast<int64_t>(s) * stride;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const uint8_t pad = dilate ? 0 : 1;  // neutral element for ignored neighbours
+  for (int i = threadIdx.x; i < 10 * 34; i += blockDim.x) {
+    const int ty = i / 34, tx = i % 34;
+    const int gx = x0 + tx - 1, gy = y0 + ty - 1;
+    tile[ty][tx] = (gx >= 0 && gy >= 0 && gx < w && gy < h) ? (in[static_cast<int64_t>(gy) * w + gx] != 0) : pad;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int gx = x0 + tx, gy = y0 + ty;
+  if (gx >= w || gy >= h) return;
+  uint32_t acc = dilate ? 0u : 1u;
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const uint32_t v = tile[ty + dy][tx + dx];
+      acc = dilate ? (acc | v) : (acc & v);
+    }
+  out[static_cast<int64_t>(gy) * w + gx] = static_cast<uint8_t>(acc);
+}
+
+// Synthetic frame raster (synth.hpp:295-328): background fill, then every
+// shape's rectangle in order (later shapes overwrite earlier ones).
+__global__ void synth_raster_kernel(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects,
+                                    const uint8_t* colors, int n) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= static_cast<int64_t>(w) * h) return;
+  const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+  int hit = -1;
+  for (int k = 0; k < n; ++k) {
+    const int ix = rects[4 * k], iy = rects[4 * k + 1], rw = rects[4 * k + 2], rh = rects[4 * k + 3];
+    if (x >= ix && x < ix + rw && y >= iy && y < iy + rh) hit = k;
+  }
+  for (int c = 0; c < ch; ++c) out[p * ch + c] = hit < 0 ? bg : colors[3 * hit + c];
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st) {
+  const int64_t chunks = ceil_div64(a.px, 16);
+  dim3 grid(static_cast<unsigned>(ceil_div64(chunks, 256)), n_streams);
+  if (channels == 1) {
+    if (wide_sums) motion_mean_kernel<1, uint32_t><<<grid, 256, 0, st>>>(a);
+    else motion_mean_kernel<1, uint16_t><<<grid, 256, 0, st>>>(a);
+  } else {
+    if (wide_sums) motion_mean_kernel<3, uint32_t><<<grid, 256, 0, st>>>(a);
+    else motion_mean_kernel<3, uint16_t><<<grid, 256, 0, st>>>(a);
+  }
+  TRB_LAUNCH_CHECK("motion_mean_kernel");
+}
+
+void launch_ring_update(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div64(a.px, 256)), n_streams);
+  if (channels == 1) {
+    if (wide_sums) ring_update_kernel<1, uint32_t><<<grid, 256, 0, st>>>(a);
+    else ring_update_kernel<1, uint16_t><<<grid, 256, 0, st>>>(a);
+  } else {
+    if (wide_sums) ring_update_kernel<3, uint32_t><<<grid, 256, 0, st>>>(a);
+    else ring_update_kernel<3, uint16_t><<<grid, 256, 0, st>>>(a);
+  }
+  TRB_LAUNCH_CHECK("ring_update_kernel");
+}
+
+void launch_motion_mode(const ModeArgs& a, int n_streams, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div64(a.px, 64)), n_streams);
+  const size_t smem = static_cast<size_t>(a.bins) * 64 * sizeof(uint16_t);
+  motion_mode_kernel<<<grid, 64, smem, st>>>(a);
+  TRB_LAUNCH_CHECK("motion_mode_kernel");
+}
+
+void launch_mean_background(const void* sums, int64_t px, int W, bool wide_sums, uint8_t* out, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(ceil_div64(px, 256));
+  if (wide_sums) mean_background_kernel<uint32_t><<<grid, 256, 0, st>>>(sums, px, W, out);
+  else mean_background_kernel<uint16_t><<<grid, 256, 0, st>>>(sums, px, W, out);
+  TRB_LAUNCH_CHECK("mean_background_kernel");
+}
+
+int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int op, cudaStream_t st) {
+  if (op == TRB_MORPH_NONE) return 0;
+  const int64_t stride = static_cast<int64_t>(w) * h;
+  dim3 grid(ceil_div(w, 32), ceil_div(h, 8), n_streams);
+  auto pass = [&](const uint8_t* in, uint8_t* out, int dilate) {
+    morph3x3_kernel<<<grid, 256, 0, st>>>(in, out, w, h, stride, dilate);
+    TRB_LAUNCH_CHECK("morph3x3_kernel");
+  };
+  switch (op) {
+    case TRB_MORPH_ERODE:
+      pass(mask, tmp, 0);
+      break;
+    case TRB_MORPH_DILATE:
+      pass(mask, tmp, 1);
+      break;
+    case TRB_MORPH_OPEN:
+      pass(mask, tmp, 0);
+      pass(tmp, mask, 1);
+      return 2;  // result back in mask
+    case TRB_MORPH_CLOSE:
+      pass(mask, tmp, 1);
+      pass(tmp, mask, 0);
+      return 2;
+    default:
+      throw Error(TRB_CONFIG_ERROR, "unknown morphology op");
+  }
+  TRB_CUDA(cudaMemcpyAsync(mask, tmp, static_cast<size_t>(stride) * n_streams, cudaMemcpyDeviceToDevice, st));
+  return 1;
+}
+
+void launch_synth_raster(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects, const uint8_t* colors,
+                         int n, cudaStream_t st) {
+  const int64_t px = static_cast<int64_t>(w) * h;
+  synth_raster_kernel<<<static_cast<unsigned>(ceil_div64(px, 256)), 256, 0, st>>>(out, w, h, ch, bg, rects, colors,
+                                                                                 n);
+  TRB_LAUNCH_CHECK("synth_raster_kernel");
+}
+
+}  // namespace trb

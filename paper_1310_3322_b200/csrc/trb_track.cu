@@ -1,0 +1,956 @@
+// trb_track.cu — tracker kernels (see trb_track.cuh for the layout).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "trb_track.cuh"
+
+namespace trb {
+
+namespace {
+
+constexpr int NT = kOsumThreads;
+
+// Exact u32 division by a runtime divisor (Granlund-Montgomery): used to
+// turn a raster element index into (x, y) inside a window.
+struct UDiv32 {
+  uint32_t m;
+  int sh1, sh2;
+  __device__ static UDiv32 make(uint32_t d) {
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    UDiv32 r;
+    r.m = static_cast<uint32_t>(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    r.sh1 = l > 0 ? 1 : 0;
+    r.sh2 = l > 0 ? l - 1 : 0;
+    return r;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> sh1)) >> sh2;
+  }
+};
+
+struct Win {
+  int x0, y0, x1, y1;
+  __device__ bool empty() const { return x0 >= x1 || y0 >= y1; }
+};
+
+// clip_window, tracking.hpp:61-66
+__device__ __forceinline__ Win clip_window(int fw, int fh, double cx, double cy, int w, int h) {
+  const int x0 = static_cast<int>(xlround(cx)) - w / 2;
+  const int y0 = static_cast<int>(xlround(cy)) - h / 2;
+  return Win{max(0, x0), max(0, y0), min(fw, x0 + w), min(fh, y0 + h)};
+}
+
+// ColorQuantizer::assign, quantize.hpp:20-29 (strict <, lowest index wins)
+__device__ __forceinline__ int q_assign(const double* c, int k, double r, double g, double b) {
+  int best = 0;
+  double best_d = __longlong_as_double(0x7ff0000000000000LL);
+  for (int i = 0; i < k; ++i) {
+    const double dr = xsub(r, c[3 * i]), dg = xsub(g, c[3 * i + 1]), db = xsub(b, c[3 * i + 2]);
+    const double d = xadd(xadd(xmul(dr, dr), xmul(dg, dg)), xmul(db, db));
+    if (d < best_d) best_d = d, best = i;
+  }
+  return best;
+}
+
+// Everything one CTA needs to walk a window of one frame.
+struct WinCtx {
+  const uint8_t* frame;
+  int fw, fh, ch;
+  int x0, y0, ww, wh;
+  UDiv32 dv;
+  const double* ux2;  // [ww] ((x-cx)/hx)^2
+  const double* uy2;  // [wh]
+  const double* centers;
+  const uint8_t* lut;  // gray -> bin, or nullptr
+  int K;
+  __device__ __forceinline__ int bin_at(int x, int y) const {
+    if (ch == 1) {
+      const int v = frame[static_cast<int64_t>(y) * fw + x];
+      if (lut) return lut[v];
+      const double dv_ = v;
+      return q_assign(centers, K, dv_, dv_, dv_);
+    }
+    const uint8_t* p = frame + (static_cast<int64_t>(y) * fw + x) * 3;
+    return q_assign(centers, K, p[0], p[1], p[2]);
+  }
+};
+
+// histogram_opt's loop body (tracking.hpp:86-98): element j of the window
+// feeds hist[bin] and total with the Epanechnikov (or uniform) weight.
+struct HistContrib {
+  WinCtx c;
+  int epan;
+  template <class F>
+  __device__ __forceinline__ void operator()(int j, F&& emit) const {
+    const int yy = static_cast<int>(c.dv.div(static_cast<uint32_t>(j)));
+    const int xx = j - yy * c.ww;
+    double wgt = 1.0;
+    if (epan) {
+      const double t = xsub(1.0, xadd(c.ux2[xx], c.uy2[yy]));
+      wgt = (0.0 < t) ? t : 0.0;  // std::max(0.0, t)
+    }
+    if (wgt <= 0.0) return;
+    const int b = c.bin_at(c.x0 + xx, c.y0 + yy);
+    emit(b, wgt);
+    emit(c.K, wgt);
+  }
+};
+
+// meanshift_step's centroid body (tracking.hpp:136-146).
+struct MsContrib {
+  WinCtx c;
+  const double* wsq;  // sqrt(q[b]/p[b]), or < 0 when p[b] <= 0
+  template <class F>
+  __device__ __forceinline__ void operator()(int j, F&& emit) const {
+    const int yy = static_cast<int>(c.dv.div(static_cast<uint32_t>(j)));
+    const int xx = j - yy * c.ww;
+    const int x = c.x0 + xx, y = c.y0 + yy;
+    const double w = wsq[c.bin_at(x, y)];
+    if (w < 0.0) return;
+    emit(0, w);
+    emit(1, xmul(w, static_cast<double>(x)));
+    emit(2, xmul(w, static_cast<double>(y)));
+  }
+};
+
+// Shared-memory map for the tracker CTAs (dynamic).
+struct TrackSmem {
+  OsumSmem os;
+  double* ux2;   // [W]
+  double* uy2;   // [H]
+  double* cen;   // [K*3]
+  double* old;   // [K*3]
+  double* q;     // [K]
+  double* p;     // [K]
+  double* wsq;   // [K]
+  uint8_t* lut;  // [256]
+  double* scal;  // [16] broadcast scalars
+  int* iscal;    // [16]
+  long long* red;  // [NT] reduction scratch (int64 / doubles reinterpret)
+  static size_t bytes(int K, int W, int H) {
+    size_t b = OsumSmem::bytes(K + 1, NT);
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(double) * (W + H + 6 * K + 16) + 256 + sizeof(int) * 16 + sizeof(long long) * 2 * NT + 64;
+    return b;
+  }
+  __device__ void carve(void* base, int K, int W, int H) {
+    os.carve(base, K + 1, NT);
+    size_t off = (OsumSmem::bytes(K + 1, NT) + 15) & ~size_t(15);
+    char* p_ = static_cast<char*>(base) + off;
+    auto take = [&](size_t n) {
+      char* r = p_;
+      p_ += (n + 15) & ~size_t(15);
+      return r;
+    };
+    ux2 = reinterpret_cast<double*>(take(sizeof(double) * W));
+    uy2 = reinterpret_cast<double*>(take(sizeof(double) * H));
+    cen = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
+    old = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
+    q = reinterpret_cast<double*>(take(sizeof(double) * K));
+    p = reinterpret_cast<double*>(take(sizeof(double) * K));
+    wsq = reinterpret_cast<double*>(take(sizeof(double) * K));
+    scal = reinterpret_cast<double*>(take(sizeof(double) * 16));
+    red = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * NT));
+    iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
+    lut = reinterpret_cast<uint8_t*>(take(256));
+  }
+};
+
+// Fill ux2/uy2 for window r around (cx, cy) with half-sizes w/2.0, h/2.0:
+// ux = (x - cx) / hx; ux*ux  (tracking.hpp:84-91, same operations).
+__device__ void fill_u2(TrackSmem& sm, const Win& r, double cx, double cy, int w, int h) {
+  const double hx = static_cast<double>(w) / 2.0, hy = static_cast<double>(h) / 2.0;
+  for (int i = threadIdx.x; i < r.x1 - r.x0; i += blockDim.x) {
+    const double ux = xdiv(xsub(static_cast<double>(r.x0 + i), cx), hx);
+    sm.ux2[i] = xmul(ux, ux);
+  }
+  for (int i = threadIdx.x; i < r.y1 - r.y0; i += blockDim.x) {
+    const double uy = xdiv(xsub(static_cast<double>(r.y0 + i), cy), hy);
+    sm.uy2[i] = xmul(uy, uy);
+  }
+}
+
+__device__ WinCtx make_ctx(const uint8_t* frame, int fw, int fh, int ch, const Win& r, TrackSmem& sm, int K,
+                           bool use_lut) {
+  WinCtx c;
+  c.frame = frame;
+  c.fw = fw, c.fh = fh, c.ch = ch;
+  c.x0 = r.x0, c.y0 = r.y0, c.ww = r.x1 - r.x0, c.wh = r.y1 - r.y0;
+  c.dv = UDiv32::make(static_cast<uint32_t>(c.ww));
+  c.ux2 = sm.ux2, c.uy2 = sm.uy2;
+  c.centers = sm.cen;
+  c.lut = use_lut ? sm.lut : nullptr;
+  c.K = K;
+  return c;
+}
+
+// histogram_opt (tracking.hpp:79-102) with the quantizer in sm.cen (and
+// sm.lut when use_lut).  Writes the normalised histogram to out[K];
+// returns false for std::nullopt.  Block-uniform.
+__device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, double cx, double cy, int w, int h,
+                                 int K, int epan, bool use_lut, TrackSmem& sm, OsumBp* bp, double* out) {
+  const Win r = clip_window(fw, fh, cx, cy, w, h);
+  if (r.empty()) return false;
+  fill_u2(sm, r, cx, cy, w, h);
+  __syncthreads();
+  HistContrib hc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), epan};
+  ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), K + 1, hc, sm.os, bp);
+  const double total = sm.os.result[K];
+  if (total <= 0.0) return false;
+  for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os.result[b], total);
+  __syncthreads();
+  return true;
+}
+
+// meanshift_step (tracking.hpp:125-157) on the track whose model sits in
+// sm.cen / sm.q (and sm.lut).  cx, cy, status updated in place (uniform).
+__device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, double& cx, double& cy, int w, int h,
+                                 int& status, int K, int max_iters, double eps, bool use_lut, TrackSmem& sm,
+                                 OsumBp* bp) {
+  if (status != TRB_TRACK_ACTIVE) return;
+  for (int it = 0; it < max_iters; ++it) {
+    const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, bp, sm.p);
+    if (threadIdx.x == 0) {
+      int lost = !ok;
+      if (ok) {
+        double bc = 0.0;  // bhattacharyya, tracking.hpp:114-119
+        for (int i = 0; i < K; ++i) bc = xadd(bc, xsqrt(xmul(sm.p[i], sm.q[i])));
+        lost = !(bc > 0.0);
+        for (int b = 0; b < K; ++b) sm.wsq[b] = sm.p[b] <= 0.0 ? -1.0 : xsqrt(xdiv(sm.q[b], sm.p[b]));
+      }
+      sm.iscal[0] = lost;
+    }
+    __syncthreads();
+    if (sm.iscal[0]) {
+      status = TRB_TRACK_LOST;
+      return;
+    }
+    const Win r = clip_window(fw, fh, cx, cy, w, h);
+    MsContrib mc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), sm.wsq};
+    ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), 3, mc, sm.os, bp);
+    const double sw = sm.os.result[0], sx = sm.os.result[1], sy = sm.os.result[2];
+    __syncthreads();
+    if (sw <= 0.0) {
+      status = TRB_TRACK_LOST;
+      return;
+    }
+    const double nx = xdiv(sx, sw), ny = xdiv(sy, sw);
+    const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
+    cx = nx;
+    cy = ny;
+    if (shift < eps) break;
+  }
+}
+
+// ------------------------------------------------------------- k-means
+// Integer-valued RGB samples; the window of a frame or an explicit list.
+struct FrameWindowSrc {
+  const uint8_t* frame;
+  int fw, ch, x0, y0, ww;
+  UDiv32 dv;
+  __device__ __forceinline__ void get(int i, int& r, int& g, int& b) const {
+    const int yy = static_cast<int>(dv.div(static_cast<uint32_t>(i)));
+    const int x = x0 + (i - yy * ww), y = y0 + yy;
+    if (ch == 1) {
+      r = g = b = frame[static_cast<int64_t>(y) * fw + x];
+    } else {
+      const uint8_t* p = frame + (static_cast<int64_t>(y) * fw + x) * 3;
+      r = p[0], g = p[1], b = p[2];
+    }
+  }
+};
+
+struct ListSrc {
+  const int* px;  // n*3 ints
+  __device__ __forceinline__ void get(int i, int& r, int& g, int& b) const {
+    r = px[3 * i], g = px[3 * i + 1], b = px[3 * i + 2];
+  }
+};
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
+  const int t = threadIdx.x;
+  red[t] = v;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (t < o) red[t] += red[t + o];
+    __syncthreads();
+  }
+  const long long r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// exclusive scan of one int64 per thread (Hillis-Steele in shared memory)
+__device__ __forceinline__ long long block_exscan_ll(long long v, long long* red) {
+  const int t = threadIdx.x;
+  red[t] = v;
+  __syncthreads();
+  for (int o = 1; o < blockDim.x; o <<= 1) {
+    const long long y = t >= o ? red[t - o] : 0;
+    __syncthreads();
+    red[t] += y;
+    __syncthreads();
+  }
+  const long long r = red[t] - v;
+  __syncthreads();
+  return r;
+}
+
+// quantize_colors (quantize.hpp:43-118).  Samples are integer-valued, so
+// the k-means++ D^2 weights, their total and prefix sums are exact
+// integers (no ordering issue); Lloyd sums are exact integers; the
+// assignment distances use non-contracted fp64 like the reference.
+// Result centres in sm.cen.  mt19937_64 draws happen on thread 0.
+template <class Src>
+__device__ void kmeans_device(const Src& src, int n, int K, int iters, uint64_t seed, TrackSmem& sm, Mt64* rng) {
+  const int t = threadIdx.x;
+  const int C = (n + NT - 1) / NT;
+  const int j0 = min(n, t * C), j1 = min(n, j0 + C);
+  double* cen = sm.cen;
+  if (t == 0) {
+    rng->seed(seed);
+    const int64_t first = rng->uniform_int(0, static_cast<int64_t>(n) - 1);
+    int r, g, b;
+    src.get(static_cast<int>(first), r, g, b);
+    cen[0] = r, cen[1] = g, cen[2] = b;
+  }
+  __syncthreads();
+  for (int nc = 1; nc < K; ++nc) {
+    // D^2 of every sample to its nearest seed (exact integers)
+    long long local = 0;
+    for (int i = j0; i < j1; ++i) {
+      int r, g, b;
+      src.get(i, r, g, b);
+      int best = INT_MAX;
+      for (int c = 0; c < nc; ++c) {
+        const int dr = r - static_cast<int>(cen[3 * c]), dg = g - static_cast<int>(cen[3 * c + 1]),
+                  db = b - static_cast<int>(cen[3 * c + 2]);
+        best = min(best, dr * dr + dg * dg + db * db);
+      }
+      local += best;
+    }
+    const long long pre = block_exscan_ll(local, sm.red);
+    const long long total = block_sum_ll(local, sm.red);
+    if (t == 0) {
+      sm.iscal[1] = n - 1;  // pick when no prefix exceeds r
+      if (total > 0) sm.scal[0] = xmul(rng->uniform(), static_cast<double>(total));
+      else sm.iscal[1] = 0;
+    }
+    __syncthreads();
+    if (total > 0) {
+      const double r = sm.scal[0];
+      // the chunk holding the first prefix > r
+      if (static_cast<double>(pre + local) > r && (t == 0 || !(static_cast<double>(pre) > r))) {
+        long long acc = pre;
+        for (int i = j0; i < j1; ++i) {
+          int rr, g, b;
+          src.get(i, rr, g, b);
+          int best = INT_MAX;
+          for (int c = 0; c < nc; ++c) {
+            const int dr = rr - static_cast<int>(cen[3 * c]), dg = g - static_cast<int>(cen[3 * c + 1]),
+                      db = b - static_cast<int>(cen[3 * c + 2]);
+            best = min(best, dr * dr + dg * dg + db * db);
+          }
+          acc += best;
+          if (static_cast<double>(acc) > r) {
+            sm.iscal[1] = i;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      int r, g, b;
+      src.get(sm.iscal[1], r, g, b);
+      cen[3 * nc] = r, cen[3 * nc + 1] = g, cen[3 * nc + 2] = b;
+    }
+    __syncthreads();
+  }
+  // Lloyd iterations
+  long long* cnt = sm.red;           // [K]
+  long long* sum = sm.red + K;       // [3K]  (needs 4K <= 2*NT)
+  double* old = sm.old;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = t; i < 3 * K; i += NT) old[i] = cen[i];
+    for (int i = t; i < 4 * K; i += NT) sm.red[i] = 0;
+    __syncthreads();
+    for (int i = j0; i < j1; ++i) {
+      int r, g, b;
+      src.get(i, r, g, b);
+      const int a = q_assign(old, K, r, g, b);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[a]), 1ull);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a]), static_cast<unsigned long long>(r));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a + 1]), static_cast<unsigned long long>(g));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a + 2]), static_cast<unsigned long long>(b));
+    }
+    __syncthreads();
+    if (t == 0) sm.iscal[2] = 0;  // moved
+    __syncthreads();
+    for (int c = 0; c < K; ++c) {
+      double nc3[3];
+      if (cnt[c] == 0) {
+        // farthest sample from its (old-assignment) centre, current centres,
+        // lowest index on ties (quantize.hpp:99-107)
+        double bd = -1.0;
+        int bi = 0;
+        for (int i = j0; i < j1; ++i) {
+          int r, g, b;
+          src.get(i, r, g, b);
+          const int a = q_assign(old, K, r, g, b);
+          const double dr = xsub(r, cen[3 * a]), dg = xsub(g, cen[3 * a + 1]), db = xsub(b, cen[3 * a + 2]);
+          const double d = xadd(xadd(xmul(dr, dr), xmul(dg, dg)), xmul(db, db));
+          if (d > bd) bd = d, bi = i;
+        }
+        // block argmax (max d, then min index); chunks are in index order
+        __shared__ double w_d[NT];
+        __shared__ int w_i[NT];
+        w_d[t] = (j0 < j1) ? bd : -2.0;
+        w_i[t] = bi;
+        __syncthreads();
+        for (int o = NT / 2; o > 0; o >>= 1) {
+          if (t < o) {
+            const double d2 = w_d[t + o];
+            const int i2 = w_i[t + o];
+            if (d2 > w_d[t] || (d2 == w_d[t] && i2 < w_i[t])) w_d[t] = d2, w_i[t] = i2;
+          }
+          __syncthreads();
+        }
+        int r, g, b;
+        src.get(w_i[0], r, g, b);
+        nc3[0] = r, nc3[1] = g, nc3[2] = b;
+        __syncthreads();
+      } else {
+        const double m = static_cast<double>(cnt[c]);
+        nc3[0] = xdiv(static_cast<double>(sum[3 * c]), m);
+        nc3[1] = xdiv(static_cast<double>(sum[3 * c + 1]), m);
+        nc3[2] = xdiv(static_cast<double>(sum[3 * c + 2]), m);
+      }
+      if (t == 0) {
+        if (nc3[0] != cen[3 * c] || nc3[1] != cen[3 * c + 1] || nc3[2] != cen[3 * c + 2]) sm.iscal[2] = 1;
+        cen[3 * c] = nc3[0], cen[3 * c + 1] = nc3[1], cen[3 * c + 2] = nc3[2];
+      }
+      __syncthreads();
+    }
+    if (!sm.iscal[2]) break;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+__device__ void build_lut(TrackSmem& sm, int K) {
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    const double d = v;
+    sm.lut[v] = static_cast<uint8_t>(q_assign(sm.cen, K, d, d, d));
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int64_t slot_index(const TrackDev& d, int s, int slot) {
+  return static_cast<int64_t>(s) * d.T + slot;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ meanshift
+// Persistent grid over (stream, list position) items; one CTA per track.
+__global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TrackSmem sm;
+  sm.carve(smem_raw, d.K, d.W, d.H);
+  OsumBp* bp = d.bp + static_cast<int64_t>(blockIdx.x) * (d.K + 1) * kOsumBpCap;
+  const int K = d.K;
+  const bool gray = d.CH == 1;
+  for (int item = blockIdx.x; item < d.S * d.T; item += gridDim.x) {
+    const int s = item / d.T, i = item - s * d.T;
+    if (i >= d.n_list[s]) continue;
+    const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
+    const int64_t g = slot_index(d, s, slot);
+    int status = d.status[g];
+    if (status != TRB_TRACK_ACTIVE) continue;
+    for (int k = threadIdx.x; k < 3 * K; k += NT) sm.cen[k] = d.centers[g * 3 * K + k];
+    for (int k = threadIdx.x; k < K; k += NT) sm.q[k] = d.hist[g * K + k];
+    if (gray)
+      for (int k = threadIdx.x; k < 256; k += NT) sm.lut[k] = d.lut[g * 256 + k];
+    __syncthreads();
+    double cx = d.cx[g], cy = d.cy[g];
+    meanshift_device(d.frames[s], d.W, d.H, d.CH, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, gray, sm, bp);
+    if (threadIdx.x == 0) {
+      d.cx[g] = cx;
+      d.cy[g] = cy;
+      d.status[g] = status;
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------- gate
+// One CTA per stream: spawn gating (tracking.hpp:185-195), spawn_track's
+// geometry and success conditions (:208-234), lost counting and retirement
+// (:197-201) and the log (:203-204).
+__global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
+  __shared__ int sh_n, sh_ncur, sh_next_id, sh_hit, sh_ok;
+  __shared__ double sh_min[2][NT / 32];
+  const int s = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  int32_t* list = d.list + static_cast<int64_t>(s) * d.T;
+  const trb_blob* blobs = d.blobs + static_cast<int64_t>(s) * d.blob_stride;
+  uint8_t* matched = d.matched + static_cast<int64_t>(s) * d.blob_stride;
+  const int nb = d.nblobs[s];
+  const int n = d.n_list[s];
+  auto gate = [&](const trb_blob& b, int slot) {
+    const int64_t g = slot_index(d, s, slot);
+    const double dist = glibc_hypot(xsub(b.cx, d.cx[g]), xsub(b.cy, d.cy[g]));
+    const double w = d.w[g], h = d.h[g];
+    const double diag = xsqrt(xadd(xmul(w, w), xmul(h, h)));  // Track::window_diagonal, :49
+    return dist <= xmul(1.5, diag);
+  };
+  // 1. blobs against the tracks that existed before this frame's spawns
+  for (int i = t; i < nb; i += NT) {
+    int m = 0;
+    for (int k = 0; k < n && !m; ++k) m = gate(blobs[i], list[k]);
+    matched[i] = static_cast<uint8_t>(m);
+  }
+  if (t == 0) sh_n = n, sh_ncur = n, sh_next_id = d.next_id[s];
+  __syncthreads();
+  // 2. unmatched blobs in label order: this frame's earlier spawns count too
+  for (int i = 0; i < nb; ++i) {
+    if (matched[i]) continue;  // uniform
+    const trb_blob b = blobs[i];
+    if (t == 0) sh_hit = 0;
+    __syncthreads();
+    for (int k = sh_n + t; k < sh_ncur; k += NT)
+      if (gate(b, list[k])) sh_hit = 1;
+    __syncthreads();
+    if (sh_hit) continue;
+    // spawn_track: the id is consumed even when the spawn fails (:210)
+    const int id = sh_next_id;
+    int tw = max(3, b.x_max - b.x_min + 1), th = max(3, b.y_max - b.y_min + 1);
+    while (tw * th < d.K) {
+      if (tw <= th) ++tw;
+      else ++th;
+    }
+    const Win r = clip_window(d.W, d.H, b.cx, b.cy, tw, th);
+    bool ok = !r.empty() && static_cast<int64_t>(r.x1 - r.x0) * (r.y1 - r.y0) >= d.K;
+    if (ok) {
+      // histogram_opt is nullopt iff no window pixel has a positive
+      // Epanechnikov weight; fl(a+b) is monotone, so test the minima.
+      const double hx = tw / 2.0, hy = th / 2.0;
+      double mx = __longlong_as_double(0x7ff0000000000000LL), my = mx;
+      for (int x = r.x0 + t; x < r.x1; x += NT) {
+        const double u = xdiv(xsub(static_cast<double>(x), b.cx), hx);
+        mx = fmin(mx, xmul(u, u));
+      }
+      for (int y = r.y0 + t; y < r.y1; y += NT) {
+        const double u = xdiv(xsub(static_cast<double>(y), b.cy), hy);
+        my = fmin(my, xmul(u, u));
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmin(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        my = fmin(my, __shfl_xor_sync(0xffffffffu, my, o));
+      }
+      if (lane == 0) sh_min[0][wid] = mx, sh_min[1][wid] = my;
+      __syncthreads();
+      if (t == 0) {
+        double a = sh_min[0][0], c = sh_min[1][0];
+        for (int k = 1; k < NT / 32; ++k) a = fmin(a, sh_min[0][k]), c = fmin(c, sh_min[1][k]);
+        sh_ok = xsub(1.0, xadd(a, c)) > 0.0;
+      }
+      __syncthreads();
+      ok = sh_ok;
+    }
+    if (t == 0) {
+      sh_next_id = id + 1;
+      if (ok) {
+        int slot = -1;
+        for (int k = 0; k < d.T; ++k)
+          if (!d.used[slot_index(d, s, k)]) {
+            slot = k;
+            break;
+          }
+        if (slot < 0 || sh_ncur >= d.T) {
+          d.err[s] |= 1;
+        } else {
+          const int64_t g = slot_index(d, s, slot);
+          d.used[g] = 1;
+          d.pending[g] = 1;
+          d.id[g] = id;
+          d.cx[g] = b.cx;
+          d.cy[g] = b.cy;
+          d.w[g] = tw;
+          d.h[g] = th;
+          d.status[g] = TRB_TRACK_ACTIVE;
+          d.lost[g] = 0;
+          list[sh_ncur] = slot;
+          sh_ncur = sh_ncur + 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // 3. lost counting, retirement (order preserving), log
+  if (t == 0) {
+    const int ncur = sh_ncur;
+    int j = 0;
+    for (int k = 0; k < ncur; ++k) {
+      const int slot = list[k];
+      const int64_t g = slot_index(d, s, slot);
+      if (d.status[g] == TRB_TRACK_LOST) d.lost[g] += 1;
+      if (d.status[g] == TRB_TRACK_LOST && d.lost[g] >= 5) {
+        d.used[g] = 0;
+        continue;
+      }
+      list[j++] = slot;
+    }
+    d.n_list[s] = j;
+    d.next_id[s] = sh_next_id;
+    sh_ncur = j;
+  }
+  __syncthreads();
+  const int nl = sh_ncur;
+  const int64_t base = d.n_log[s];
+  const int frame = d.frame_no[s];
+  trb_track_log_entry* log = d.log + static_cast<int64_t>(s) * d.log_cap;
+  for (int k = t; k < nl; k += NT) {
+    const int64_t pos = base + k;
+    if (pos >= d.log_cap) {
+      atomicOr(&d.err[s], 2);
+      continue;
+    }
+    const int64_t g = slot_index(d, s, list[k]);
+    trb_track_log_entry e;
+    e.frame = frame;
+    e.track_id = d.id[g];
+    e.x = d.cx[g];
+    e.y = d.cy[g];
+    e.w = d.w[g];
+    e.h = d.h[g];
+    e.status = d.status[g];
+    e._pad = 0;
+    log[pos] = e;
+  }
+  __syncthreads();
+  if (t == 0) {
+    d.n_log[s] = base + nl;
+    d.frame_no[s] = frame + 1;
+  }
+}
+
+// ---------------------------------------------------------------- spawn
+// One CTA per pending track: quantize_colors on the window pixels with
+// seed mix_seed(cfg.seed, id) (tracking.hpp:221-229), then the target
+// histogram (:230-232) and the gray->bin table.
+__global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Mt64 rng;
+  TrackSmem sm;
+  sm.carve(smem_raw, d.K, d.W, d.H);
+  OsumBp* bp = d.bp + static_cast<int64_t>(blockIdx.x) * (d.K + 1) * kOsumBpCap;
+  const int K = d.K;
+  const bool gray = d.CH == 1;
+  for (int item = blockIdx.x; item < d.S * d.T; item += gridDim.x) {
+    const int s = item / d.T, slot = item - s * d.T;
+    const int64_t g = slot_index(d, s, slot);
+    if (!d.pending[g]) continue;
+    const double cx = d.cx[g], cy = d.cy[g];
+    const int w = d.w[g], h = d.h[g];
+    const Win r = clip_window(d.W, d.H, cx, cy, w, h);
+    FrameWindowSrc src{d.frames[s], d.W, d.CH, r.x0, r.y0, r.x1 - r.x0, UDiv32::make(r.x1 - r.x0)};
+    const int n = (r.x1 - r.x0) * (r.y1 - r.y0);
+    kmeans_device(src, n, K, d.kmeans_iters, mix_seed(d.seed, static_cast<uint64_t>(d.id[g])), sm, &rng);
+    if (gray) build_lut(sm, K);
+    window_histogram(d.frames[s], d.W, d.H, d.CH, cx, cy, w, h, K, 1, gray, sm, bp, sm.q);
+    for (int k = threadIdx.x; k < 3 * K; k += NT) d.centers[g * 3 * K + k] = sm.cen[k];
+    for (int k = threadIdx.x; k < K; k += NT) d.hist[g * K + k] = sm.q[k];
+    if (gray)
+      for (int k = threadIdx.x; k < 256; k += NT) d.lut[g * 256 + k] = sm.lut[k];
+    if (threadIdx.x == 0) d.pending[g] = 0;
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------- standalone ops
+struct OneArgs {
+  const uint8_t* frame;
+  int W, H, CH;
+  double cx, cy;
+  int w, h, status, K, max_iters, epan, mode;  // mode 0 meanshift, 1 histogram
+  double eps;
+  const double* centers;  // device K*3
+  const double* target;   // device K
+  double* out;            // device: [cx, cy, status, ok] or hist[K] + ok
+  OsumBp* bp;
+};
+
+__global__ void __launch_bounds__(NT) track_one_kernel(OneArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TrackSmem sm;
+  sm.carve(smem_raw, a.K, a.W, a.H);
+  for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
+  if (a.target)
+    for (int k = threadIdx.x; k < a.K; k += NT) sm.q[k] = a.target[k];
+  __syncthreads();
+  const bool gray = a.CH == 1;
+  if (gray) build_lut(sm, a.K);
+  if (a.mode == 0) {
+    double cx = a.cx, cy = a.cy;
+    int status = a.status;
+    meanshift_device(a.frame, a.W, a.H, a.CH, cx, cy, a.w, a.h, status, a.K, a.max_iters, a.eps, gray, sm, a.bp);
+    if (threadIdx.x == 0) a.out[0] = cx, a.out[1] = cy, a.out[2] = status;
+  } else {
+    const bool ok = window_histogram(a.frame, a.W, a.H, a.CH, a.cx, a.cy, a.w, a.h, a.K, a.epan, gray, sm, a.bp, sm.p);
+    for (int k = threadIdx.x; k < a.K; k += NT) a.out[k] = sm.p[k];
+    if (threadIdx.x == 0) a.out[a.K] = ok ? 1.0 : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int K, int iters, uint64_t seed,
+                                                      double* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Mt64 rng;
+  TrackSmem sm;
+  sm.carve(smem_raw, K, 1, 1);
+  kmeans_device(ListSrc{px}, n, K, iters, seed, sm, &rng);
+  for (int k = threadIdx.x; k < 3 * K; k += NT) out[k] = sm.cen[k];
+}
+
+// ------------------------------------------------------------- host side
+static void set_smem(const void* fn, size_t bytes) {
+  TRB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+static size_t check_smem(int K, int W, int H) {
+  const size_t b = TrackSmem::bytes(K, W, H);
+  if (b > 220 * 1024)
+    throw Error(TRB_CONFIG_ERROR, "tracker k_clusters / frame size exceed the device shared-memory budget");
+  if (4 * K > 2 * NT) throw Error(TRB_CONFIG_ERROR, "tracker k_clusters too large for the device k-means");
+  return b;
+}
+
+TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, int64_t log_cap)
+    : cfg_(cfg), S_(S), T_(track_cap), K_(cfg.k_clusters), log_cap_(log_cap) {
+  validate_tracker(cfg);
+  const int64_t n = static_cast<int64_t>(S) * T_;
+  // int32 block: n_list,next_id,frame_no,err (4*S) + list, id,w,h,status,lost,used,pending (8*n)
+  i32_.alloc(sizeof(int32_t) * (4 * S + 8 * n));
+  f64_.alloc(sizeof(double) * n * (2 + 4 * K_));
+  lut_.alloc(static_cast<size_t>(n) * 256);
+  log_.alloc(sizeof(trb_track_log_entry) * log_cap_ * S, false);
+  nlog_.alloc(sizeof(int64_t) * S);
+  grid_ = static_cast<int>(std::min<int64_t>(n, 2 * 148));
+  bp_.alloc(sizeof(OsumBp) * static_cast<size_t>(grid_) * (K_ + 1) * kOsumBpCap, false);
+  int32_t* p = i32_.as<int32_t>();
+  d_.S = S, d_.T = T_, d_.K = K_;
+  d_.max_iters = cfg.max_iters, d_.kmeans_iters = cfg.kmeans_iters, d_.eps = cfg.eps, d_.seed = cfg.seed;
+  d_.n_list = p, d_.next_id = p + S, d_.frame_no = p + 2 * S, d_.err = p + 3 * S;
+  p += 4 * S;
+  d_.list = p, d_.id = p + n, d_.w = p + 2 * n, d_.h = p + 3 * n, d_.status = p + 4 * n, d_.lost = p + 5 * n;
+  d_.used = p + 6 * n, d_.pending = p + 7 * n;
+  double* f = f64_.as<double>();
+  d_.cx = f, d_.cy = f + n, d_.centers = f + 2 * n, d_.hist = f + 2 * n + 3 * K_ * n;
+  d_.lut = lut_.as<uint8_t>();
+  d_.log = log_.as<trb_track_log_entry>();
+  d_.log_cap = log_cap_;
+  d_.n_log = nlog_.as<int64_t>();
+  d_.bp = bp_.as<OsumBp>();
+  // next_id starts at 1 (tracking.hpp:239)
+  std::vector<int32_t> ones(S, 1);
+  TRB_CUDA(cudaMemcpy(d_.next_id, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
+}
+
+TrackerState::~TrackerState() = default;
+
+void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int ch, const trb_blob* blobs,
+                           int64_t blob_stride, const int32_t* nblobs, cudaStream_t st, int* launches) {
+  if (matched_cap_ < blob_stride) {
+    matched_.alloc(static_cast<size_t>(blob_stride) * S_);
+    matched_cap_ = blob_stride;
+  }
+  d_.W = w, d_.H = h, d_.CH = ch;
+  d_.frames = frames_dev;
+  d_.blobs = blobs;
+  d_.blob_stride = blob_stride;
+  d_.nblobs = nblobs;
+  d_.matched = matched_.as<uint8_t>();
+  const size_t smem = check_smem(K_, w, h);
+  set_smem(reinterpret_cast<const void*>(track_meanshift_kernel), smem);
+  set_smem(reinterpret_cast<const void*>(track_spawn_kernel), smem);
+  track_meanshift_kernel<<<grid_, NT, smem, st>>>(d_);
+  TRB_LAUNCH_CHECK("track_meanshift_kernel");
+  track_gate_kernel<<<S_, NT, 0, st>>>(d_);
+  TRB_LAUNCH_CHECK("track_gate_kernel");
+  track_spawn_kernel<<<grid_, NT, smem, st>>>(d_);
+  TRB_LAUNCH_CHECK("track_spawn_kernel");
+  *launches += 3;
+}
+
+void TrackerState::check_errors(cudaStream_t st) {
+  std::vector<int32_t> e(S_);
+  TRB_CUDA(cudaMemcpyAsync(e.data(), d_.err, sizeof(int32_t) * S_, cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  for (int s = 0; s < S_; ++s) {
+    if (e[s] & 1) throw Error(TRB_CAPACITY, "tracker: track capacity exceeded on stream " + std::to_string(s));
+    if (e[s] & 2) throw Error(TRB_CAPACITY, "tracker: device track-log capacity exceeded on stream " + std::to_string(s));
+  }
+}
+
+int TrackerState::num_tracks(int s, cudaStream_t st) {
+  int32_t n = 0;
+  TRB_CUDA(cudaMemcpyAsync(&n, d_.n_list + s, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  return n;
+}
+
+void TrackerState::tracks(int s, trb_track* out, int cap, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(S_) * T_;
+  std::vector<int32_t> i32(4 * S_ + 8 * n);
+  std::vector<double> f(2 * n);
+  TRB_CUDA(cudaMemcpyAsync(i32.data(), i32_.p, sizeof(int32_t) * i32.size(), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaMemcpyAsync(f.data(), f64_.p, sizeof(double) * f.size(), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  const int32_t* p = i32.data() + 4 * S_;
+  const int nl = i32[s];
+  for (int i = 0; i < nl && i < cap; ++i) {
+    const int slot = p[static_cast<int64_t>(s) * T_ + i];
+    const int64_t g = static_cast<int64_t>(s) * T_ + slot;
+    trb_track& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    o.track_id = p[n + g];
+    o.w = p[2 * n + g];
+    o.h = p[3 * n + g];
+    o.status = p[4 * n + g];
+    o.lost_frames = p[5 * n + g];
+    o.k = K_;
+    o.cx = f[g];
+    o.cy = f[n + g];
+  }
+}
+
+void TrackerState::track_model(int s, int i, double* centers, double* hist, cudaStream_t st) {
+  int32_t slot = 0;
+  TRB_CUDA(cudaMemcpyAsync(&slot, d_.list + static_cast<int64_t>(s) * T_ + i, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  const int64_t g = static_cast<int64_t>(s) * T_ + slot;
+  if (centers)
+    TRB_CUDA(cudaMemcpyAsync(centers, d_.centers + g * 3 * K_, sizeof(double) * 3 * K_, cudaMemcpyDeviceToHost, st));
+  if (hist) TRB_CUDA(cudaMemcpyAsync(hist, d_.hist + g * K_, sizeof(double) * K_, cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+}
+
+int64_t TrackerState::log_size(int s, cudaStream_t st) {
+  int64_t n = 0;
+  TRB_CUDA(cudaMemcpyAsync(&n, d_.n_log + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  return n;
+}
+
+void TrackerState::log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st) {
+  const int64_t n = std::min(log_size(s, st), std::min(cap, log_cap_));
+  if (n > 0)
+    TRB_CUDA(cudaMemcpyAsync(out, d_.log + static_cast<int64_t>(s) * log_cap_, sizeof(trb_track_log_entry) * n,
+                             cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+}
+
+int TrackerState::frames_processed(int s, cudaStream_t st) {
+  int32_t n = 0;
+  TRB_CUDA(cudaMemcpyAsync(&n, d_.frame_no + s, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  return n;
+}
+
+// ---- standalone ops ----
+static DevBuf& scratch_bp() {
+  thread_local DevBuf b;
+  return b;
+}
+
+static OsumBp* bp_for(int K) {
+  DevBuf& b = scratch_bp();
+  b.alloc(sizeof(OsumBp) * (K + 1) * kOsumBpCap, false);
+  return b.as<OsumBp>();
+}
+
+void device_meanshift_step(const uint8_t* frame_dev, int w, int h, int ch, double* cx, double* cy, int tw, int th,
+                           const double* centers, const double* target, int k, int max_iters, double eps,
+                           int* status, cudaStream_t st) {
+  DevBuf buf;
+  buf.alloc(sizeof(double) * (4 * k + 8), false);
+  double* dc = buf.as<double>();
+  TRB_CUDA(cudaMemcpyAsync(dc, centers, sizeof(double) * 3 * k, cudaMemcpyHostToDevice, st));
+  TRB_CUDA(cudaMemcpyAsync(dc + 3 * k, target, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+  OneArgs a{};
+  a.frame = frame_dev;
+  a.W = w, a.H = h, a.CH = ch;
+  a.cx = *cx, a.cy = *cy, a.w = tw, a.h = th, a.status = *status, a.K = k, a.max_iters = max_iters, a.eps = eps;
+  a.mode = 0;
+  a.centers = dc;
+  a.target = dc + 3 * k;
+  a.out = dc + 4 * k;
+  a.bp = bp_for(k);
+  const size_t smem = check_smem(k, w, h);
+  set_smem(reinterpret_cast<const void*>(track_one_kernel), smem);
+  track_one_kernel<<<1, NT, smem, st>>>(a);
+  TRB_LAUNCH_CHECK("track_one_kernel");
+  double out[3];
+  TRB_CUDA(cudaMemcpyAsync(out, a.out, sizeof(out), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  *cx = out[0], *cy = out[1], *status = static_cast<int>(out[2]);
+}
+
+bool device_histogram(const uint8_t* frame_dev, int w, int h, int ch, double cx, double cy, int tw, int th,
+                      const double* centers, int k, int epanechnikov, double* hist, cudaStream_t st) {
+  DevBuf buf;
+  buf.alloc(sizeof(double) * (4 * k + 8), false);
+  double* dc = buf.as<double>();
+  TRB_CUDA(cudaMemcpyAsync(dc, centers, sizeof(double) * 3 * k, cudaMemcpyHostToDevice, st));
+  OneArgs a{};
+  a.frame = frame_dev;
+  a.W = w, a.H = h, a.CH = ch;
+  a.cx = cx, a.cy = cy, a.w = tw, a.h = th, a.K = k, a.epan = epanechnikov, a.mode = 1;
+  a.centers = dc;
+  a.out = dc + 3 * k;
+  a.bp = bp_for(k);
+  const size_t smem = check_smem(k, w, h);
+  set_smem(reinterpret_cast<const void*>(track_one_kernel), smem);
+  track_one_kernel<<<1, NT, smem, st>>>(a);
+  TRB_LAUNCH_CHECK("track_one_kernel");
+  std::vector<double> out(k + 1);
+  TRB_CUDA(cudaMemcpyAsync(out.data(), a.out, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  if (out[k] == 0.0) return false;
+  std::memcpy(hist, out.data(), sizeof(double) * k);
+  return true;
+}
+
+void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint64_t seed, double* centers,
+                            cudaStream_t st) {
+  if (k < 2) throw Error(TRB_INVALID_ARGUMENT, "quantize_colors needs k >= 2");
+  if (iters < 1) throw Error(TRB_INVALID_ARGUMENT, "quantize_colors needs iters >= 1");
+  if (n < k)
+    throw Error(TRB_INVALID_ARGUMENT,
+                "quantize_colors: " + std::to_string(n) + " pixels < k=" + std::to_string(k));
+  std::vector<int> ip(static_cast<size_t>(n) * 3);
+  for (int64_t i = 0; i < 3 * n; ++i) {
+    const double v = pixels[i];
+    if (!(v >= 0.0 && v <= 65535.0) || v != static_cast<double>(static_cast<int>(v)))
+      throw Error(TRB_INVALID_ARGUMENT, "device quantize_colors needs integer-valued samples in [0, 65535]");
+    ip[i] = static_cast<int>(v);
+  }
+  DevBuf dpx, dout;
+  dpx.alloc(sizeof(int) * ip.size(), false);
+  dout.alloc(sizeof(double) * 3 * k, false);
+  TRB_CUDA(cudaMemcpyAsync(dpx.p, ip.data(), sizeof(int) * ip.size(), cudaMemcpyHostToDevice, st));
+  const size_t smem = check_smem(k, 1, 1);
+  set_smem(reinterpret_cast<const void*>(quantize_kernel), smem);
+  quantize_kernel<<<1, NT, smem, st>>>(dpx.as<int>(), static_cast<int>(n), k, iters, seed, dout.as<double>());
+  TRB_LAUNCH_CHECK("quantize_kernel");
+  TRB_CUDA(cudaMemcpyAsync(centers, dout.p, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace trb

@@ -1,0 +1,97 @@
+// trb_track.cuh — device-resident multi-object tracker (north-star kernel
+// (5): nearest-centroid track association, plus the mean-shift update and
+// the k-means colour model it depends on).
+//
+// Reference: Tracker (tracking.hpp:170-241), meanshift_step (:125-157),
+// histogram_opt (:79-102), spawn_track (:208-234), quantize_colors
+// (quantize.hpp:43-118).  Bit-exact: every fp64 operation is an explicit
+// round-to-nearest intrinsic, sequential sums go through ordered_sums()
+// (trb_osum.cuh), hypot is glibc's algorithm (trb_exact.cuh).
+//
+// State layout (per stream s, slot capacity T, K clusters), all in HBM:
+//   list[s][T]      slot ids in the reference's track-list order
+//   slot arrays     id, w, h, status, lost, pending, cx, cy,
+//                   centers[K][3], hist[K], lut[256] (gray -> bin)
+//   log[s][cap]     TrackLogEntry records (tracking.hpp:159-165)
+// Per frame: meanshift (one CTA per active track, persistent grid) ->
+// gate (one CTA per stream: association, spawn decisions, retire, log) ->
+// spawn (one CTA per new track: k-means++ / Lloyd / target histogram).
+#pragma once
+
+#include "trb_engine.cuh"
+#include "trb_osum.cuh"
+
+namespace trb {
+
+struct TrackDev {
+  int S, T, K;
+  int max_iters, kmeans_iters;
+  double eps;
+  uint64_t seed;
+  int W, H, CH;  // frame geometry
+  const uint8_t* const* frames;  // [S] device frame pointers
+  // per stream
+  int32_t* n_list;
+  int32_t* list;  // [S][T]
+  int32_t* next_id;
+  int32_t* frame_no;
+  int32_t* err;  // bit0 track-capacity overflow, bit1 log overflow
+  // per slot [S][T]
+  int32_t *id, *w, *h, *status, *lost, *used, *pending;
+  double *cx, *cy;
+  double* centers;  // [S][T][K][3]
+  double* hist;     // [S][T][K]
+  uint8_t* lut;     // [S][T][256]
+  // blobs of the current frame
+  const trb_blob* blobs;
+  int64_t blob_stride;
+  const int32_t* nblobs;
+  uint8_t* matched;  // [S][blob_stride] scratch
+  // log
+  trb_track_log_entry* log;
+  int64_t log_cap;
+  int64_t* n_log;  // [S]
+  // osum breakpoint scratch: [grid][K+1][kOsumBpCap]
+  OsumBp* bp;
+};
+
+class TrackerState {
+ public:
+  TrackerState(const trb_tracker_config& cfg, int S, int track_cap = 256, int64_t log_cap = 1 << 16);
+  ~TrackerState();
+  // One Tracker::process for every stream.  blobs: device [S][blob_stride].
+  void process(const uint8_t* const* frames_dev, int w, int h, int ch, const trb_blob* blobs, int64_t blob_stride,
+               const int32_t* nblobs, cudaStream_t st, int* launches);
+  // host-side readers (synchronise `st`)
+  int num_tracks(int s, cudaStream_t st);
+  void tracks(int s, trb_track* out, int cap, cudaStream_t st);
+  void track_model(int s, int i, double* centers, double* hist, cudaStream_t st);
+  int64_t log_size(int s, cudaStream_t st);
+  void log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st);
+  int frames_processed(int s, cudaStream_t st);
+  void check_errors(cudaStream_t st);
+  const trb_tracker_config& cfg() const { return cfg_; }
+
+ private:
+  trb_tracker_config cfg_;
+  int S_, T_, K_;
+  int64_t log_cap_;
+  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_;
+  TrackDev d_{};
+  int64_t matched_cap_ = 0;
+  int grid_ = 0;
+};
+
+// ---- standalone device ops behind the C ABI (tests and compat layer) ----
+// meanshift_step (tracking.hpp:125-157) on one track; frame on the device.
+void device_meanshift_step(const uint8_t* frame_dev, int w, int h, int ch, double* cx, double* cy, int tw, int th,
+                           const double* centers, const double* target, int k, int max_iters, double eps,
+                           int* status, cudaStream_t st);
+// histogram_opt (tracking.hpp:79-102); returns false for nullopt.
+bool device_histogram(const uint8_t* frame_dev, int w, int h, int ch, double cx, double cy, int tw, int th,
+                      const double* centers, int k, int epanechnikov, double* hist, cudaStream_t st);
+// quantize_colors (quantize.hpp:43-118) for integer-valued samples.
+void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint64_t seed, double* centers,
+                            cudaStream_t st);
+
+}  // namespace trb

@@ -1,0 +1,119 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference.
+
+Runs the reference headers (compiled by oracle/Makefile into
+oracle/_ref/libteamrec_ref.so from /root/reference/proj/include) on the
+cases below and stores compact results: per-frame SHA-256 digests of the
+masks and label images, the blob tables and the full track logs.  Re-run
+after changing a case:
+
+    make -C oracle && python tests/golden/make_golden.py
+
+Cases:
+  c1_pipeline       recipe C1, frames 0..159, default configs
+  c2_pipeline       recipe C2 (UC-Teamwork-like), frames 0..139
+  harness_vision    harness_test.cpp:377-389 clip (48x36 RGB, W=9)
+  bench_vision      bench_run's clip (harness.hpp:571-581, 96x72 RGB, W=91)
+  two_squares       tracking_test.cpp:249-270 clip, TrackerConfig k=4 seed=7
+  acceptance6       acceptance.cpp:344-358 clip (criterion 6), default tracker
+  retire            tracking_test.cpp:343-372 (lost tracks retire after 5)
+  random_ccl        200 random 32x32 masks (seed 303, acceptance.cpp:139-171)
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
+from paper_1310_3322_b200.synth import Clip, Rng, Shape, bench_vision_clip, harness_vision_clip, recipe  # noqa: E402
+from tests import _oracle as O  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def two_squares_clip() -> Clip:
+    red, yellow, blue = (255, 0, 0), (255, 255, 0), (0, 0, 255)
+    shapes = [Shape(9, 9, red, 4, 4, 0.5, 0.25), Shape(5, 5, yellow, 6, 6, 0.5, 0.25),
+              Shape(9, 9, blue, 48, 32, -0.5, 0.0), Shape(5, 5, red, 50, 34, -0.5, 0.0)]
+    return Clip(64, 48, 3, 0, shapes, 30, 0, "two_squares")
+
+
+def acceptance6_clip() -> Clip:
+    span = 29.0
+    shapes = [Shape(9, 9, (230, 40, 40), 4.0, 6.0, (46.0 - 4.0) / span, (12.0 - 6.0) / span),
+              Shape(8, 8, (40, 60, 230), 52.0, 36.0, (6.0 - 52.0) / span, (30.0 - 36.0) / span)]
+    return Clip(64, 48, 3, 0, shapes, 30, 606, "acceptance6")
+
+
+def random_mask(w, h, density, rng: Rng) -> np.ndarray:
+    """oracle::random_mask (tests/oracles.hpp:90-94)."""
+    return np.array([1 if rng.uniform() < density else 0 for _ in range(w * h)], np.uint8)
+
+
+def pipeline_case(clip: Clip, n: int, mcfg: MOTION_CFG, impl: str = "ref"):
+    frames, _ = O.ref_frames(clip, n) if impl == "ref" else O.orc_frames(clip, n)
+    out, log, _ = O.run_pipeline_cpu(clip, frames, mcfg, SEG_CFG(), TRACKER_CFG(), impl)
+    steady = np.array([t for t, *_ in out], np.int32)
+    mask_sha = np.array([sha(m) for _, m, _, _ in out])
+    label_sha = np.array([sha(l_) for _, _, l_, _ in out])
+    nblobs = np.array([len(b) for *_, b in out], np.int32)
+    blobs = np.concatenate([b for *_, b in out]) if out else np.zeros(0)
+    return dict(steady=steady, mask_sha=mask_sha, label_sha=label_sha, nblobs=nblobs, blobs=blobs, log=log,
+                frames_sha=np.array([sha(f) for f in frames]))
+
+
+def tracker_case(clip: Clip, tcfg: TRACKER_CFG, min_area=4):
+    frames, rects = O.ref_frames(clip)
+    trk = O.CpuTracker(tcfg, "ref")
+    w, h = clip.width, clip.height
+    for t in range(clip.n_frames):
+        # blobs of the generator's union mask (tracking_test.cpp blobs_of)
+        m = np.zeros(w * h, np.uint8)
+        for (ix, iy, rw, rh) in rects[t]:
+            mm = m.reshape(h, w)
+            mm[iy:iy + rh, ix:ix + rw] = 1
+        _, blobs, _ = O.cpu_label(m, w, h, 1, min_area, "ref", sequential=True)
+        trk.process(frames[t], w, h, clip.channels, blobs)
+    return dict(log=trk.log(), frames_sha=np.array([sha(f) for f in frames]))
+
+
+def main():
+    if not O.ref_available():
+        sys.exit("oracle/_ref/libteamrec_ref.so missing: run `make -C oracle` where /root/reference exists")
+    out = {}
+    out["c1_pipeline"] = pipeline_case(recipe("C1"), 160, MOTION_CFG())
+    out["c2_pipeline"] = pipeline_case(recipe("C2"), 140, MOTION_CFG())
+    out["harness_vision"] = pipeline_case(harness_vision_clip(), 29, MOTION_CFG(window=9))
+    bc = bench_vision_clip()
+    out["bench_vision"] = pipeline_case(bc, bc.n_frames, MOTION_CFG())
+    out["two_squares"] = tracker_case(two_squares_clip(), TRACKER_CFG(k_clusters=4, seed=7))
+    out["acceptance6"] = tracker_case(acceptance6_clip(), TRACKER_CFG())
+    # random CCL masks, acceptance.cpp:139-171 (density 0.25 + 0.5*u, conn alternating, min_area 1)
+    rng = Rng(303)
+    masks, labels_sha, nb, conns = [], [], [], []
+    for trial in range(200):
+        density = 0.25 + 0.5 * rng.uniform()
+        m = random_mask(32, 32, density, rng)
+        conn = 1 if trial % 2 else 0
+        lab, blobs, _ = O.cpu_label(m, 32, 32, conn, 1, "ref", n_blocks=4)
+        masks.append(m)
+        labels_sha.append(sha(lab))
+        nb.append(len(blobs))
+        conns.append(conn)
+    out["random_ccl"] = dict(masks=np.array(masks), label_sha=np.array(labels_sha), nblobs=np.array(nb),
+                             conn=np.array(conns))
+    for name, d in out.items():
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+        print(name, {k: getattr(v, "shape", None) for k, v in d.items()})
+
+
+if __name__ == "__main__":
+    main()
