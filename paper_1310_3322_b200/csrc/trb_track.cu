@@ -133,7 +133,9 @@ struct TrackSmem {
   static size_t bytes(int K, int W, int H) {
     size_t b = OsumSmem::bytes(K + 1, NT);
     b = (b + 15) & ~size_t(15);
-    b += sizeof(double) * (W + H + 6 * K + 16) + 256 + sizeof(int) * 16 + sizeof(long long) * 2 * NT + 64;
+    // ux2, uy2, cen, old, q, p, wsq, scal, red, iscal, lut — each region
+    // rounded up to 16 bytes by carve()
+    b += sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT + sizeof(int) * 16 + 256 + 11 * 16;
     return b;
   }
   __device__ void carve(void* base, int K, int W, int H) {
