@@ -303,6 +303,58 @@ int ref_synth(int w, int h, int ch, uint8_t bg, int n, const int32_t* si, const 
   }
 }
 
+// ---- stepwise multi-stream reference loop (bench.py --impl reference) ----
+// Each step advances every stream by one frame: push -> label_blocked
+// (sequential backend) -> Tracker::process, streams spread over `threads`
+// host threads.  Returns the number of frames that produced a mask.
+struct RefStreams {
+  int n, w, h, ch;
+  std::vector<std::unique_ptr<MotionDetector>> det;
+  std::vector<std::unique_ptr<Tracker>> trk;
+  SegmentationConfig seg;
+  std::vector<int64_t> digest;
+};
+
+void* ref_streams_create(int n, int w, int h, int ch, const trb_motion_config* mc, const trb_seg_config* sc,
+                         const trb_tracker_config* tc) {
+  try {
+    auto* r = new RefStreams{n, w, h, ch, {}, {}, to_seg(sc), {}};
+    for (int s = 0; s < n; ++s) {
+      r->det.push_back(std::make_unique<MotionDetector>(to_motion(mc), w, h));
+      r->trk.push_back(std::make_unique<Tracker>(to_tracker(tc)));
+    }
+    return r;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void ref_streams_destroy(void* p) { delete static_cast<RefStreams*>(p); }
+
+int64_t ref_streams_step(void* p, const uint8_t* const* frames, int threads) {
+  auto* r = static_cast<RefStreams*>(p);
+  std::atomic<int> next{0};
+  std::atomic<int64_t> steady{0};
+  auto worker = [&]() {
+    for (;;) {
+      const int s = next.fetch_add(1);
+      if (s >= r->n) return;
+      Frame f = make_frame(frames[s], r->w, r->h, r->ch);
+      auto mask = r->det[s]->push(r->ch == 1 ? f : grayscale(f));
+      if (!mask) continue;
+      const Labeling lab = label_blocked(*mask, r->seg, Backend::sequential());
+      r->trk[s]->process(f, lab.blobs, Backend::sequential());
+      steady.fetch_add(1);
+    }
+  };
+  const int nt = std::max(1, std::min(threads, r->n));
+  std::vector<std::thread> pool;
+  for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  return steady.load();
+}
+
 // ---- the reference per-frame loop, used as the CPU baseline ----
 // Runs push -> label_blocked(sequential backend) -> Tracker::process over
 // n_frames frames of each of n_streams streams (frames[s] = n_frames*w*h*ch

@@ -129,6 +129,8 @@ def _declare(L):
         "trb_streams_num_tracks": [vp, i32, C.POINTER(C.c_int)],
         "trb_streams_last_step_launches": [vp, C.POINTER(C.c_int)],
         "trb_streams_device_planes": [vp, i32, vp, vp],
+        "trb_streams_profile": [vp, i32],
+        "trb_streams_profile_read": [vp, vp, C.POINTER(C.c_int)],
         "trb_synth_raster": [vp, i32, i32, i32, C.c_uint8, vp, vp, i32, vp],
         "trb_meanshift_step": [vp, i32, i32, i32, C.POINTER(dbl), C.POINTER(dbl), i32, i32, vp, vp, i32, i32, dbl,
                                C.POINTER(C.c_int), i32],
@@ -401,6 +403,16 @@ class Streams:
         arr = (LOGE * max(1, n.value))()
         _check(lib().trb_streams_download_log(self._h, s, arr, n.value))
         return log_to_array(arr, n.value)
+
+    def profile(self, enable: bool) -> None:
+        _check(lib().trb_streams_profile(self._h, int(enable)))
+
+    def profile_read(self):
+        """-> (ms per stage [motion, ccl, tracking] summed, steps)"""
+        ms = np.zeros(3)
+        n = C.c_int(0)
+        _check(lib().trb_streams_profile_read(self._h, _ptr(ms), C.byref(n)))
+        return ms, n.value
 
     def device_planes(self, s: int):
         m, l_ = C.c_void_p(), C.c_void_p()

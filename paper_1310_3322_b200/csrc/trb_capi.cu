@@ -559,6 +559,21 @@ int trb_streams_last_step_launches(const trb_streams* s, int* n) {
   });
 }
 
+int trb_streams_profile(trb_streams* s, int enable) {
+  return guard([&] {
+    need(s != nullptr, "null argument");
+    s->s->set_profiling(enable != 0);
+  });
+}
+
+int trb_streams_profile_read(const trb_streams* s, double* ms_out, int* steps) {
+  return guard([&] {
+    need(s && ms_out && steps, "null argument");
+    for (int i = 0; i < trb::Streams::kStages; ++i) ms_out[i] = s->s->profile_ms()[i];
+    *steps = s->s->profile_steps();
+  });
+}
+
 int trb_streams_device_planes(trb_streams* s, int stream, uint8_t** mask, int32_t** labels) {
   return guard([&] {
     need(s != nullptr, "null argument");
@@ -574,7 +589,7 @@ int trb_synth_raster(uint8_t* out_device, int width, int height, int channels, u
     need(out_device != nullptr, "null argument");
     need(channels == 1 || channels == 3, "clip channels must be 1 or 3");
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    DevBuf d;
+    thread_local DevBuf d;  // reused: the call synchronises before returning
     d.alloc(sizeof(int32_t) * 4 * n_shapes + 3 * n_shapes + 16, false);
     int32_t* dr = d.as<int32_t>();
     uint8_t* dc = reinterpret_cast<uint8_t*>(dr + 4 * n_shapes);

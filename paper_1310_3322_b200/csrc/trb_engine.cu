@@ -195,52 +195,83 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S);
   mask_.alloc(static_cast<size_t>(px_) * S);
   if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S);
-  frame_ptrs_.alloc(sizeof(void*) * S);
-  ptrs_host_.alloc(sizeof(void*) * S);
+  // ring of per-step frame-pointer tables: a table is rewritten only after
+  // the event of its previous use completed, so steps never block the host
+  frame_ptrs_.alloc(sizeof(void*) * S * kPtrSlots);
+  ptrs_host_.alloc(sizeof(void*) * S * kPtrSlots);
+  for (int i = 0; i < kPtrSlots; ++i) TRB_CUDA(cudaEventCreateWithFlags(&slot_ev_[i], cudaEventDisableTiming));
+  for (int i = 0; i < kStages + 1; ++i) TRB_CUDA(cudaEventCreate(&prof_ev_[i]));
   TRB_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
 }
 
 Streams::~Streams() {
+  for (auto& e : slot_ev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : prof_ev_)
+    if (e) cudaEventDestroy(e);
   if (own_) cudaStreamDestroy(own_);
+}
+
+void Streams::set_profiling(bool on) {
+  profiling_ = on;
+  for (double& v : prof_ms_) v = 0.0;
+  prof_steps_ = 0;
 }
 
 void Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st) {
   int launches = 0;
+  if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[0], st));
   const bool emitted = motion_->push(frames_dev, mask_.as<uint8_t>(), mask_tmp_.as<uint8_t>(), st, &launches);
-  if (emitted) {
-    ccl_->run(mask_.as<uint8_t>(), st, &launches);
-    if (tracker_)
-      tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches);
+  if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[1], st));
+  if (emitted) ccl_->run(mask_.as<uint8_t>(), st, &launches);
+  if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[2], st));
+  if (emitted && tracker_)
+    tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches);
+  if (profiling_) {
+    TRB_CUDA(cudaEventRecord(prof_ev_[3], st));
+    TRB_CUDA(cudaEventSynchronize(prof_ev_[3]));
+    for (int i = 0; i < kStages; ++i) {
+      float ms = 0.f;
+      TRB_CUDA(cudaEventElapsedTime(&ms, prof_ev_[i], prof_ev_[i + 1]));
+      prof_ms_[i] += ms;
+    }
+    ++prof_steps_;
   }
   has_output_ = emitted;
   last_launches_ = launches;
 }
 
+const uint8_t* const* Streams::upload_ptrs_(const uint8_t* const* frames, cudaStream_t st) {
+  const int slot = ptr_slot_;
+  ptr_slot_ = (ptr_slot_ + 1) % kPtrSlots;
+  TRB_CUDA(cudaEventSynchronize(slot_ev_[slot]));  // previous use of this table is done
+  const uint8_t** hp = ptrs_host_.as<const uint8_t*>() + static_cast<size_t>(slot) * S_;
+  std::memcpy(hp, frames, sizeof(void*) * S_);
+  const uint8_t** dp = frame_ptrs_.as<const uint8_t*>() + static_cast<size_t>(slot) * S_;
+  TRB_CUDA(cudaMemcpyAsync(dp, hp, sizeof(void*) * S_, cudaMemcpyHostToDevice, st));
+  return dp;
+}
+
 void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
   if (!st) st = own_;
-  // the kernels read the per-stream frame pointers from device memory
-  // (pinned staging must not be overwritten while a previous copy is in flight)
-  TRB_CUDA(cudaStreamSynchronize(st));
-  std::memcpy(ptrs_host_.p, frames, sizeof(void*) * S_);
-  TRB_CUDA(cudaMemcpyAsync(frame_ptrs_.p, ptrs_host_.p, sizeof(void*) * S_, cudaMemcpyHostToDevice, st));
-  ptrs_staging_ = false;
-  run_(frame_ptrs_.as<const uint8_t* const>(), st);
+  const int slot = ptr_slot_;
+  const uint8_t* const* dp = upload_ptrs_(frames, st);
+  run_(dp, st);
+  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
 }
 
 void Streams::step_host(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
   if (!st) st = own_;
   const size_t fb = static_cast<size_t>(px_) * ch_;
   if (!staging_.p) staging_.alloc(fb * S_, false);
-  if (!ptrs_staging_) {
-    TRB_CUDA(cudaStreamSynchronize(st));
-    ptrs_staging_ = true;
-    const uint8_t** hp = ptrs_host_.as<const uint8_t*>();
-    for (int s = 0; s < S_; ++s) hp[s] = staging_.as<uint8_t>() + fb * s;
-    TRB_CUDA(cudaMemcpyAsync(frame_ptrs_.p, ptrs_host_.p, sizeof(void*) * S_, cudaMemcpyHostToDevice, st));
-  }
+  std::vector<const uint8_t*> dev(S_);
+  for (int s = 0; s < S_; ++s) dev[s] = staging_.as<uint8_t>() + fb * s;
+  const int slot = ptr_slot_;
+  const uint8_t* const* dp = upload_ptrs_(dev.data(), st);
   for (int s = 0; s < S_; ++s)
     TRB_CUDA(cudaMemcpyAsync(staging_.as<uint8_t>() + fb * s, frames[s], fb, cudaMemcpyHostToDevice, st));
-  run_(frame_ptrs_.as<const uint8_t* const>(), st);
+  run_(dp, st);
+  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
   if (result_host) {
     if (has_output_)
       TRB_CUDA(cudaMemcpyAsync(result_host, ccl_->nblobs(), sizeof(int32_t) * S_, cudaMemcpyDeviceToHost, st));

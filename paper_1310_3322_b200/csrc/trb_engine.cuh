@@ -121,9 +121,16 @@ class Streams {
   uint8_t* mask(int s) const { return mask_.as<uint8_t>() + px_ * s; }
   CclState& ccl() { return *ccl_; }
   TrackerState* tracker() { return tracker_.get(); }
+  // per-stage device time (motion, ccl, tracking) accumulated over steps
+  static constexpr int kStages = 3;
+  void set_profiling(bool on);
+  const double* profile_ms() const { return prof_ms_; }
+  int profile_steps() const { return prof_steps_; }
 
  private:
+  static constexpr int kPtrSlots = 16;
   void run_(const uint8_t* const* frames_dev, cudaStream_t st);
+  const uint8_t* const* upload_ptrs_(const uint8_t* const* frames, cudaStream_t st);
   int S_, w_, h_, ch_;
   int64_t px_;
   trb_motion_config mc_;
@@ -134,8 +141,13 @@ class Streams {
   PinnedBuf ptrs_host_;
   cudaStream_t own_ = nullptr;
   bool has_output_ = false;
-  bool ptrs_staging_ = false;
   int last_launches_ = 0;
+  int ptr_slot_ = 0;
+  cudaEvent_t slot_ev_[kPtrSlots] = {};
+  cudaEvent_t prof_ev_[kStages + 1] = {};
+  bool profiling_ = false;
+  double prof_ms_[kStages] = {};
+  int prof_steps_ = 0;
 };
 
 }  // namespace trb

@@ -778,8 +778,11 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   d_.nblobs = nblobs;
   d_.matched = matched_.as<uint8_t>();
   const size_t smem = check_smem(K_, w, h);
-  set_smem(reinterpret_cast<const void*>(track_meanshift_kernel), smem);
-  set_smem(reinterpret_cast<const void*>(track_spawn_kernel), smem);
+  if (smem != smem_set_) {
+    set_smem(reinterpret_cast<const void*>(track_meanshift_kernel), smem);
+    set_smem(reinterpret_cast<const void*>(track_spawn_kernel), smem);
+    smem_set_ = smem;
+  }
   track_meanshift_kernel<<<grid_, NT, smem, st>>>(d_);
   TRB_LAUNCH_CHECK("track_meanshift_kernel");
   track_gate_kernel<<<S_, NT, 0, st>>>(d_);

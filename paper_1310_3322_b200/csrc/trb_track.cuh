@@ -80,6 +80,7 @@ class TrackerState {
   TrackDev d_{};
   int64_t matched_cap_ = 0;
   int grid_ = 0;
+  size_t smem_set_ = 0;
 };
 
 // ---- standalone device ops behind the C ABI (tests and compat layer) ----
