@@ -213,6 +213,11 @@ int trb_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint6
 /* ---- self tests of the exact-arithmetic replicas (host build of the same
  * header the kernels use; on_device = 1 runs the device build) ---- */
 int trb_selftest_hypot(const double* x, const double* y, int64_t n, double* out, int on_device);
+/* device diagnostics: [0] ordered-sum calls [1] sums [2] sums replayed by the
+ * exact serial fallback [3] breakpoints [4] elements [5] mean-shift
+ * iterations [6] spawns [7] Lloyd iterations [8] empty-cluster passes
+ * [9] tracks advanced.  reset != 0 zeroes them after reading. */
+int trb_debug_stats(uint64_t* out16, int reset);
 
 #ifdef __cplusplus
 }

@@ -137,6 +137,7 @@ def _declare(L):
         "trb_histogram": [vp, i32, i32, i32, dbl, dbl, i32, i32, vp, i32, i32, vp, i32],
         "trb_quantize_colors": [vp, i64, i32, i32, C.c_uint64, vp, i32],
         "trb_selftest_hypot": [vp, vp, i64, vp, i32],
+        "trb_debug_stats": [vp, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -432,6 +433,16 @@ def synth_raster(out_device_ptr: int, width: int, height: int, channels: int, ba
     c = np.ascontiguousarray(np.asarray(colors, dtype=np.uint8).reshape(-1))
     _check(lib().trb_synth_raster(C.c_void_p(out_device_ptr), width, height, channels, background, _ptr(r), _ptr(c),
                                   r.size // 4, C.c_void_p(cuda_stream)))
+
+
+STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints", "osum_elements",
+              "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced")
+
+
+def debug_stats(reset: bool = False) -> dict:
+    out = np.zeros(16, np.uint64)
+    _check(lib().trb_debug_stats(_ptr(out), int(reset)))
+    return {k: int(v) for k, v in zip(STAT_NAMES, out)}
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

@@ -649,6 +649,14 @@ int trb_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint6
 
 }  // extern "C"
 
+extern "C" int trb_debug_stats(uint64_t* out16, int reset) {
+  return guard([&] {
+    need(out16 != nullptr, "null argument");
+    use_device(0);
+    trb::read_debug_stats(reinterpret_cast<unsigned long long*>(out16), reset != 0);
+  });
+}
+
 // ------------------------------------------------------------ self tests
 namespace {
 __global__ void hypot_kernel(const double* x, const double* y, int64_t n, double* out) {

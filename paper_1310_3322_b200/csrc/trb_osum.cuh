@@ -191,8 +191,11 @@ __device__ __forceinline__ void osum_scan_pieces(OsumSmem& s, int M, int NT) {
 // The engine.  `contrib(j, emit)` calls emit(m, v) for every sum element j
 // feeds, with v >= 0.  bp: global scratch of M*kOsumBpCap records.
 // Results land in s.result[m].  Must be called by all NT threads.
+// stats (optional, global): [0] calls, [1] sums, [2] sums replayed by the
+// serial fallback, [3] breakpoints, [4] elements
 template <class Contrib>
-__device__ void ordered_sums(int N, int M, const Contrib& contrib, OsumSmem& s, OsumBp* bp) {
+__device__ void ordered_sums(int N, int M, const Contrib& contrib, OsumSmem& s, OsumBp* bp,
+                             unsigned long long* stats = nullptr) {
   const int NT = blockDim.x, t = threadIdx.x;
   const int C = (N + NT - 1) / NT;
   const int j0 = min(N, t * C), j1 = min(N, j0 + C);
@@ -330,6 +333,15 @@ __device__ void ordered_sums(int N, int M, const Contrib& contrib, OsumSmem& s, 
     s.bad[m] = ok ? 0 : 1;
   }
   __syncthreads();
+  if (stats && t == 0) {
+    unsigned long long nb = 0, nbad = 0;
+    for (int m = 0; m < M; ++m) nb += s.nbp[m], nbad += s.bad[m];
+    atomicAdd(&stats[0], 1ull);
+    atomicAdd(&stats[1], static_cast<unsigned long long>(M));
+    atomicAdd(&stats[2], nbad);
+    atomicAdd(&stats[3], nb);
+    atomicAdd(&stats[4], static_cast<unsigned long long>(N));
+  }
   // exact serial fallback for any sum whose prediction failed
   for (int m = 0; m < M; ++m) {
     if (!s.bad[m]) continue;  // uniform across the block

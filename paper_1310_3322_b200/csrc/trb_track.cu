@@ -7,6 +7,11 @@
 
 namespace trb {
 
+// Device-side diagnostics: [0..4] ordered_sums stats (see trb_osum.cuh),
+// [5] mean-shift iterations, [6] spawns, [7] Lloyd iterations, [8] farthest
+// point passes, [9] tracks advanced.
+__device__ unsigned long long g_trb_stats[16];
+
 namespace {
 
 constexpr int NT = kOsumThreads;
@@ -199,7 +204,7 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
   fill_u2(sm, r, cx, cy, w, h);
   __syncthreads();
   HistContrib hc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), epan};
-  ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), K + 1, hc, sm.os, bp);
+  ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), K + 1, hc, sm.os, bp, g_trb_stats);
   const double total = sm.os.result[K];
   if (total <= 0.0) return false;
   for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os.result[b], total);
@@ -213,7 +218,9 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
                                  int& status, int K, int max_iters, double eps, bool use_lut, TrackSmem& sm,
                                  OsumBp* bp) {
   if (status != TRB_TRACK_ACTIVE) return;
+  if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
   for (int it = 0; it < max_iters; ++it) {
+    if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull);
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, bp, sm.p);
     if (threadIdx.x == 0) {
       int lost = !ok;
@@ -232,7 +239,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     }
     const Win r = clip_window(fw, fh, cx, cy, w, h);
     MsContrib mc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), sm.wsq};
-    ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), 3, mc, sm.os, bp);
+    ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), 3, mc, sm.os, bp, g_trb_stats);
     const double sw = sm.os.result[0], sx = sm.os.result[1], sy = sm.os.result[2];
     __syncthreads();
     if (sw <= 0.0) {
@@ -376,7 +383,9 @@ __device__ void kmeans_device(const Src& src, int n, int K, int iters, uint64_t 
   long long* cnt = sm.red;           // [K]
   long long* sum = sm.red + K;       // [3K]  (needs 4K <= 2*NT)
   double* old = sm.old;
+  if (t == 0) atomicAdd(&g_trb_stats[6], 1ull);
   for (int it = 0; it < iters; ++it) {
+    if (t == 0) atomicAdd(&g_trb_stats[7], 1ull);
     for (int i = t; i < 3 * K; i += NT) old[i] = cen[i];
     for (int i = t; i < 4 * K; i += NT) sm.red[i] = 0;
     __syncthreads();
@@ -395,6 +404,7 @@ __device__ void kmeans_device(const Src& src, int n, int K, int iters, uint64_t 
     for (int c = 0; c < K; ++c) {
       double nc3[3];
       if (cnt[c] == 0) {
+        if (t == 0) atomicAdd(&g_trb_stats[8], 1ull);
         // farthest sample from its (old-assignment) centre, current centres,
         // lowest index on ties (quantize.hpp:99-107)
         double bd = -1.0;
@@ -720,6 +730,14 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
 }
 
 // ------------------------------------------------------------- host side
+void read_debug_stats(unsigned long long* out, bool reset) {
+  TRB_CUDA(cudaMemcpyFromSymbol(out, g_trb_stats, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {};
+    TRB_CUDA(cudaMemcpyToSymbol(g_trb_stats, z, sizeof(z)));
+  }
+}
+
 static void set_smem(const void* fn, size_t bytes) {
   TRB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
 }

@@ -83,6 +83,9 @@ class TrackerState {
   size_t smem_set_ = 0;
 };
 
+// device diagnostics counters (see g_trb_stats in trb_track.cu)
+void read_debug_stats(unsigned long long* out, bool reset);
+
 // ---- standalone device ops behind the C ABI (tests and compat layer) ----
 // meanshift_step (tracking.hpp:125-157) on one track; frame on the device.
 void device_meanshift_step(const uint8_t* frame_dev, int w, int h, int ch, double* cx, double* cy, int tw, int th,

@@ -1,0 +1,51 @@
+"""Diagnostics: per-step timings and device tracker counters on C5 streams.
+
+python tools/diag_tracking.py --streams 8 --steps 10
+"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1310_3322_b200 as trb  # noqa: E402
+from paper_1310_3322_b200 import api  # noqa: E402
+from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
+from paper_1310_3322_b200.synth import recipe  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--streams", type=int, default=8)
+p.add_argument("--steps", type=int, default=10)
+p.add_argument("--start", type=int, default=0, help="extra steady steps before measuring")
+args = p.parse_args()
+S = args.streams
+stream = torch.cuda.Stream()
+clips = [recipe("C5", s) for s in range(S)]
+n = 90 + 3 + args.start + args.steps
+frames = bench.make_frames(trb, clips, n, stream)
+st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+ptrs = [[frames[s, t].data_ptr() for s in range(S)] for t in range(n)]
+t = 0
+for _ in range(93 + args.start):
+    st.step_device(ptrs[t], stream.cuda_stream)
+    t += 1
+torch.cuda.synchronize()
+api.debug_stats(reset=True)
+st.profile(True)
+for k in range(args.steps):
+    st.step_device(ptrs[t], stream.cuda_stream)
+    t += 1
+    ms, steps = st.profile_read()
+    st.profile(True)
+    d = api.debug_stats(reset=True)
+    print(f"step {k}: motion {ms[0]:.3f} ms  ccl {ms[1]:.3f} ms  track {ms[2]:.3f} ms  {d}")
+st.profile(False)
+for s in range(min(S, 4)):
+    b = st.blobs(s)
+    print("stream", s, "blobs", len(b), "areas", sorted(b["area"].tolist())[-5:], "tracks",
+          trb.Streams.__dict__ and None)
