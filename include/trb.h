@@ -216,8 +216,9 @@ int trb_selftest_hypot(const double* x, const double* y, int64_t n, double* out,
 /* device diagnostics: [0] ordered-sum calls [1] sums [2] sums replayed by the
  * exact serial fallback [3] breakpoints [4] elements [5] mean-shift
  * iterations [6] spawns [7] Lloyd iterations [8] empty-cluster passes
- * [9] tracks advanced.  reset != 0 zeroes them after reading. */
-int trb_debug_stats(uint64_t* out16, int reset);
+ * [9] tracks advanced, [16..25] ordered-sum failure reasons by bit.
+ * reset != 0 zeroes them after reading. */
+int trb_debug_stats(uint64_t* out32, int reset);
 
 #ifdef __cplusplus
 }

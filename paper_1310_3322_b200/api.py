@@ -436,13 +436,17 @@ def synth_raster(out_device_ptr: int, width: int, height: int, channels: int, ba
 
 
 STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints", "osum_elements",
-              "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced")
+              "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced",
+              "", "", "", "", "", "",
+              "bad_scan_merge", "bad_phaseB_merge", "bad_bp_overflow", "bad_cross_cta", "bad_fold_carry",
+              "bad_fold_merge", "bad_verify_start", "bad_verify_end", "bad_final_start", "bad_final_end",
+              "many_bp_centroid", "many_bp_total", "many_bp_bin", "max_bp")
 
 
 def debug_stats(reset: bool = False) -> dict:
-    out = np.zeros(16, np.uint64)
+    out = np.zeros(32, np.uint64)
     _check(lib().trb_debug_stats(_ptr(out), int(reset)))
-    return {k: int(v) for k, v in zip(STAT_NAMES, out)}
+    return {k: int(v) for k, v in zip(STAT_NAMES, out) if k and int(v)}
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

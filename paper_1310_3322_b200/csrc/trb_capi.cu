@@ -649,7 +649,7 @@ int trb_quantize_colors(const double* pixels, int64_t n, int k, int iters, uint6
 
 }  // extern "C"
 
-extern "C" int trb_debug_stats(uint64_t* out16, int reset) {
+extern "C" int trb_debug_stats(uint64_t* out16, int reset) {  // 32 entries
   return guard([&] {
     need(out16 != nullptr, "null argument");
     use_device(0);

@@ -1,89 +1,91 @@
-// trb_osum.cuh — block-parallel, bit-exact reproduction of a SEQUENTIAL
-// fp64 summation  S_j = fl(S_{j-1} + a_j), S_{-1} = +0, a_j >= 0.
+// trb_osum.cuh — cluster-parallel, bit-exact reproduction of SEQUENTIAL
+// fp64 summations  S_j = fl(S_{j-1} + a_j), S_{-1} = +0, a_j >= 0.
 //
 // Why: the reference tracker accumulates its Epanechnikov histogram
 // (tracking.hpp:86-98) and its mean-shift centroid (tracking.hpp:135-146) as
 // plain sequential double sums in raster order; the track log is printed
 // with %.17g, so a tree reduction (different rounding) would break parity.
 //
-// Idea: while the running sum S stays inside one binade [2^e, 2^(e+1)) it is
-// a multiple of u = 2^(e-52), and  fl(S + a) = S + RN_u(a)  exactly, where
-// RN_u rounds a to the nearest multiple of u — independent of S — unless
-// a sits exactly half-way between two multiples (a tie, resolved by S's
-// parity) or S + a leaves the binade.  So every "safe" step contributes an
-// exact integer r = RN_u(a)/u, and runs of safe steps are summed with exact
-// int64 arithmetic in parallel.  The remaining "breakpoint" steps (binade
-// crossings, ties, the first element) are replayed serially with real IEEE
-// additions.  Which binade each step sees is predicted from an approximate
-// parallel prefix P (error <= delta relative); a step whose interval
-// [P_prev(1-delta), P_next(1+delta)] is not inside one binade is made a
-// breakpoint, and the serial replay re-checks every prediction, falling back
-// to a full serial sum (exact by construction) if one ever fails.
+// Idea.  While the running sum S stays inside one binade [2^e, 2^(e+1)) it
+// is X*u with u = 2^(e-52) and X an integer in [2^52, 2^53).  For a step
+// with a >= 0 that keeps S in the binade, fl(S + a) = (X + RN(a/u))*u where
+// the rounding of a/u to an integer depends on a alone — except when a/u is
+// exactly k + 1/2, where round-half-even gives E(X + k) with
+// E(y) = y + (y & 1) ("up to even").  Both step kinds are integer maps
+//         add(r):  X -> X + r          tie(k):  X -> E(X + k)
+// and the set {X -> X + B} U {X -> E(X + A) + B} is closed under
+// composition (E(X+A) is even, so E(E(X+A) + y) = E(X+A) + E(y)).  A run of
+// steps inside one binade is therefore a "piece" (tie?, A, B) of exact int64
+// numbers, and pieces compose associatively — a parallel scan.  The only
+// steps left for a serial replay are "breakpoints": the first element and
+// binade crossings (~log2 of the dynamic range per sum).  Which binade a step
+// sees is predicted from an approximate parallel prefix P (relative error
+// <= delta); a step whose interval [P(1-delta), P_next(1+delta)] is not inside
+// one binade becomes a breakpoint, and the replay re-verifies every
+// prediction, falling back to a full serial sum (exact by construction) if
+// one ever fails.
 //
-// Shape: one CTA of NT threads, thread t owns the contiguous element chunk
-// [t*C, (t+1)*C).  M concurrent sums; an element may feed several sums
-// (`emit(m, v)` calls, in the reference's per-element order).
-//   phase A  chunk totals (approximate)   -> block exclusive scan  -> P at chunk starts
-//   phase B  classify steps: safe -> exact int64 pieces, else breakpoint record
-//   phase C  block segmented scan of pieces (reset at breakpoints)
-//   phase D  per sum, breakpoints ranked by element index, then one thread
-//            per sum replays: S += R*u (exact), S = fl(S + a_bp)
+// Shape: one thread-block CLUSTER of G CTAs x NT threads; cluster thread g
+// owns the contiguous element chunk [g*C, (g+1)*C).  Up to 3 lanes (sums fed
+// by the same elements) and optional segments (independent sums laid end to
+// end; used for the histogram bins after a stable partition by bin).  All
+// per-thread state lives in registers.
+//   phase A  chunk totals -> segmented cluster scan (warp shuffles, smem,
+//            DSMEM carry) -> approximate prefix at every chunk start
+//   phase B  walk the chunk: safe/tie steps compose into the thread's piece,
+//            breakpoints are recorded (piece-before, value, index)
+//   phase C  segmented cluster scan of the thread pieces (reset at
+//            breakpoints); the carried-in piece is folded into each thread's
+//            first breakpoint; breakpoints ranked into one cluster list
+//   phase D  CTA 0 replays each lane / segment serially and broadcasts the
+//            results through DSMEM.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <limits.h>
 
 #include "trb_exact.cuh"
 
 namespace trb {
 
+namespace cg = cooperative_groups;
+
 constexpr int kOsumThreads = 256;
-constexpr int kOsumBpCap = 256;  // breakpoints per sum (~ binades crossed)
+constexpr int kOsumBpRecs = 384;  // breakpoint records per CTA (all lanes)
+constexpr int kMaxCluster = 16;
+constexpr int kMaxSegs = 256;     // segments (histogram bins) per run
 constexpr int kEmptyE = INT_MIN;
 
-struct OsumBp {
-  long long R;  // safe increments before this step (units 2^(e-52)), after fix-up
-  double v;     // the element value
-  int j;        // element index
-  int e;        // binade of the piece before this step
-  int t;        // owning thread
-  int first;    // first breakpoint of this sum in thread t's chunk
+// ----------------------------------------------------------- piece algebra
+struct Piece {
+  long long A, B;
+  int e;    // binade of every step in the piece, kEmptyE = identity
+  int tie;  // 0: X -> X + B ; 1: X -> E(X + A) + B
 };
 
-// Shared-memory workspace for M sums at NT threads: 21*M*NT + 40*M bytes.
-struct OsumSmem {
-  double* run;      // [M][NT]
-  long long* R;     // [M][NT]
-  int* e;           // [M][NT]
-  unsigned char* f; // [M][NT]  has-breakpoint flag
-  double* result;   // [M]
-  long long* finR;  // [M]
-  int* fine;        // [M]
-  int* nbp;         // [M]
-  int* bad;         // [M]
-  static __host__ __device__ size_t bytes(int M, int NT) {
-    return static_cast<size_t>(M) * NT * (8 + 8 + 4 + 1) + static_cast<size_t>(M) * (8 + 8 + 4 + 4 + 4) + 64;
+__device__ __forceinline__ Piece piece_identity() { return Piece{0, 0, kEmptyE, 0}; }
+__device__ __forceinline__ long long up_even(long long y) { return y + (y & 1); }
+
+// p then q; *bad is set when two non-empty pieces disagree on the binade
+__device__ __forceinline__ Piece compose(const Piece& p, const Piece& q, int* bad) {
+  if (q.e == kEmptyE) return p;
+  if (p.e == kEmptyE) return q;
+  if (p.e != q.e) *bad = 1;
+  Piece r;
+  r.e = p.e;
+  if (!q.tie) {
+    r.tie = p.tie, r.A = p.A, r.B = p.B + q.B;
+  } else if (!p.tie) {
+    r.tie = 1, r.A = p.B + q.A, r.B = q.B;
+  } else {
+    r.tie = 1, r.A = p.A, r.B = up_even(p.B + q.A) + q.B;
   }
-  __device__ void carve(void* base, int M, int NT) {
-    char* p = static_cast<char*>(base);
-    run = reinterpret_cast<double*>(p);
-    p += sizeof(double) * M * NT;
-    R = reinterpret_cast<long long*>(p);
-    p += sizeof(long long) * M * NT;
-    result = reinterpret_cast<double*>(p);
-    p += sizeof(double) * M;
-    finR = reinterpret_cast<long long*>(p);
-    p += sizeof(long long) * M;
-    e = reinterpret_cast<int*>(p);
-    p += sizeof(int) * M * NT;
-    fine = reinterpret_cast<int*>(p);
-    p += sizeof(int) * M;
-    nbp = reinterpret_cast<int*>(p);
-    p += sizeof(int) * M;
-    bad = reinterpret_cast<int*>(p);
-    p += sizeof(int) * M;
-    f = reinterpret_cast<unsigned char*>(p);
-  }
-};
+  return r;
+}
+
+__device__ __forceinline__ long long apply(const Piece& p, long long X) {
+  return p.tie ? up_even(X + p.A) + p.B : X + p.B;
+}
 
 __device__ __forceinline__ int osum_exp(double x) {  // binade of a positive normal double, else kEmptyE
   const long long b = __double_as_longlong(x);
@@ -91,270 +93,475 @@ __device__ __forceinline__ int osum_exp(double x) {  // binade of a positive nor
   return (be == 0 || be == 0x7ff || b < 0) ? kEmptyE : be - 1023;
 }
 
-// merge two piece exponents (kEmptyE = piece without safe steps); returns
-// false when two non-empty pieces of one segment disagree on the binade
-__device__ __forceinline__ bool osum_merge_e(int a_e, int b_e, int* out) {
-  if (a_e == kEmptyE) {
-    *out = b_e;
-    return true;
-  }
-  *out = a_e;
-  return b_e == kEmptyE || a_e == b_e;
+// 2^k as a double for -1022 <= k <= 1023 (exact, no libm call)
+__device__ __forceinline__ double osum_pow2(int k) {
+  return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
 
-// Exclusive scan of run[m][*] (doubles) for every m; warp w scans sums
-// m = w, w + nwarps, ...  Each lane first reduces NT/32 consecutive entries.
-__device__ __forceinline__ void osum_scan_run(OsumSmem& s, int M, int NT) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT >> 5;
-  const int per = NT >> 5;
-  for (int m = wid; m < M; m += nw) {
-    double* row = s.run + static_cast<size_t>(m) * NT;
-    double acc = 0.0;
-    for (int i = 0; i < per; ++i) acc = xadd(acc, row[lane * per + i]);
-    double incl = acc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl = xadd(incl, y);
-    }
-    double run = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) run = 0.0;
-    for (int i = 0; i < per; ++i) {
-      const double v = row[lane * per + i];
-      row[lane * per + i] = run;
-      run = xadd(run, v);
-    }
-  }
+// ------------------------------------------------------------- records
+struct OsumBp {
+  Piece p;      // piece before this step (after the fold: since the previous breakpoint)
+  double v;     // the element value
+  int j;        // element index
+  short t;      // owning thread (CTA-local)
+  char first;   // first breakpoint of this lane in the thread's chunk
+  char start;   // the element starts a segment
+  int seg;      // segment id (SEG runs)
+  int pad;
+};
+
+// Global scratch of one cluster: the ranked cluster-wide breakpoint list.
+struct OsumScratch {
+  OsumBp* sorted;  // [L][G*kOsumBpRecs]
+  static __host__ __device__ size_t records(int G) { return static_cast<size_t>(3) * G * kOsumBpRecs; }
+};
+
+// Shared memory of the engine (static size).
+struct OsumShared {
+  OsumBp bp[kOsumBpRecs];
+  double warp_d[32][4];       // phase A warp aggregates: [warp][f, P0..P2]
+  double cta_d[2][4];         // phase A CTA aggregate (double-buffered)
+  Piece warp_p[32][3];
+  int warp_pf[32][3];
+  int warp_pbad[32];
+  Piece cta_p[2][3];
+  int cta_pf[2][3];
+  int nbp[3];
+  int bp_base[3];
+  int nbp_total[3];
+  Piece carry_p[3];
+  Piece fin_p[3];
+  int bad[4];
+  int segpos[kMaxSegs + 1];
+  double result[kMaxSegs];
+  int phase;
+};
+
+// warp-shuffle helpers for the scan payloads
+__device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
+  Piece r;
+  r.A = __shfl_up_sync(0xffffffffu, p.A, o);
+  r.B = __shfl_up_sync(0xffffffffu, p.B, o);
+  r.e = __shfl_up_sync(0xffffffffu, p.e, o);
+  r.tie = __shfl_up_sync(0xffffffffu, p.tie, o);
+  return r;
 }
 
-// Segmented exclusive scan of the per-thread tail pieces (f, e, R) of every
-// sum; afterwards e/R[m][t] hold the piece accumulated since the last
-// breakpoint before thread t, and finR/fine[m] the final piece.
-__device__ __forceinline__ void osum_scan_pieces(OsumSmem& s, int M, int NT) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT >> 5;
-  const int per = NT >> 5;
-  for (int m = wid; m < M; m += nw) {
-    long long* Rr = s.R + static_cast<size_t>(m) * NT;
-    int* er = s.e + static_cast<size_t>(m) * NT;
-    unsigned char* fr = s.f + static_cast<size_t>(m) * NT;
-    // lane aggregate over its run of threads
-    int af = 0, ae = kEmptyE;
-    long long aR = 0;
-    bool ok = true;
-    for (int i = 0; i < per; ++i) {
-      const int t = lane * per + i;
-      if (fr[t]) {
-        af = 1, ae = er[t], aR = Rr[t];
-      } else {
-        int me;
-        ok &= osum_merge_e(ae, er[t], &me);
-        ae = me, aR += Rr[t];
-      }
-    }
-    // warp inclusive scan of the lane aggregates with the segmented operator
-    int sf = af, se = ae;
-    long long sR = aR;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int pf = __shfl_up_sync(0xffffffffu, sf, o);
-      const int pe = __shfl_up_sync(0xffffffffu, se, o);
-      const long long pR = __shfl_up_sync(0xffffffffu, sR, o);
-      if (lane >= o && !sf) {
-        int me;
-        ok &= osum_merge_e(pe, se, &me);
-        sf = pf, se = me, sR += pR;
-      }
-    }
-    // exclusive prefix for this lane
-    int xf = __shfl_up_sync(0xffffffffu, sf, 1), xe = __shfl_up_sync(0xffffffffu, se, 1);
-    long long xR = __shfl_up_sync(0xffffffffu, sR, 1);
-    if (lane == 0) xf = 0, xe = kEmptyE, xR = 0;
-    if (lane == 31) s.finR[m] = sR, s.fine[m] = se;
-    for (int i = 0; i < per; ++i) {
-      const int t = lane * per + i;
-      const int tf = fr[t], te = er[t];
-      const long long tR = Rr[t];
-      er[t] = xe, Rr[t] = xR;  // exclusive value for thread t
-      if (tf) {
-        xf = 1, xe = te, xR = tR;
-      } else {
-        int me;
-        ok &= osum_merge_e(xe, te, &me);
-        xe = me, xR += tR;
-      }
-    }
-    (void)xf;
-    if (!ok) s.bad[m] = 1;
-  }
-}
-
-// The engine.  `contrib(j, emit)` calls emit(m, v) for every sum element j
-// feeds, with v >= 0.  bp: global scratch of M*kOsumBpCap records.
-// Results land in s.result[m].  Must be called by all NT threads.
-// stats (optional, global): [0] calls, [1] sums, [2] sums replayed by the
-// serial fallback, [3] breakpoints, [4] elements
-template <class Contrib>
-__device__ void ordered_sums(int N, int M, const Contrib& contrib, OsumSmem& s, OsumBp* bp,
-                             unsigned long long* stats = nullptr) {
-  const int NT = blockDim.x, t = threadIdx.x;
-  const int C = (N + NT - 1) / NT;
-  const int j0 = min(N, t * C), j1 = min(N, j0 + C);
-  // error of P relative to the true sequential sum: <= (N + 2C + 64) ulp-ish
-  const double delta = static_cast<double>(N + 2 * C + 64) * 2.220446049250313e-16;
+// One run of the engine.
+//   Src::Cursor cur = src.begin(j0);  cur.next(start, seg, has, v)  walks
+//   elements j0, j0+1, ...; `start` marks a segment start (SEG only), `has`
+//   whether the element contributes, v[L] its values (>= 0).
+//   results: SEG -> s.result[seg] for seg < nseg (0 for empty segments);
+//            else s.result[lane].  Visible in every CTA on return.
+// stats (optional, global): [0] runs, [1] lanes/segments, [2] fallbacks,
+// [3] breakpoints, [4] elements, [16+bit] failure reasons.
+template <int L, bool SEG, class Src>
+__device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const OsumScratch& scr,
+                         unsigned long long* stats = nullptr) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int NT = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
+  const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
+  const int GT = G * NT, gt = rank * NT + t;
+  const int C = (N + GT - 1) / GT;
+  const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
+  const double delta = static_cast<double>(N + 2 * C + 96 + G) * 2.220446049250313e-16;
   const double lo_f = 1.0 - delta, hi_f = 1.0 + delta;
+  const int cap_lane = kOsumBpRecs / L;
+  const int buf = s.phase;  // double-buffer index for the CTA aggregates
+  if (t < 3) s.nbp[t] = 0;
+  if (t < 4) s.bad[t] = 0;
+  if (SEG)
+    for (int k = t; k < nseg; k += NT) s.result[k] = 0.0;
+  __syncthreads();
 
-  for (int m = t; m < M; m += NT) s.nbp[m] = 0, s.bad[m] = 0;
-  for (int m = 0; m < M; ++m) {
-    s.run[m * NT + t] = 0.0;
-    s.R[m * NT + t] = 0;
-    s.e[m * NT + t] = kEmptyE;
-    s.f[m * NT + t] = 0;
+  // ---------------- phase A: approximate (segmented) prefix at chunk starts
+  int af = 0;
+  double aP[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) aP[l] = 0.0;
+  {
+    auto cur = src.begin(j0);
+    for (int j = j0; j < j1; ++j) {
+      bool start, has;
+      int seg;
+      double v[L];
+      cur.next(start, seg, has, v);
+      if (SEG && start) {
+        af = 1;
+#pragma unroll
+        for (int l = 0; l < L; ++l) aP[l] = 0.0;
+      }
+      if (has)
+#pragma unroll
+        for (int l = 0; l < L; ++l) aP[l] = xadd(aP[l], v[l]);
+    }
   }
-  // ---- phase A: approximate chunk totals
-  for (int j = j0; j < j1; ++j)
-    contrib(j, [&](int m, double v) { s.run[m * NT + t] = xadd(s.run[m * NT + t], v); });
+  // warp inclusive segmented scan
+  int sf = af;
+  double sP[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) sP[l] = aP[l];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int pf = __shfl_up_sync(0xffffffffu, sf, o);
+    double pP[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) pP[l] = __shfl_up_sync(0xffffffffu, sP[l], o);
+    if (lane >= o && !sf) {
+      sf = pf;
+#pragma unroll
+      for (int l = 0; l < L; ++l) sP[l] = xadd(pP[l], sP[l]);
+    }
+  }
+  if (lane == 31) {
+    s.warp_d[wid][0] = sf;
+#pragma unroll
+    for (int l = 0; l < L; ++l) s.warp_d[wid][1 + l] = sP[l];
+  }
   __syncthreads();
-  osum_scan_run(s, M, NT);
-  __syncthreads();
-  // ---- phase B: classify every step
-  for (int j = j0; j < j1; ++j) {
-    contrib(j, [&](int m, double v) {
-      if (v == 0.0) return;  // fl(S + 0) == S: no effect on the sequence
-      const int k = m * NT + t;
-      const double P = s.run[k];
-      const double Pn = xadd(P, v);
-      s.run[k] = Pn;
-      bool safe = false;
-      long long r = 0;
-      int e = kEmptyE;
-      if (P > 0.0) {
-        e = osum_exp(P);
-        if (e != kEmptyE && e > -1000 && e < 1000 && osum_exp(xmul(P, lo_f)) == e && osum_exp(xmul(Pn, hi_f)) == e) {
-          const double q = scalbn(v, 52 - e);  // exact power-of-two scaling
-          const double fl = floor(q);
-          const double fr = q - fl;  // exact
-          if (fr != 0.5) {
+  if (t == 0) {  // CTA aggregate
+    int f = 0;
+    double P[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) P[l] = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      if (s.warp_d[w][0] != 0.0) {
+        f = 1;
+#pragma unroll
+        for (int l = 0; l < L; ++l) P[l] = s.warp_d[w][1 + l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < L; ++l) P[l] = xadd(P[l], s.warp_d[w][1 + l]);
+      }
+    }
+    s.cta_d[buf][0] = f;
+#pragma unroll
+    for (int l = 0; l < L; ++l) s.cta_d[buf][1 + l] = P[l];
+  }
+  cl.sync();
+  // exclusive prefix for this thread: carry(CTAs < rank) . warps < wid . lanes < lane
+  double xP[L];
+  {
+    int f = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) xP[l] = 0.0;
+    for (int r = 0; r < rank; ++r) {
+      const double* d = cl.map_shared_rank(&s.cta_d[buf][0], r);
+      if (d[0] != 0.0) {
+        f = 1;
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = d[1 + l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = xadd(xP[l], d[1 + l]);
+      }
+    }
+    for (int w = 0; w < wid; ++w) {
+      if (s.warp_d[w][0] != 0.0) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = s.warp_d[w][1 + l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = xadd(xP[l], s.warp_d[w][1 + l]);
+      }
+    }
+    // lanes before me inside the warp: exclusive = inclusive of lane-1
+    const int lf = __shfl_up_sync(0xffffffffu, sf, 1);
+    double lP[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) lP[l] = __shfl_up_sync(0xffffffffu, sP[l], 1);
+    if (lane > 0) {
+      if (lf) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = lP[l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < L; ++l) xP[l] = xadd(xP[l], lP[l]);
+      }
+    }
+    (void)f;
+  }
+
+  // ---------------- phase B: classify every step
+  Piece pc[L];
+  int hadbp[L], firstbp[L];
+  int tbad = 0, tover = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1;
+  {
+    double P[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) P[l] = xP[l];
+    auto cur = src.begin(j0);
+    for (int j = j0; j < j1; ++j) {
+      bool start, has;
+      int seg;
+      double v[L];
+      cur.next(start, seg, has, v);
+      if (SEG && start)
+#pragma unroll
+        for (int l = 0; l < L; ++l) P[l] = 0.0;
+      if (!has) continue;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const double vl = v[l];
+        const double Pp = P[l];
+        const double Pn = xadd(Pp, vl);
+        P[l] = Pn;
+        // a zero step never changes S — except at a segment start, where it
+        // must still open the segment (S = +0 + 0)
+        if (vl == 0.0 && !(SEG && start)) continue;
+        bool safe = false;
+        Piece q;
+        if (Pp > 0.0 && !(SEG && start)) {
+          const int e = osum_exp(Pp);
+          if (e != kEmptyE && e > -960 && e < 960 && osum_exp(xmul(Pp, lo_f)) == e &&
+              osum_exp(xmul(Pn, hi_f)) == e) {
+            const double qv = xmul(vl, osum_pow2(52 - e));  // exact (qv < 2^53)
+            const double fl = floor(qv);
+            const double fr = xsub(qv, fl);
             safe = true;
-            r = static_cast<long long>(fl) + (fr > 0.5 ? 1 : 0);
+            q.e = e;
+            if (fr == 0.5) {
+              q.tie = 1, q.A = static_cast<long long>(fl), q.B = 0;
+            } else {
+              q.tie = 0, q.A = 0, q.B = static_cast<long long>(fl) + (fr > 0.5 ? 1 : 0);
+            }
           }
         }
-      }
-      if (safe) {
-        int me;
-        if (!osum_merge_e(s.e[k], e, &me)) s.bad[m] = 1;
-        s.e[k] = me;
-        s.R[k] += r;
-      } else {
-        const int idx = atomicAdd(&s.nbp[m], 1);
-        if (idx < kOsumBpCap) {
-          OsumBp& b = bp[m * kOsumBpCap + idx];
-          b.R = s.R[k];
-          b.e = s.e[k];
-          b.v = v;
-          b.j = j;
-          b.t = t;
-          b.first = !s.f[k];
+        if (safe) {
+          pc[l] = compose(pc[l], q, &tbad);
         } else {
-          s.bad[m] = 1;
+          const int idx = atomicAdd(&s.nbp[l], 1);
+          if (idx < cap_lane) {
+            OsumBp& b = s.bp[l * cap_lane + idx];
+            b.p = pc[l];
+            b.v = vl;
+            b.j = j;
+            b.t = static_cast<short>(t);
+            b.first = static_cast<char>(!hadbp[l]);
+            b.start = static_cast<char>(SEG && start);
+            b.seg = seg;
+            if (!hadbp[l]) firstbp[l] = idx;
+          } else {
+            tover = 1;
+          }
+          hadbp[l] = 1;
+          pc[l] = piece_identity();
         }
-        s.f[k] = 1;
-        s.R[k] = 0;
-        s.e[k] = kEmptyE;
       }
-    });
+    }
   }
-  __syncthreads();
-  // ---- phase C: segmented scan of pieces
-  osum_scan_pieces(s, M, NT);
+  if (tbad) atomicOr(&s.bad[0], 2);
+  if (tover) atomicOr(&s.bad[0], 4);
+
+  // ---------------- phase C: segmented scan of the pieces (per lane)
+  Piece xp[L];  // exclusive piece before this thread (since the last breakpoint)
+  {
+    int wbad = 0;
+    Piece sp[L];
+    int spf[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) sp[l] = pc[l], spf[l] = hadbp[l];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const Piece pp = shfl_up_piece(sp[l], o);
+        const int pf = __shfl_up_sync(0xffffffffu, spf[l], o);
+        if (lane >= o && !spf[l]) {
+          sp[l] = compose(pp, sp[l], &wbad);
+          spf[l] = pf;
+        }
+      }
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) s.warp_p[wid][l] = sp[l], s.warp_pf[wid][l] = spf[l];
+      s.warp_pbad[wid] = wbad;
+    }
+    __syncthreads();
+    if (t == 0) {
+      int bad = 0;
+      for (int l = 0; l < L; ++l) {
+        Piece a = piece_identity();
+        int f = 0;
+        for (int w = 0; w < nw; ++w) {
+          bad |= s.warp_pbad[w];
+          if (s.warp_pf[w][l]) a = s.warp_p[w][l], f = 1;
+          else a = compose(a, s.warp_p[w][l], &bad);
+        }
+        s.cta_p[buf][l] = a;
+        s.cta_pf[buf][l] = f;
+      }
+      if (bad) atomicOr(&s.bad[0], 8);
+    }
+    cl.sync();
+    // carry from lower CTAs, breakpoint bases, cluster-final piece
+    if (t < L) {
+      const int l = t;
+      Piece a = piece_identity();
+      int base = 0, bad = 0;
+      for (int r = 0; r < G; ++r) {
+        if (r == rank) s.carry_p[l] = a, s.bp_base[l] = base;
+        const Piece rp = *cl.map_shared_rank(&s.cta_p[buf][l], r);
+        const int rf = *cl.map_shared_rank(&s.cta_pf[buf][l], r);
+        base += min(*cl.map_shared_rank(&s.nbp[l], r), cap_lane);
+        if (rf) a = rp;
+        else a = compose(a, rp, &bad);
+      }
+      s.fin_p[l] = a;
+      s.nbp_total[l] = base;
+      if (bad) atomicOr(&s.bad[0], 8);
+    }
+    __syncthreads();
+    // exclusive piece of this thread = carry . warps < wid . lanes < lane
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      Piece a = s.carry_p[l];
+      int bad = 0;
+      for (int w = 0; w < wid; ++w) {
+        if (s.warp_pf[w][l]) a = s.warp_p[w][l];
+        else a = compose(a, s.warp_p[w][l], &bad);
+      }
+      const Piece lp = shfl_up_piece(sp[l], 1);
+      const int lf = __shfl_up_sync(0xffffffffu, spf[l], 1);
+      if (lane > 0) {
+        if (lf) a = lp;
+        else a = compose(a, lp, &bad);
+      }
+      xp[l] = a;
+      if (bad) atomicOr(&s.bad[0], 8);
+    }
+  }
   __syncthreads();
   // fold the carried-in piece into each thread's first breakpoint
-  for (int m = 0; m < M; ++m) {
-    const int n = min(s.nbp[m], kOsumBpCap);
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    if (firstbp[l] >= 0) {
+      OsumBp& b = s.bp[l * cap_lane + firstbp[l]];
+      int bad = 0;
+      b.p = compose(xp[l], b.p, &bad);
+      if (bad) atomicOr(&s.bad[0], 16);
+    }
+  }
+  __syncthreads();
+  // rank each CTA list by element index into the cluster list
+  for (int l = 0; l < L; ++l) {
+    const int n = min(s.nbp[l], cap_lane);
+    OsumBp* out = scr.sorted + static_cast<size_t>(l) * G * cap_lane + s.bp_base[l];
     for (int i = t; i < n; i += NT) {
-      OsumBp& b = bp[m * kOsumBpCap + i];
-      if (!b.first) continue;
-      const int k = m * NT + b.t;
-      int me;
-      if (!osum_merge_e(s.e[k], b.e, &me)) s.bad[m] = 1;
-      b.e = me;
-      b.R += s.R[k];
+      const int ji = s.bp[l * cap_lane + i].j;
+      int rk = 0;
+      for (int q = 0; q < n; ++q) rk += s.bp[l * cap_lane + q].j < ji;
+      out[rk] = s.bp[l * cap_lane + i];
     }
   }
-  __syncthreads();
-  // ---- phase D: rank breakpoints by element index (stable: j is unique per sum)
-  //      rank stored in .t (no longer needed)
-  for (int m = 0; m < M; ++m) {
-    const int n = min(s.nbp[m], kOsumBpCap);
-    for (int i = t; i < n; i += NT) {
-      const int ji = bp[m * kOsumBpCap + i].j;
-      int rank = 0;
-      for (int q = 0; q < n; ++q) rank += bp[m * kOsumBpCap + q].j < ji;
-      bp[m * kOsumBpCap + i].t = rank;
+  if (t == 0 && s.bad[0] && rank != 0) atomicOr(cl.map_shared_rank(&s.bad[0], 0), s.bad[0]);
+  cl.sync();
+
+  // ---------------- phase D: replay on CTA 0
+  if (rank == 0) {
+    const int why = s.bad[0];
+    if (why && t == 0) s.bad[1] = 1;
+    const int nlanes = SEG ? nseg : L;
+    if (SEG) {  // segment -> first breakpoint position
+      for (int k = t; k <= nseg; k += NT) s.segpos[k] = -1;
+      __syncthreads();
+      const OsumBp* list = scr.sorted;
+      for (int q = t; q < s.nbp_total[0]; q += NT)
+        if (list[q].start) s.segpos[list[q].seg] = q;
+      __syncthreads();
     }
-  }
-  __syncthreads();
-  // serial replay, one thread per sum
-  for (int m = t; m < M; m += NT) {
-    double S = 0.0;
-    bool ok = !s.bad[m];
-    const int n = min(s.nbp[m], kOsumBpCap);
-    // walk breakpoints in rank order; ranks are a permutation of 0..n-1
-    for (int rk = 0; rk < n && ok; ++rk) {
-      const OsumBp* b = nullptr;
-      for (int q = 0; q < n; ++q)
-        if (bp[m * kOsumBpCap + q].t == rk) {
-          b = &bp[m * kOsumBpCap + q];
-          break;
+    for (int k = t; k < nlanes; k += NT) {
+      const int l = SEG ? 0 : k;
+      const OsumBp* list = scr.sorted + static_cast<size_t>(l) * G * cap_lane;
+      const int n = s.nbp_total[l];
+      int q0 = 0, q1 = n;
+      if (SEG) {
+        q0 = s.segpos[k];
+        if (q0 < 0) {  // empty segment
+          s.result[k] = 0.0;
+          continue;
         }
-      if (b->e != kEmptyE) {  // a run of safe steps predicted in binade e: verify, then add exactly
-        if (osum_exp(S) != b->e) {
-          ok = false;
-          break;
-        }
-        const double S2 = xadd(S, scalbn(static_cast<double>(b->R), b->e - 52));
-        if (osum_exp(S2) != b->e) {
-          ok = false;
-          break;
-        }
-        S = S2;
+        q1 = q0 + 1;
+        while (q1 < n && !list[q1].start) ++q1;
       }
-      S = xadd(S, b->v);
-    }
-    if (ok && s.fine[m] != kEmptyE) {
-      if (osum_exp(S) != s.fine[m]) {
-        ok = false;
-      } else {
-        const double S2 = xadd(S, scalbn(static_cast<double>(s.finR[m]), s.fine[m] - 52));
-        if (osum_exp(S2) != s.fine[m]) ok = false;
-        else S = S2;
-      }
-    }
-    s.result[m] = S;
-    s.bad[m] = ok ? 0 : 1;
-  }
-  __syncthreads();
-  if (stats && t == 0) {
-    unsigned long long nb = 0, nbad = 0;
-    for (int m = 0; m < M; ++m) nb += s.nbp[m], nbad += s.bad[m];
-    atomicAdd(&stats[0], 1ull);
-    atomicAdd(&stats[1], static_cast<unsigned long long>(M));
-    atomicAdd(&stats[2], nbad);
-    atomicAdd(&stats[3], nb);
-    atomicAdd(&stats[4], static_cast<unsigned long long>(N));
-  }
-  // exact serial fallback for any sum whose prediction failed
-  for (int m = 0; m < M; ++m) {
-    if (!s.bad[m]) continue;  // uniform across the block
-    if (t == 0) {
+      bool ok = !why;
       double S = 0.0;
-      for (int j = 0; j < N; ++j)
-        contrib(j, [&](int mm, double v) {
-          if (mm == m) S = xadd(S, v);
-        });
-      s.result[m] = S;
+      auto run_piece = [&](const Piece& p) {
+        if (p.e == kEmptyE) return;
+        if (osum_exp(S) != p.e) {
+          ok = false;
+          return;
+        }
+        const long long X = static_cast<long long>(xmul(S, osum_pow2(52 - p.e)));
+        const long long X2 = apply(p, X);
+        if (X2 < (1LL << 52) || X2 >= (1LL << 53)) {
+          ok = false;
+          return;
+        }
+        S = xmul(static_cast<double>(X2), osum_pow2(p.e - 52));
+      };
+      for (int q = q0; q < q1 && ok; ++q) {
+        const OsumBp b = list[q];
+        if (q > q0 || !SEG) run_piece(b.p);  // a segment start's piece belongs to the previous segment
+        S = xadd(S, b.v);
+      }
+      if (ok) run_piece((SEG && q1 < n) ? list[q1].p : s.fin_p[l]);
+      s.result[k] = S;
+      if (!ok) atomicOr(&s.bad[1], 1);
     }
+    __syncthreads();
+    if (stats && t == 0) {
+      atomicAdd(&stats[0], 1ull);
+      atomicAdd(&stats[1], static_cast<unsigned long long>(nlanes));
+      unsigned long long nb = 0;
+      for (int l = 0; l < L; ++l) nb += s.nbp_total[l];
+      atomicAdd(&stats[3], nb);
+      atomicAdd(&stats[4], static_cast<unsigned long long>(N));
+      for (int bit = 0; bit < 8; ++bit)
+        if (why & (1 << bit)) atomicAdd(&stats[16 + bit], 1ull);
+      if (s.bad[1]) atomicAdd(&stats[2], 1ull);
+    }
+    // exact serial fallback (all lanes / segments) if anything failed
+    if (s.bad[1]) {
+      if (t == 0) {
+        double S[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) S[l] = 0.0;
+        auto cur = src.begin(0);
+        int cs = -1;
+        for (int j = 0; j < N; ++j) {
+          bool start, has;
+          int seg;
+          double v[L];
+          cur.next(start, seg, has, v);
+          if (SEG && start) {
+            if (cs >= 0) s.result[cs] = S[0];
+            cs = seg;
+            S[0] = 0.0;
+          }
+          if (!has) continue;
+#pragma unroll
+          for (int l = 0; l < L; ++l) S[l] = xadd(S[l], v[l]);
+        }
+        if (SEG) {
+          for (int k = 0; k < nseg; ++k)
+            if (s.segpos[k] < 0) s.result[k] = 0.0;
+          if (cs >= 0) s.result[cs] = S[0];
+        } else {
+#pragma unroll
+          for (int l = 0; l < L; ++l) s.result[l] = S[l];
+        }
+      }
+      __syncthreads();
+    }
+    for (int r = 1; r < G; ++r)
+      for (int k = t; k < nlanes; k += NT) *cl.map_shared_rank(&s.result[k], r) = s.result[k];
   }
-  __syncthreads();
+  if (t == 0) s.phase = buf ^ 1;
+  cl.sync();
 }
 
 }  // namespace trb

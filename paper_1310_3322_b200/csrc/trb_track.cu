@@ -10,7 +10,8 @@ namespace trb {
 // Device-side diagnostics: [0..4] ordered_sums stats (see trb_osum.cuh),
 // [5] mean-shift iterations, [6] spawns, [7] Lloyd iterations, [8] farthest
 // point passes, [9] tracks advanced.
-__device__ unsigned long long g_trb_stats[16];
+// [16..25] ordered_sums failure reasons (bit index of the `bad` mask).
+__device__ unsigned long long g_trb_stats[32];
 
 namespace {
 
@@ -60,70 +61,20 @@ __device__ __forceinline__ int q_assign(const double* c, int k, double r, double
   return best;
 }
 
-// Everything one CTA needs to walk a window of one frame.
-struct WinCtx {
-  const uint8_t* frame;
-  int fw, fh, ch;
-  int x0, y0, ww, wh;
-  UDiv32 dv;
-  const double* ux2;  // [ww] ((x-cx)/hx)^2
-  const double* uy2;  // [wh]
-  const double* centers;
-  const uint8_t* lut;  // gray -> bin, or nullptr
-  int K;
-  __device__ __forceinline__ int bin_at(int x, int y) const {
-    if (ch == 1) {
-      const int v = frame[static_cast<int64_t>(y) * fw + x];
-      if (lut) return lut[v];
-      const double dv_ = v;
-      return q_assign(centers, K, dv_, dv_, dv_);
-    }
-    const uint8_t* p = frame + (static_cast<int64_t>(y) * fw + x) * 3;
-    return q_assign(centers, K, p[0], p[1], p[2]);
+// Per-cluster global scratch of the tracker kernels.
+struct TrackScratch {
+  OsumScratch os;
+  double* vals;    // [maxN] positive Epanechnikov weights, partitioned by bin
+  uint8_t* bins;   // [maxN] bin of every window pixel (raster order)
+  static __host__ __device__ size_t bytes(int G, int64_t maxN) {
+    return sizeof(OsumBp) * OsumScratch::records(G) + sizeof(double) * maxN + maxN + 256;
   }
 };
 
-// histogram_opt's loop body (tracking.hpp:86-98): element j of the window
-// feeds hist[bin] and total with the Epanechnikov (or uniform) weight.
-struct HistContrib {
-  WinCtx c;
-  int epan;
-  template <class F>
-  __device__ __forceinline__ void operator()(int j, F&& emit) const {
-    const int yy = static_cast<int>(c.dv.div(static_cast<uint32_t>(j)));
-    const int xx = j - yy * c.ww;
-    double wgt = 1.0;
-    if (epan) {
-      const double t = xsub(1.0, xadd(c.ux2[xx], c.uy2[yy]));
-      wgt = (0.0 < t) ? t : 0.0;  // std::max(0.0, t)
-    }
-    if (wgt <= 0.0) return;
-    const int b = c.bin_at(c.x0 + xx, c.y0 + yy);
-    emit(b, wgt);
-    emit(c.K, wgt);
-  }
-};
-
-// meanshift_step's centroid body (tracking.hpp:136-146).
-struct MsContrib {
-  WinCtx c;
-  const double* wsq;  // sqrt(q[b]/p[b]), or < 0 when p[b] <= 0
-  template <class F>
-  __device__ __forceinline__ void operator()(int j, F&& emit) const {
-    const int yy = static_cast<int>(c.dv.div(static_cast<uint32_t>(j)));
-    const int xx = j - yy * c.ww;
-    const int x = c.x0 + xx, y = c.y0 + yy;
-    const double w = wsq[c.bin_at(x, y)];
-    if (w < 0.0) return;
-    emit(0, w);
-    emit(1, xmul(w, static_cast<double>(x)));
-    emit(2, xmul(w, static_cast<double>(y)));
-  }
-};
-
-// Shared-memory map for the tracker CTAs (dynamic).
+// Shared-memory map for the tracker CTAs (dynamic part; the engine's
+// OsumShared is static).
 struct TrackSmem {
-  OsumSmem os;
+  OsumShared* os;
   double* ux2;   // [W]
   double* uy2;   // [H]
   double* cen;   // [K*3]
@@ -131,22 +82,20 @@ struct TrackSmem {
   double* q;     // [K]
   double* p;     // [K]
   double* wsq;   // [K]
-  uint8_t* lut;  // [256]
   double* scal;  // [16] broadcast scalars
+  long long* red;  // [2*NT] reduction scratch
+  int* cnt;      // [K][NT] per-thread bin counts, then scatter cursors
+  int* binoff;   // [K+1] bin offsets in the partitioned sequence
+  int* bincta;   // [K] this CTA's per-bin totals
   int* iscal;    // [16]
-  long long* red;  // [NT] reduction scratch (int64 / doubles reinterpret)
+  uint8_t* lut;  // [256]
   static size_t bytes(int K, int W, int H) {
-    size_t b = OsumSmem::bytes(K + 1, NT);
-    b = (b + 15) & ~size_t(15);
-    // ux2, uy2, cen, old, q, p, wsq, scal, red, iscal, lut — each region
-    // rounded up to 16 bytes by carve()
-    b += sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT + sizeof(int) * 16 + 256 + 11 * 16;
-    return b;
+    return sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT + sizeof(int) * (K * NT + 2 * K + 1 + 16) +
+           256 + 16 * 16;
   }
-  __device__ void carve(void* base, int K, int W, int H) {
-    os.carve(base, K + 1, NT);
-    size_t off = (OsumSmem::bytes(K + 1, NT) + 15) & ~size_t(15);
-    char* p_ = static_cast<char*>(base) + off;
+  __device__ void carve(void* base, OsumShared* osh, int K, int W, int H) {
+    os = osh;
+    char* p_ = static_cast<char*>(base);
     auto take = [&](size_t n) {
       char* r = p_;
       p_ += (n + 15) & ~size_t(15);
@@ -161,8 +110,12 @@ struct TrackSmem {
     wsq = reinterpret_cast<double*>(take(sizeof(double) * K));
     scal = reinterpret_cast<double*>(take(sizeof(double) * 16));
     red = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * NT));
+    cnt = reinterpret_cast<int*>(take(sizeof(int) * K * NT));
+    binoff = reinterpret_cast<int*>(take(sizeof(int) * (K + 1)));
+    bincta = reinterpret_cast<int*>(take(sizeof(int) * K));
     iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
     lut = reinterpret_cast<uint8_t*>(take(256));
+    if (threadIdx.x == 0) osh->phase = 0;
   }
 };
 
@@ -180,34 +133,182 @@ __device__ void fill_u2(TrackSmem& sm, const Win& r, double cx, double cy, int w
   }
 }
 
-__device__ WinCtx make_ctx(const uint8_t* frame, int fw, int fh, int ch, const Win& r, TrackSmem& sm, int K,
-                           bool use_lut) {
-  WinCtx c;
-  c.frame = frame;
-  c.fw = fw, c.fh = fh, c.ch = ch;
-  c.x0 = r.x0, c.y0 = r.y0, c.ww = r.x1 - r.x0, c.wh = r.y1 - r.y0;
-  c.dv = UDiv32::make(static_cast<uint32_t>(c.ww));
-  c.ux2 = sm.ux2, c.uy2 = sm.uy2;
-  c.centers = sm.cen;
-  c.lut = use_lut ? sm.lut : nullptr;
-  c.K = K;
-  return c;
+__device__ __forceinline__ double epan_weight(const TrackSmem& sm, int xx, int yy, int epan) {
+  if (!epan) return 1.0;
+  const double t = xsub(1.0, xadd(sm.ux2[xx], sm.uy2[yy]));
+  return (0.0 < t) ? t : 0.0;  // std::max(0.0, t)
+}
+
+// --- element sources for the engine (cursor walks from j0 upward) ---
+// histogram total: every window pixel in raster order, weight > 0
+struct TotalSrc {
+  const TrackSmem* sm;
+  int ww, epan;
+  struct Cursor {
+    const TotalSrc* s;
+    int xx, yy;
+    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
+      const double w = epan_weight(*s->sm, xx, yy, s->epan);
+      start = false, seg = 0, has = w > 0.0, v[0] = w;
+      if (++xx == s->ww) xx = 0, ++yy;
+    }
+  };
+  __device__ Cursor begin(int j0) const { return Cursor{this, j0 % ww, j0 / ww}; }
+};
+
+// histogram bins: the positive weights stably partitioned by bin; one
+// segment per non-empty bin
+struct BinsSrc {
+  const double* vals;
+  const int* off;  // [K+1]
+  int K;
+  struct Cursor {
+    const BinsSrc* s;
+    int j, b;
+    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
+      while (j >= s->off[b + 1]) ++b;
+      start = (j == s->off[b]), seg = b, has = true, v[0] = s->vals[j];
+      ++j;
+    }
+  };
+  __device__ Cursor begin(int j0) const {
+    int b = 0;
+    while (b < K - 1 && off[b + 1] <= j0) ++b;
+    return Cursor{this, j0, b};
+  }
+};
+
+// mean-shift centroid: every window pixel, weight sqrt(q/p) of its bin
+struct CentroidSrc {
+  const uint8_t* bins;
+  const double* wsq;  // < 0 when p[b] <= 0
+  int x0, y0, ww;
+  struct Cursor {
+    const CentroidSrc* s;
+    int j, xx, yy;
+    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
+      const double w = s->wsq[s->bins[j]];
+      start = false, seg = 0, has = w >= 0.0;
+      v[0] = w;
+      v[1] = xmul(w, static_cast<double>(s->x0 + xx));
+      v[2] = xmul(w, static_cast<double>(s->y0 + yy));
+      ++j;
+      if (++xx == s->ww) xx = 0, ++yy;
+    }
+  };
+  __device__ Cursor begin(int j0) const { return Cursor{this, j0, j0 % ww, j0 / ww}; }
+};
+
+__device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int x, int y, const TrackSmem& sm, int K,
+                                      bool use_lut) {
+  if (ch == 1) {
+    const int v = frame[static_cast<int64_t>(y) * fw + x];
+    if (use_lut) return sm.lut[v];
+    const double d = v;
+    return q_assign(sm.cen, K, d, d, d);
+  }
+  const uint8_t* p = frame + (static_cast<int64_t>(y) * fw + x) * 3;
+  return q_assign(sm.cen, K, p[0], p[1], p[2]);
+}
+
+// Bin every window pixel (cached for the centroid pass) and stably
+// partition the positive-weight pixels by bin across the cluster:
+// sm.binoff[b] = start of bin b, scratch.vals = weights in (bin, raster)
+// order.  Returns the number of positive-weight pixels.
+__device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win& r, int K, int epan, bool use_lut,
+                                TrackSmem& sm, const TrackScratch& scr) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int NT_ = blockDim.x, t = threadIdx.x;
+  const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
+  const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
+  const int GT = G * NT_, C = (N + GT - 1) / GT;
+  const int j0 = min(N, (rank * NT_ + t) * C), j1 = min(N, j0 + C);
+  for (int b = 0; b < K; ++b) sm.cnt[b * NT_ + t] = 0;
+  {
+    int xx = j0 % ww, yy = j0 / ww;
+    for (int j = j0; j < j1; ++j) {
+      const int b = bin_of(frame, fw, ch, r.x0 + xx, r.y0 + yy, sm, K, use_lut);
+      scr.bins[j] = static_cast<uint8_t>(b);
+      if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1;
+      if (++xx == ww) xx = 0, ++yy;
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the counts of every bin over the CTA's threads
+  const int lane = t & 31, wid = t >> 5, nw = NT_ >> 5, per = NT_ >> 5;
+  for (int b = wid; b < K; b += nw) {
+    int* row = sm.cnt + b * NT_;
+    int acc = 0;
+    for (int i = 0; i < per; ++i) acc += row[lane * per + i];
+    int incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int run = incl - acc;
+    if (lane == 31) sm.bincta[b] = incl;
+    for (int i = 0; i < per; ++i) {
+      const int v = row[lane * per + i];
+      row[lane * per + i] = run;
+      run += v;
+    }
+  }
+  cl.sync();
+  // bin offsets (cluster totals) and this CTA's carry per bin
+  if (t == 0) {
+    int off = 0;
+    for (int b = 0; b < K; ++b) {
+      int carry = 0, tot = 0;
+      for (int q = 0; q < G; ++q) {
+        const int c = *cl.map_shared_rank(&sm.bincta[b], q);
+        if (q < rank) carry += c;
+        tot += c;
+      }
+      sm.binoff[b] = off;
+      sm.red[b] = off + carry;  // where this CTA's bin-b run starts
+      off += tot;
+    }
+    sm.binoff[K] = off;
+  }
+  __syncthreads();
+  for (int b = 0; b < K; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
+  {
+    int xx = j0 % ww, yy = j0 / ww;
+    for (int j = j0; j < j1; ++j) {
+      const double w = epan_weight(sm, xx, yy, epan);
+      if (w > 0.0) {
+        const int b = scr.bins[j];
+        scr.vals[sm.cnt[b * NT_ + t]++] = w;
+      }
+      if (++xx == ww) xx = 0, ++yy;
+    }
+  }
+  cl.sync();  // every CTA reads the other CTAs' bincta before it is reused; vals complete
+  return sm.binoff[K];
 }
 
 // histogram_opt (tracking.hpp:79-102) with the quantizer in sm.cen (and
 // sm.lut when use_lut).  Writes the normalised histogram to out[K];
-// returns false for std::nullopt.  Block-uniform.
+// returns false for std::nullopt.  Cluster-uniform.
 __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, double cx, double cy, int w, int h,
-                                 int K, int epan, bool use_lut, TrackSmem& sm, OsumBp* bp, double* out) {
+                                 int K, int epan, bool use_lut, TrackSmem& sm, const TrackScratch& scr, double* out) {
   const Win r = clip_window(fw, fh, cx, cy, w, h);
   if (r.empty()) return false;
   fill_u2(sm, r, cx, cy, w, h);
   __syncthreads();
-  HistContrib hc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), epan};
-  ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), K + 1, hc, sm.os, bp, g_trb_stats);
-  const double total = sm.os.result[K];
-  if (total <= 0.0) return false;
-  for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os.result[b], total);
+  const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
+  const int npos = partition_window(frame, fw, ch, r, K, epan, use_lut, sm, scr);
+  // total (raster order) and per-bin (partitioned order) sequential sums
+  TotalSrc ts{&sm, ww, epan};
+  osum_run<1, false>(N, 0, ts, *sm.os, scr.os, g_trb_stats);
+  const double total = sm.os->result[0];
+  if (npos > 0) {
+    BinsSrc bs{scr.vals, sm.binoff, K};
+    osum_run<1, true>(npos, K, bs, *sm.os, scr.os, g_trb_stats);
+  }
+  if (!(total > 0.0)) return false;
+  for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os->result[b], total);
   __syncthreads();
   return true;
 }
@@ -216,12 +317,12 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
 // sm.cen / sm.q (and sm.lut).  cx, cy, status updated in place (uniform).
 __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, double& cx, double& cy, int w, int h,
                                  int& status, int K, int max_iters, double eps, bool use_lut, TrackSmem& sm,
-                                 OsumBp* bp) {
+                                 const TrackScratch& scr) {
   if (status != TRB_TRACK_ACTIVE) return;
   if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
   for (int it = 0; it < max_iters; ++it) {
     if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull);
-    const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, bp, sm.p);
+    const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
     if (threadIdx.x == 0) {
       int lost = !ok;
       if (ok) {
@@ -237,10 +338,11 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
       status = TRB_TRACK_LOST;
       return;
     }
+    // the window is the same (same cx, cy); its bins are cached in scr.bins
     const Win r = clip_window(fw, fh, cx, cy, w, h);
-    MsContrib mc{make_ctx(frame, fw, fh, ch, r, sm, K, use_lut), sm.wsq};
-    ordered_sums((r.x1 - r.x0) * (r.y1 - r.y0), 3, mc, sm.os, bp, g_trb_stats);
-    const double sw = sm.os.result[0], sx = sm.os.result[1], sy = sm.os.result[2];
+    CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0};
+    osum_run<3, false>((r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, scr.os, g_trb_stats);
+    const double sw = sm.os->result[0], sx = sm.os->result[1], sy = sm.os->result[2];
     __syncthreads();
     if (sw <= 0.0) {
       status = TRB_TRACK_LOST;
@@ -468,15 +570,33 @@ __device__ __forceinline__ int64_t slot_index(const TrackDev& d, int s, int slot
 }  // namespace
 
 // ------------------------------------------------------------ meanshift
-// Persistent grid over (stream, list position) items; one CTA per track.
+// Persistent grid of thread-block clusters over (stream, list position)
+// items; one CLUSTER per track, its window split across the cluster's CTAs.
+__device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, size_t stride, int64_t maxN) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = static_cast<int>(cl.num_blocks());
+  const int cid = blockIdx.x / G;
+  unsigned char* p = base + static_cast<size_t>(cid) * stride;
+  TrackScratch s;
+  s.os.sorted = reinterpret_cast<OsumBp*>(p);
+  s.vals = reinterpret_cast<double*>(p + sizeof(OsumBp) * OsumScratch::records(G));
+  s.bins = reinterpret_cast<uint8_t*>(s.vals + maxN);
+  return s;
+}
+
 __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ OsumShared osh;
+  cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
-  sm.carve(smem_raw, d.K, d.W, d.H);
-  OsumBp* bp = d.bp + static_cast<int64_t>(blockIdx.x) * (d.K + 1) * kOsumBpCap;
+  sm.carve(smem_raw, &osh, d.K, d.W, d.H);
   const int K = d.K;
+  const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
+  const int G = static_cast<int>(cl.num_blocks());
+  const int cid = blockIdx.x / G, ncl = gridDim.x / G;
   const bool gray = d.CH == 1;
-  for (int item = blockIdx.x; item < d.S * d.T; item += gridDim.x) {
+  const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
+  for (int item = cid; item < d.S * d.T; item += ncl) {
     const int s = item / d.T, i = item - s * d.T;
     if (i >= d.n_list[s]) continue;
     const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
@@ -489,17 +609,18 @@ __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
       for (int k = threadIdx.x; k < 256; k += NT) sm.lut[k] = d.lut[g * 256 + k];
     __syncthreads();
     double cx = d.cx[g], cy = d.cy[g];
-    meanshift_device(d.frames[s], d.W, d.H, d.CH, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, gray, sm, bp);
-    if (threadIdx.x == 0) {
+    meanshift_device(d.frames[s], d.W, d.H, d.CH, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, gray, sm,
+                     scr);
+    cl.sync();  // every CTA has read the track before the leader updates it
+    if (lead) {
       d.cx[g] = cx;
       d.cy[g] = cy;
       d.status[g] = status;
     }
-    __syncthreads();
   }
 }
 
-// ----------------------------------------------------------------- gate
+// ---------------------------------------------------------------- gate
 // One CTA per stream: spawn gating (tracking.hpp:185-195), spawn_track's
 // geometry and success conditions (:208-234), lost counting and retirement
 // (:197-201) and the log (:203-204).
@@ -652,35 +773,48 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
 }
 
 // ---------------------------------------------------------------- spawn
-// One CTA per pending track: quantize_colors on the window pixels with
-// seed mix_seed(cfg.seed, id) (tracking.hpp:221-229), then the target
+// One cluster per pending track: quantize_colors on the window pixels with
+// seed mix_seed(cfg.seed, id) (tracking.hpp:221-229) on the leader CTA, the
+// centres broadcast through DSMEM, then the cluster-parallel target
 // histogram (:230-232) and the gray->bin table.
 __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Mt64 rng;
+  __shared__ OsumShared osh;
+  cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
-  sm.carve(smem_raw, d.K, d.W, d.H);
-  OsumBp* bp = d.bp + static_cast<int64_t>(blockIdx.x) * (d.K + 1) * kOsumBpCap;
+  sm.carve(smem_raw, &osh, d.K, d.W, d.H);
   const int K = d.K;
+  const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
+  const int G = static_cast<int>(cl.num_blocks());
+  const int cid = blockIdx.x / G, ncl = gridDim.x / G;
+  const int rank = static_cast<int>(cl.block_rank());
   const bool gray = d.CH == 1;
-  for (int item = blockIdx.x; item < d.S * d.T; item += gridDim.x) {
+  for (int item = cid; item < d.S * d.T; item += ncl) {
     const int s = item / d.T, slot = item - s * d.T;
     const int64_t g = slot_index(d, s, slot);
     if (!d.pending[g]) continue;
     const double cx = d.cx[g], cy = d.cy[g];
     const int w = d.w[g], h = d.h[g];
-    const Win r = clip_window(d.W, d.H, cx, cy, w, h);
-    FrameWindowSrc src{d.frames[s], d.W, d.CH, r.x0, r.y0, r.x1 - r.x0, UDiv32::make(r.x1 - r.x0)};
-    const int n = (r.x1 - r.x0) * (r.y1 - r.y0);
-    kmeans_device(src, n, K, d.kmeans_iters, mix_seed(d.seed, static_cast<uint64_t>(d.id[g])), sm, &rng);
+    if (rank == 0) {
+      const Win r = clip_window(d.W, d.H, cx, cy, w, h);
+      FrameWindowSrc src{d.frames[s], d.W, d.CH, r.x0, r.y0, r.x1 - r.x0, UDiv32::make(r.x1 - r.x0)};
+      const int n = (r.x1 - r.x0) * (r.y1 - r.y0);
+      kmeans_device(src, n, K, d.kmeans_iters, mix_seed(d.seed, static_cast<uint64_t>(d.id[g])), sm, &rng);
+      for (int rr = 1; rr < G; ++rr)
+        for (int k = threadIdx.x; k < 3 * K; k += NT) *cl.map_shared_rank(&sm.cen[k], rr) = sm.cen[k];
+    }
+    cl.sync();
     if (gray) build_lut(sm, K);
-    window_histogram(d.frames[s], d.W, d.H, d.CH, cx, cy, w, h, K, 1, gray, sm, bp, sm.q);
-    for (int k = threadIdx.x; k < 3 * K; k += NT) d.centers[g * 3 * K + k] = sm.cen[k];
-    for (int k = threadIdx.x; k < K; k += NT) d.hist[g * K + k] = sm.q[k];
-    if (gray)
-      for (int k = threadIdx.x; k < 256; k += NT) d.lut[g * 256 + k] = sm.lut[k];
-    if (threadIdx.x == 0) d.pending[g] = 0;
-    __syncthreads();
+    window_histogram(d.frames[s], d.W, d.H, d.CH, cx, cy, w, h, K, 1, gray, sm, scr, sm.q);
+    if (rank == 0) {
+      for (int k = threadIdx.x; k < 3 * K; k += NT) d.centers[g * 3 * K + k] = sm.cen[k];
+      for (int k = threadIdx.x; k < K; k += NT) d.hist[g * K + k] = sm.q[k];
+      if (gray)
+        for (int k = threadIdx.x; k < 256; k += NT) d.lut[g * 256 + k] = sm.lut[k];
+    }
+    cl.sync();  // all CTAs have read `pending` and the slot before it is cleared
+    if (rank == 0 && threadIdx.x == 0) d.pending[g] = 0;
   }
 }
 
@@ -694,28 +828,37 @@ struct OneArgs {
   const double* centers;  // device K*3
   const double* target;   // device K
   double* out;            // device: [cx, cy, status, ok] or hist[K] + ok
-  OsumBp* bp;
+  unsigned char* scratch;
+  size_t scratch_stride;
+  int64_t maxN;
 };
 
+// One cluster: meanshift_step or histogram_opt on a single explicit track.
 __global__ void __launch_bounds__(NT) track_one_kernel(OneArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ OsumShared osh;
   TrackSmem sm;
-  sm.carve(smem_raw, a.K, a.W, a.H);
+  sm.carve(smem_raw, &osh, a.K, a.W, a.H);
+  const TrackScratch scr = cluster_scratch(a.scratch, a.scratch_stride, a.maxN);
   for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
   if (a.target)
     for (int k = threadIdx.x; k < a.K; k += NT) sm.q[k] = a.target[k];
   __syncthreads();
   const bool gray = a.CH == 1;
   if (gray) build_lut(sm, a.K);
+  const bool lead = cl.block_rank() == 0;
   if (a.mode == 0) {
     double cx = a.cx, cy = a.cy;
     int status = a.status;
-    meanshift_device(a.frame, a.W, a.H, a.CH, cx, cy, a.w, a.h, status, a.K, a.max_iters, a.eps, gray, sm, a.bp);
-    if (threadIdx.x == 0) a.out[0] = cx, a.out[1] = cy, a.out[2] = status;
+    meanshift_device(a.frame, a.W, a.H, a.CH, cx, cy, a.w, a.h, status, a.K, a.max_iters, a.eps, gray, sm, scr);
+    if (lead && threadIdx.x == 0) a.out[0] = cx, a.out[1] = cy, a.out[2] = status;
   } else {
-    const bool ok = window_histogram(a.frame, a.W, a.H, a.CH, a.cx, a.cy, a.w, a.h, a.K, a.epan, gray, sm, a.bp, sm.p);
-    for (int k = threadIdx.x; k < a.K; k += NT) a.out[k] = sm.p[k];
-    if (threadIdx.x == 0) a.out[a.K] = ok ? 1.0 : 0.0;
+    const bool ok = window_histogram(a.frame, a.W, a.H, a.CH, a.cx, a.cy, a.w, a.h, a.K, a.epan, gray, sm, scr, sm.p);
+    if (lead) {
+      for (int k = threadIdx.x; k < a.K; k += NT) a.out[k] = sm.p[k];
+      if (threadIdx.x == 0) a.out[a.K] = ok ? 1.0 : 0.0;
+    }
   }
 }
 
@@ -723,17 +866,18 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
                                                       double* out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Mt64 rng;
+  __shared__ OsumShared osh;
   TrackSmem sm;
-  sm.carve(smem_raw, K, 1, 1);
+  sm.carve(smem_raw, &osh, K, 1, 1);
   kmeans_device(ListSrc{px}, n, K, iters, seed, sm, &rng);
   for (int k = threadIdx.x; k < 3 * K; k += NT) out[k] = sm.cen[k];
 }
 
 // ------------------------------------------------------------- host side
 void read_debug_stats(unsigned long long* out, bool reset) {
-  TRB_CUDA(cudaMemcpyFromSymbol(out, g_trb_stats, sizeof(unsigned long long) * 16));
+  TRB_CUDA(cudaMemcpyFromSymbol(out, g_trb_stats, sizeof(unsigned long long) * 32));
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[32] = {};
     TRB_CUDA(cudaMemcpyToSymbol(g_trb_stats, z, sizeof(z)));
   }
 }
@@ -744,10 +888,65 @@ static void set_smem(const void* fn, size_t bytes) {
 
 static size_t check_smem(int K, int W, int H) {
   const size_t b = TrackSmem::bytes(K, W, H);
-  if (b > 220 * 1024)
+  if (b > 200 * 1024)
     throw Error(TRB_CONFIG_ERROR, "tracker k_clusters / frame size exceed the device shared-memory budget");
   if (4 * K > 2 * NT) throw Error(TRB_CONFIG_ERROR, "tracker k_clusters too large for the device k-means");
   return b;
+}
+
+// Cluster size of the tracker kernels (CTAs per track).  TRB_CLUSTER
+// overrides; sizes above 8 use the non-portable cluster attribute.
+static int cluster_size() {
+  static int g = [] {
+    const char* e = getenv("TRB_CLUSTER");
+    int v = e ? atoi(e) : 8;
+    return std::max(1, std::min(v, kMaxCluster));
+  }();
+  return g;
+}
+
+template <typename Kern>
+static void prepare_cluster_kernel(Kern kern, size_t smem, int G) {
+  set_smem(reinterpret_cast<const void*>(kern), smem);
+  if (G > 8)
+    TRB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+// Number of G-CTA clusters that can be co-resident for `kern`.
+template <typename Kern>
+static int max_clusters(Kern kern, size_t smem, int G) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G * 64);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  TRB_CUDA(cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(kern), &cfg));
+  return std::max(1, n);
+}
+
+template <typename Arg>
+static void launch_cluster(void (*kern)(Arg), int n_clusters, int G, size_t smem, cudaStream_t st, Arg arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_clusters * G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TRB_CUDA(cudaLaunchKernelEx(&cfg, kern, arg));
 }
 
 TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, int64_t log_cap)
@@ -760,8 +959,8 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   lut_.alloc(static_cast<size_t>(n) * 256);
   log_.alloc(sizeof(trb_track_log_entry) * log_cap_ * S, false);
   nlog_.alloc(sizeof(int64_t) * S);
-  grid_ = static_cast<int>(std::min<int64_t>(n, 2 * 148));
-  bp_.alloc(sizeof(OsumBp) * static_cast<size_t>(grid_) * (K_ + 1) * kOsumBpCap, false);
+  // the cluster grid and breakpoint scratch are sized at the first process()
+  // call, once the frame geometry (shared-memory need) is known
   int32_t* p = i32_.as<int32_t>();
   d_.S = S, d_.T = T_, d_.K = K_;
   d_.max_iters = cfg.max_iters, d_.kmeans_iters = cfg.kmeans_iters, d_.eps = cfg.eps, d_.seed = cfg.seed;
@@ -775,7 +974,6 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   d_.log = log_.as<trb_track_log_entry>();
   d_.log_cap = log_cap_;
   d_.n_log = nlog_.as<int64_t>();
-  d_.bp = bp_.as<OsumBp>();
   // next_id starts at 1 (tracking.hpp:239)
   std::vector<int32_t> ones(S, 1);
   TRB_CUDA(cudaMemcpy(d_.next_id, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
@@ -796,17 +994,22 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   d_.nblobs = nblobs;
   d_.matched = matched_.as<uint8_t>();
   const size_t smem = check_smem(K_, w, h);
+  const int G = cluster_size();
   if (smem != smem_set_) {
-    set_smem(reinterpret_cast<const void*>(track_meanshift_kernel), smem);
-    set_smem(reinterpret_cast<const void*>(track_spawn_kernel), smem);
+    prepare_cluster_kernel(track_meanshift_kernel, smem, G);
+    prepare_cluster_kernel(track_spawn_kernel, smem, G);
+    const int64_t items = static_cast<int64_t>(S_) * T_;
+    grid_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift_kernel, smem, G)));
+    d_.maxN = static_cast<int64_t>(w) * h;
+    d_.scratch_stride = (TrackScratch::bytes(G, d_.maxN) + 255) & ~size_t(255);
+    bp_.alloc(d_.scratch_stride * static_cast<size_t>(grid_), false);
+    d_.scratch = bp_.as<unsigned char>();
     smem_set_ = smem;
   }
-  track_meanshift_kernel<<<grid_, NT, smem, st>>>(d_);
-  TRB_LAUNCH_CHECK("track_meanshift_kernel");
+  launch_cluster(track_meanshift_kernel, grid_, G, smem, st, d_);
   track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
-  track_spawn_kernel<<<grid_, NT, smem, st>>>(d_);
-  TRB_LAUNCH_CHECK("track_spawn_kernel");
+  launch_cluster(track_spawn_kernel, grid_, G, smem, st, d_);
   *launches += 3;
 }
 
@@ -892,10 +1095,18 @@ static DevBuf& scratch_bp() {
   return b;
 }
 
-static OsumBp* bp_for(int K) {
+static void scratch_for(OneArgs& a) {
   DevBuf& b = scratch_bp();
-  b.alloc(sizeof(OsumBp) * (K + 1) * kOsumBpCap, false);
-  return b.as<OsumBp>();
+  a.maxN = static_cast<int64_t>(a.W) * a.H;
+  a.scratch_stride = (TrackScratch::bytes(cluster_size(), a.maxN) + 255) & ~size_t(255);
+  b.alloc(a.scratch_stride, false);
+  a.scratch = b.as<unsigned char>();
+}
+
+static void launch_one(const OneArgs& a, size_t smem, cudaStream_t st) {
+  const int G = cluster_size();
+  prepare_cluster_kernel(track_one_kernel, smem, G);
+  launch_cluster(track_one_kernel, 1, G, smem, st, a);
 }
 
 void device_meanshift_step(const uint8_t* frame_dev, int w, int h, int ch, double* cx, double* cy, int tw, int th,
@@ -914,11 +1125,9 @@ void device_meanshift_step(const uint8_t* frame_dev, int w, int h, int ch, doubl
   a.centers = dc;
   a.target = dc + 3 * k;
   a.out = dc + 4 * k;
-  a.bp = bp_for(k);
+  scratch_for(a);
   const size_t smem = check_smem(k, w, h);
-  set_smem(reinterpret_cast<const void*>(track_one_kernel), smem);
-  track_one_kernel<<<1, NT, smem, st>>>(a);
-  TRB_LAUNCH_CHECK("track_one_kernel");
+  launch_one(a, smem, st);
   double out[3];
   TRB_CUDA(cudaMemcpyAsync(out, a.out, sizeof(out), cudaMemcpyDeviceToHost, st));
   TRB_CUDA(cudaStreamSynchronize(st));
@@ -937,11 +1146,9 @@ bool device_histogram(const uint8_t* frame_dev, int w, int h, int ch, double cx,
   a.cx = cx, a.cy = cy, a.w = tw, a.h = th, a.K = k, a.epan = epanechnikov, a.mode = 1;
   a.centers = dc;
   a.out = dc + 3 * k;
-  a.bp = bp_for(k);
+  scratch_for(a);
   const size_t smem = check_smem(k, w, h);
-  set_smem(reinterpret_cast<const void*>(track_one_kernel), smem);
-  track_one_kernel<<<1, NT, smem, st>>>(a);
-  TRB_LAUNCH_CHECK("track_one_kernel");
+  launch_one(a, smem, st);
   std::vector<double> out(k + 1);
   TRB_CUDA(cudaMemcpyAsync(out.data(), a.out, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
   TRB_CUDA(cudaStreamSynchronize(st));

@@ -51,8 +51,10 @@ struct TrackDev {
   trb_track_log_entry* log;
   int64_t log_cap;
   int64_t* n_log;  // [S]
-  // osum breakpoint scratch: [grid][K+1][kOsumBpCap]
-  OsumBp* bp;
+  // per-cluster scratch (breakpoint list, partitioned weights, bin cache)
+  unsigned char* scratch;
+  size_t scratch_stride;
+  int64_t maxN;
 };
 
 class TrackerState {
