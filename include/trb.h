@@ -219,6 +219,9 @@ int trb_selftest_hypot(const double* x, const double* y, int64_t n, double* out,
  * [9] tracks advanced, [16..25] ordered-sum failure reasons by bit.
  * reset != 0 zeroes them after reading. */
 int trb_debug_stats(uint64_t* out32, int reset);
+/* hang diagnostics: tracker CTAs publish {kernel, item, iteration, stage}
+ * into host-mapped memory; *host_out points at n_ctas*4 ints. */
+int trb_debug_progress(int n_ctas, int** host_out);
 
 #ifdef __cplusplus
 }

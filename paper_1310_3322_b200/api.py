@@ -138,6 +138,7 @@ def _declare(L):
         "trb_quantize_colors": [vp, i64, i32, i32, C.c_uint64, vp, i32],
         "trb_selftest_hypot": [vp, vp, i64, vp, i32],
         "trb_debug_stats": [vp, i32],
+        "trb_debug_progress": [i32, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -447,6 +448,13 @@ def debug_stats(reset: bool = False) -> dict:
     out = np.zeros(32, np.uint64)
     _check(lib().trb_debug_stats(_ptr(out), int(reset)))
     return {k: int(v) for k, v in zip(STAT_NAMES, out) if k and int(v)}
+
+
+def debug_progress(n_ctas: int = 4096):
+    """Host-mapped progress records of the tracker CTAs ([n, 4] int view)."""
+    p = C.POINTER(C.c_int)()
+    _check(lib().trb_debug_progress(n_ctas, C.byref(p)))
+    return np.ctypeslib.as_array(p, shape=(n_ctas, 4))
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

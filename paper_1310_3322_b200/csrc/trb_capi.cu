@@ -685,3 +685,11 @@ extern "C" int trb_selftest_hypot(const double* x, const double* y, int64_t n, d
     TRB_CUDA(cudaMemcpy(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
   });
 }
+
+extern "C" int trb_debug_progress(int n_ctas, int** host_out) {
+  return guard([&] {
+    need(host_out != nullptr, "null argument");
+    use_device(0);
+    *host_out = trb::enable_progress(n_ctas);
+  });
+}

@@ -46,6 +46,10 @@
 
 #include "trb_exact.cuh"
 
+#ifndef TRB_OSUM_MARK
+#define TRB_OSUM_MARK(stage) ((void)0)
+#endif
+
 namespace trb {
 
 namespace cg = cooperative_groups;
@@ -168,10 +172,11 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
   const double lo_f = 1.0 - delta, hi_f = 1.0 + delta;
   const int cap_lane = kOsumBpRecs / L;
   const int buf = s.phase;  // double-buffer index for the CTA aggregates
+  // NB: s.result is NOT touched before the barriers below — callers read the
+  // previous run's results right up to this call (CTA 0 rewrites every
+  // result, including empty segments, in phase D).
   if (t < 3) s.nbp[t] = 0;
   if (t < 4) s.bad[t] = 0;
-  if (SEG)
-    for (int k = t; k < nseg; k += NT) s.result[k] = 0.0;
   __syncthreads();
 
   // ---------------- phase A: approximate (segmented) prefix at chunk starts
@@ -238,7 +243,9 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
 #pragma unroll
     for (int l = 0; l < L; ++l) s.cta_d[buf][1 + l] = P[l];
   }
+  TRB_OSUM_MARK(1);
   cl.sync();
+  TRB_OSUM_MARK(2);
   // exclusive prefix for this thread: carry(CTAs < rank) . warps < wid . lanes < lane
   double xP[L];
   {
@@ -396,7 +403,9 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
       }
       if (bad) atomicOr(&s.bad[0], 8);
     }
+    TRB_OSUM_MARK(3);
     cl.sync();
+    TRB_OSUM_MARK(4);
     // carry from lower CTAs, breakpoint bases, cluster-final piece
     if (t < L) {
       const int l = t;
@@ -458,7 +467,9 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
     }
   }
   if (t == 0 && s.bad[0] && rank != 0) atomicOr(cl.map_shared_rank(&s.bad[0], 0), s.bad[0]);
+  TRB_OSUM_MARK(5);
   cl.sync();
+  TRB_OSUM_MARK(6);
 
   // ---------------- phase D: replay on CTA 0
   if (rank == 0) {
@@ -561,7 +572,9 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
       for (int k = t; k < nlanes; k += NT) *cl.map_shared_rank(&s.result[k], r) = s.result[k];
   }
   if (t == 0) s.phase = buf ^ 1;
+  TRB_OSUM_MARK(7);
   cl.sync();
+  TRB_OSUM_MARK(8);
 }
 
 }  // namespace trb

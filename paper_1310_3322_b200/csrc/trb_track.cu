@@ -3,6 +3,16 @@
 #include <cstring>
 #include <vector>
 
+namespace trb {
+// Optional hang diagnostics: host-mapped [cta][4] = {kernel, item, iter, stage}.
+__device__ int* g_progress;
+}  // namespace trb
+#define TRB_OSUM_MARK(stage)                                                                   \
+  do {                                                                                         \
+    if (::trb::g_progress && threadIdx.x == 0)                                                 \
+      (reinterpret_cast<volatile int*>(::trb::g_progress))[4 * blockIdx.x + 3] = 100 + (stage); \
+  } while (0)
+
 #include "trb_track.cuh"
 
 namespace trb {
@@ -12,6 +22,13 @@ namespace trb {
 // point passes, [9] tracks advanced.
 // [16..25] ordered_sums failure reasons (bit index of the `bad` mask).
 __device__ unsigned long long g_trb_stats[32];
+#define TRB_PROGRESS(slot, a, b, c, d)                                                      \
+  do {                                                                                      \
+    if (g_progress && threadIdx.x == 0) {                                                   \
+      volatile int* p_ = g_progress + 4 * (slot);                                           \
+      p_[0] = (a), p_[1] = (b), p_[2] = (c), p_[3] = (d);                                   \
+    }                                                                                       \
+  } while (0)
 
 namespace {
 
@@ -322,7 +339,9 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
   if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
   for (int it = 0; it < max_iters; ++it) {
     if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull);
+    TRB_PROGRESS(blockIdx.x, 1, -1, it, 1);
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
+    TRB_PROGRESS(blockIdx.x, 1, -1, it, 2);
     if (threadIdx.x == 0) {
       int lost = !ok;
       if (ok) {
@@ -598,6 +617,7 @@ __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
   const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
   for (int item = cid; item < d.S * d.T; item += ncl) {
     const int s = item / d.T, i = item - s * d.T;
+    TRB_PROGRESS(blockIdx.x, 1, item, -1, 0);
     if (i >= d.n_list[s]) continue;
     const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
     const int64_t g = slot_index(d, s, slot);
@@ -792,6 +812,7 @@ __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
   const bool gray = d.CH == 1;
   for (int item = cid; item < d.S * d.T; item += ncl) {
     const int s = item / d.T, slot = item - s * d.T;
+    TRB_PROGRESS(blockIdx.x, 2, item, -1, 0);
     const int64_t g = slot_index(d, s, slot);
     if (!d.pending[g]) continue;
     const double cx = d.cx[g], cy = d.cy[g];
@@ -874,6 +895,22 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
 }
 
 // ------------------------------------------------------------- host side
+// Hang diagnostics: progress records of every CTA in host-mapped memory.
+int* enable_progress(int n_ctas) {
+  static int* host = nullptr;
+  static int cap = 0;
+  if (n_ctas > cap) {
+    if (host) cudaFreeHost(host);
+    TRB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host), sizeof(int) * 4 * n_ctas, cudaHostAllocMapped));
+    cap = n_ctas;
+  }
+  for (int i = 0; i < 4 * cap; ++i) host[i] = -7;
+  int* dev = nullptr;
+  TRB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+  TRB_CUDA(cudaMemcpyToSymbol(g_progress, &dev, sizeof(dev)));
+  return host;
+}
+
 void read_debug_stats(unsigned long long* out, bool reset) {
   TRB_CUDA(cudaMemcpyFromSymbol(out, g_trb_stats, sizeof(unsigned long long) * 32));
   if (reset) {

@@ -101,3 +101,8 @@ void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, u
                             cudaStream_t st);
 
 }  // namespace trb
+
+namespace trb {
+// hang diagnostics: host-mapped progress records [n_ctas][4]
+int* enable_progress(int n_ctas);
+}  // namespace trb

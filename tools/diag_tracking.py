@@ -31,19 +31,43 @@ frames = bench.make_frames(trb, clips, n, stream)
 st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
 ptrs = [[frames[s, t].data_ptr() for s in range(S)] for t in range(n)]
 t = 0
-for _ in range(93 + args.start):
+prog = api.debug_progress(4096)
+import threading
+state = {"step": -1000, "t": time.time()}
+
+
+def watchdog():
+    while True:
+        time.sleep(2)
+        if time.time() - state["t"] > 30:
+            import numpy as np
+            rec = prog.copy()
+            live = np.nonzero(rec[:, 0] != -7)[0]
+            print(f"WATCHDOG: step {state['step']} stuck; {len(live)} CTAs reported", flush=True)
+            kinds = {}
+            for i in live:
+                kinds.setdefault(tuple(rec[i]), []).append(int(i))
+            for k, v in sorted(kinds.items(), key=lambda kv: -len(kv[1]))[:40]:
+                print("  rec", k, "ctas", v[:16], len(v), flush=True)
+            os._exit(3)
+
+
+threading.Thread(target=watchdog, daemon=True).start()
+for k in range(93 + args.start):
+    state["step"], state["t"] = -1000 + k, time.time()
     st.step_device(ptrs[t], stream.cuda_stream)
+    torch.cuda.synchronize()
     t += 1
-torch.cuda.synchronize()
 api.debug_stats(reset=True)
 st.profile(True)
 for k in range(args.steps):
+    state["step"], state["t"] = k, time.time()
     st.step_device(ptrs[t], stream.cuda_stream)
     t += 1
     ms, steps = st.profile_read()
     st.profile(True)
     d = api.debug_stats(reset=True)
-    print(f"step {k}: motion {ms[0]:.3f} ms  ccl {ms[1]:.3f} ms  track {ms[2]:.3f} ms  {d}")
+    print(f"step {k}: motion {ms[0]:.3f} ms  ccl {ms[1]:.3f} ms  track {ms[2]:.3f} ms  {d}", flush=True)
 st.profile(False)
 for s in range(min(S, 4)):
     b = st.blobs(s)
