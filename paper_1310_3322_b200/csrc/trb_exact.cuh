@@ -141,3 +141,18 @@ TRB_HD uint64_t mix_seed(uint64_t seed, uint64_t salt) {
 }
 
 }  // namespace trb
+
+// Device bounds checks, compiled in with -DTRB_DEBUG (make DEBUG=1).
+#if defined(TRB_DEBUG) && defined(__CUDA_ARCH__)
+#include <cstdio>
+#define TRB_CHECK(cond, what, a, b)                                                                  \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("TRB_CHECK failed: %s (%lld, %lld) block %d thread %d line %d\n", what, (long long)(a), \
+             (long long)(b), blockIdx.x, threadIdx.x, __LINE__);                                     \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define TRB_CHECK(cond, what, a, b) ((void)0)
+#endif

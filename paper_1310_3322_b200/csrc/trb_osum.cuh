@@ -169,7 +169,11 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
   const int C = (N + GT - 1) / GT;
   const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
   const double delta = static_cast<double>(N + 2 * C + 96 + G) * 2.220446049250313e-16;
-  const double lo_f = 1.0 - delta, hi_f = 1.0 + delta;
+  // mantissa bounds (units of 2^-52 of the binade) equivalent to a relative
+  // margin of >= 2*delta on each side
+  constexpr long long kMant = (1LL << 52) - 1;
+  const long long marg = static_cast<long long>(delta * 4503599627370496.0 * 2.0) + 4;
+  const long long lowm = marg, highm = kMant - 2 * marg;
   const int cap_lane = kOsumBpRecs / L;
   const int buf = s.phase;  // double-buffer index for the CTA aggregates
   // NB: s.result is NOT touched before the barriers below — callers read the
@@ -319,26 +323,36 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
         // must still open the segment (S = +0 + 0)
         if (vl == 0.0 && !(SEG && start)) continue;
         bool safe = false;
-        Piece q;
         if (Pp > 0.0 && !(SEG && start)) {
-          const int e = osum_exp(Pp);
-          if (e != kEmptyE && e > -960 && e < 960 && osum_exp(xmul(Pp, lo_f)) == e &&
-              osum_exp(xmul(Pn, hi_f)) == e) {
+          // P and P_next in one binade with relative margin delta on both
+          // sides, checked on the raw bits: P(1-delta) >= 2^e and
+          // P_next(1+delta) < 2^(e+1)  <=  mantissa(P) >= lowm, mantissa(P_next) <= highm
+          const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
+          const int eb = static_cast<int>(bp_ >> 52);
+          if (eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm &&
+              (bn_ & kMant) <= highm) {
+            const int e = eb - 1023;
             const double qv = xmul(vl, osum_pow2(52 - e));  // exact (qv < 2^53)
-            const double fl = floor(qv);
-            const double fr = xsub(qv, fl);
+            const long long qi = __double2ll_rz(qv);       // floor (qv >= 0)
+            const double fr = xsub(qv, static_cast<double>(qi));
             safe = true;
-            q.e = e;
             if (fr == 0.5) {
-              q.tie = 1, q.A = static_cast<long long>(fl), q.B = 0;
+              Piece q;
+              q.e = e, q.tie = 1, q.A = qi, q.B = 0;
+              pc[l] = compose(pc[l], q, &tbad);
             } else {
-              q.tie = 0, q.A = 0, q.B = static_cast<long long>(fl) + (fr > 0.5 ? 1 : 0);
+              const long long r = qi + (fr > 0.5 ? 1 : 0);
+              if (pc[l].e == e) {
+                pc[l].B += r;  // fast path: same binade, plain add
+              } else {
+                Piece q;
+                q.e = e, q.tie = 0, q.A = 0, q.B = r;
+                pc[l] = compose(pc[l], q, &tbad);
+              }
             }
           }
         }
-        if (safe) {
-          pc[l] = compose(pc[l], q, &tbad);
-        } else {
+        if (!safe) {
           const int idx = atomicAdd(&s.nbp[l], 1);
           if (idx < cap_lane) {
             OsumBp& b = s.bp[l * cap_lane + idx];
@@ -463,6 +477,7 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
       const int ji = s.bp[l * cap_lane + i].j;
       int rk = 0;
       for (int q = 0; q < n; ++q) rk += s.bp[l * cap_lane + q].j < ji;
+      TRB_CHECK(s.bp_base[l] + rk < G * cap_lane, "sorted list write", s.bp_base[l], rk);
       out[rk] = s.bp[l * cap_lane + i];
     }
   }
@@ -481,7 +496,10 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
       __syncthreads();
       const OsumBp* list = scr.sorted;
       for (int q = t; q < s.nbp_total[0]; q += NT)
-        if (list[q].start) s.segpos[list[q].seg] = q;
+        if (list[q].start) {
+          TRB_CHECK(list[q].seg >= 0 && list[q].seg < nseg, "segment id", list[q].seg, q);
+          s.segpos[list[q].seg] = q;
+        }
       __syncthreads();
     }
     for (int k = t; k < nlanes; k += NT) {
@@ -500,21 +518,20 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
       }
       bool ok = !why;
       double S = 0.0;
+      // no early exit: the loads of the list do not depend on S, so the loop
+      // pipelines; a failed check only clears `ok` (the result is then
+      // recomputed by the serial fallback)
       auto run_piece = [&](const Piece& p) {
         if (p.e == kEmptyE) return;
-        if (osum_exp(S) != p.e) {
-          ok = false;
-          return;
-        }
-        const long long X = static_cast<long long>(xmul(S, osum_pow2(52 - p.e)));
+        const int pe = (p.e > -1000 && p.e < 1000) ? p.e : 0;
+        ok &= osum_exp(S) == pe;
+        const long long X = static_cast<long long>(xmul(S, osum_pow2(52 - pe)));
         const long long X2 = apply(p, X);
-        if (X2 < (1LL << 52) || X2 >= (1LL << 53)) {
-          ok = false;
-          return;
-        }
-        S = xmul(static_cast<double>(X2), osum_pow2(p.e - 52));
+        ok &= X2 >= (1LL << 52) && X2 < (1LL << 53);
+        S = xmul(static_cast<double>(X2), osum_pow2(pe - 52));
       };
-      for (int q = q0; q < q1 && ok; ++q) {
+      for (int q = q0; q < q1; ++q) {
+        TRB_CHECK(q >= 0 && q < G * cap_lane, "replay read", q, n);
         const OsumBp b = list[q];
         if (q > q0 || !SEG) run_piece(b.p);  // a segment start's piece belongs to the previous segment
         S = xadd(S, b.v);

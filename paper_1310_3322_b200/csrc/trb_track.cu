@@ -81,10 +81,10 @@ __device__ __forceinline__ int q_assign(const double* c, int k, double r, double
 // Per-cluster global scratch of the tracker kernels.
 struct TrackScratch {
   OsumScratch os;
-  double* vals;    // [maxN] positive Epanechnikov weights, partitioned by bin
+  double* vals;    // [2*maxN] positive Epanechnikov weights, partitioned by bin, then raster
   uint8_t* bins;   // [maxN] bin of every window pixel (raster order)
   static __host__ __device__ size_t bytes(int G, int64_t maxN) {
-    return sizeof(OsumBp) * OsumScratch::records(G) + sizeof(double) * maxN + maxN + 256;
+    return sizeof(OsumBp) * OsumScratch::records(G) + sizeof(double) * 2 * maxN + maxN + 256;
   }
 };
 
@@ -101,14 +101,14 @@ struct TrackSmem {
   double* wsq;   // [K]
   double* scal;  // [16] broadcast scalars
   long long* red;  // [2*NT] reduction scratch
-  int* cnt;      // [K][NT] per-thread bin counts, then scatter cursors
-  int* binoff;   // [K+1] bin offsets in the partitioned sequence
-  int* bincta;   // [K] this CTA's per-bin totals
+  int* cnt;      // [K+1][NT] per-thread segment counts, then scatter cursors
+  int* binoff;   // [K+2] segment offsets in the partitioned sequence
+  int* bincta;   // [K+1] this CTA's per-segment totals
   int* iscal;    // [16]
   uint8_t* lut;  // [256]
   static size_t bytes(int K, int W, int H) {
-    return sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT + sizeof(int) * (K * NT + 2 * K + 1 + 16) +
-           256 + 16 * 16;
+    return sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT +
+           sizeof(int) * ((K + 1) * NT + 2 * K + 3 + 16) + 256 + 16 * 16;
   }
   __device__ void carve(void* base, OsumShared* osh, int K, int W, int H) {
     os = osh;
@@ -127,9 +127,9 @@ struct TrackSmem {
     wsq = reinterpret_cast<double*>(take(sizeof(double) * K));
     scal = reinterpret_cast<double*>(take(sizeof(double) * 16));
     red = reinterpret_cast<long long*>(take(sizeof(long long) * 2 * NT));
-    cnt = reinterpret_cast<int*>(take(sizeof(int) * K * NT));
-    binoff = reinterpret_cast<int*>(take(sizeof(int) * (K + 1)));
-    bincta = reinterpret_cast<int*>(take(sizeof(int) * K));
+    cnt = reinterpret_cast<int*>(take(sizeof(int) * (K + 1) * NT));
+    binoff = reinterpret_cast<int*>(take(sizeof(int) * (K + 2)));
+    bincta = reinterpret_cast<int*>(take(sizeof(int) * (K + 1)));
     iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
     lut = reinterpret_cast<uint8_t*>(take(256));
     if (threadIdx.x == 0) osh->phase = 0;
@@ -184,6 +184,7 @@ struct BinsSrc {
     int j, b;
     __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
       while (j >= s->off[b + 1]) ++b;
+      TRB_CHECK(b < s->K, "BinsSrc segment", b, j);
       start = (j == s->off[b]), seg = b, has = true, v[0] = s->vals[j];
       ++j;
     }
@@ -234,26 +235,32 @@ __device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int 
 // order.  Returns the number of positive-weight pixels.
 __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win& r, int K, int epan, bool use_lut,
                                 TrackSmem& sm, const TrackScratch& scr) {
+  // Segments of the partitioned sequence: bins 0..K-1 (positive weights of
+  // each bin, raster order), then segment K = all positive weights in raster
+  // order (the histogram total, tracking.hpp:96).  One engine run then
+  // yields hist[0..K-1] and total.
   cg::cluster_group cl = cg::this_cluster();
   const int NT_ = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
   const int GT = G * NT_, C = (N + GT - 1) / GT;
   const int j0 = min(N, (rank * NT_ + t) * C), j1 = min(N, j0 + C);
-  for (int b = 0; b < K; ++b) sm.cnt[b * NT_ + t] = 0;
+  const int NB = K + 1;
+  for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] = 0;
   {
-    int xx = j0 % ww, yy = j0 / ww;
+    int xx = j0 % ww, yy = j0 / ww, npos = 0;
     for (int j = j0; j < j1; ++j) {
       const int b = bin_of(frame, fw, ch, r.x0 + xx, r.y0 + yy, sm, K, use_lut);
       scr.bins[j] = static_cast<uint8_t>(b);
-      if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1;
+      if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1, ++npos;
       if (++xx == ww) xx = 0, ++yy;
     }
+    sm.cnt[K * NT_ + t] = npos;
   }
   __syncthreads();
-  // exclusive scan of the counts of every bin over the CTA's threads
+  // exclusive scan of the counts of every segment over the CTA's threads
   const int lane = t & 31, wid = t >> 5, nw = NT_ >> 5, per = NT_ >> 5;
-  for (int b = wid; b < K; b += nw) {
+  for (int b = wid; b < NB; b += nw) {
     int* row = sm.cnt + b * NT_;
     int acc = 0;
     for (int i = 0; i < per; ++i) acc += row[lane * per + i];
@@ -272,10 +279,10 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     }
   }
   cl.sync();
-  // bin offsets (cluster totals) and this CTA's carry per bin
+  // segment offsets (cluster totals) and this CTA's carry per segment
   if (t == 0) {
     int off = 0;
-    for (int b = 0; b < K; ++b) {
+    for (int b = 0; b < NB; ++b) {
       int carry = 0, tot = 0;
       for (int q = 0; q < G; ++q) {
         const int c = *cl.map_shared_rank(&sm.bincta[b], q);
@@ -283,26 +290,29 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
         tot += c;
       }
       sm.binoff[b] = off;
-      sm.red[b] = off + carry;  // where this CTA's bin-b run starts
+      sm.red[b] = off + carry;  // where this CTA's segment-b run starts
       off += tot;
     }
-    sm.binoff[K] = off;
+    sm.binoff[NB] = off;
   }
   __syncthreads();
-  for (int b = 0; b < K; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
+  for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
   {
     int xx = j0 % ww, yy = j0 / ww;
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
       if (w > 0.0) {
         const int b = scr.bins[j];
+        TRB_CHECK(b < K && sm.cnt[b * NT_ + t] < 2 * N && sm.cnt[K * NT_ + t] < 2 * N, "partition scatter", b,
+                  sm.cnt[K * NT_ + t]);
         scr.vals[sm.cnt[b * NT_ + t]++] = w;
+        scr.vals[sm.cnt[K * NT_ + t]++] = w;
       }
       if (++xx == ww) xx = 0, ++yy;
     }
   }
   cl.sync();  // every CTA reads the other CTAs' bincta before it is reused; vals complete
-  return sm.binoff[K];
+  return sm.binoff[NB];
 }
 
 // histogram_opt (tracking.hpp:79-102) with the quantizer in sm.cen (and
@@ -314,16 +324,13 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
   if (r.empty()) return false;
   fill_u2(sm, r, cx, cy, w, h);
   __syncthreads();
-  const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
-  const int npos = partition_window(frame, fw, ch, r, K, epan, use_lut, sm, scr);
-  // total (raster order) and per-bin (partitioned order) sequential sums
-  TotalSrc ts{&sm, ww, epan};
-  osum_run<1, false>(N, 0, ts, *sm.os, scr.os, g_trb_stats);
-  const double total = sm.os->result[0];
-  if (npos > 0) {
-    BinsSrc bs{scr.vals, sm.binoff, K};
-    osum_run<1, true>(npos, K, bs, *sm.os, scr.os, g_trb_stats);
-  }
+  const int nseq = partition_window(frame, fw, ch, r, K, epan, use_lut, sm, scr);
+  // per-bin sums (segments 0..K-1) and the total (segment K), each a
+  // sequential sum in its reference order
+  if (nseq == 0) return false;  // no positive weight: total == 0
+  BinsSrc bs{scr.vals, sm.binoff, K + 1};
+  osum_run<1, true>(nseq, K + 1, bs, *sm.os, scr.os, g_trb_stats);
+  const double total = sm.os->result[K];
   if (!(total > 0.0)) return false;
   for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os->result[b], total);
   __syncthreads();
@@ -599,7 +606,7 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
   TrackScratch s;
   s.os.sorted = reinterpret_cast<OsumBp*>(p);
   s.vals = reinterpret_cast<double*>(p + sizeof(OsumBp) * OsumScratch::records(G));
-  s.bins = reinterpret_cast<uint8_t*>(s.vals + maxN);
+  s.bins = reinterpret_cast<uint8_t*>(s.vals + 2 * maxN);
   return s;
 }
 
