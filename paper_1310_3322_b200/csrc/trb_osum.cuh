@@ -55,9 +55,10 @@ namespace trb {
 namespace cg = cooperative_groups;
 
 constexpr int kOsumThreads = 256;
-constexpr int kOsumBpRecs = 384;  // breakpoint records per CTA (all lanes)
+constexpr int kOsumBpRecs = 240;  // breakpoint records per CTA (all lanes)
 constexpr int kMaxCluster = 16;
 constexpr int kMaxSegs = 256;     // segments (histogram bins) per run
+constexpr int kOsumGather = 480;  // cluster-wide breakpoints gathered in CTA 0 (all lanes)
 constexpr int kEmptyE = INT_MIN;
 
 // ----------------------------------------------------------- piece algebra
@@ -139,6 +140,13 @@ struct OsumShared {
   int segpos[kMaxSegs + 1];
   double result[kMaxSegs];
   int phase;
+  // parallel DSMEM gathers of the other CTAs' aggregates
+  double gath_d[kMaxCluster][4];
+  Piece gath_p[kMaxCluster][3];
+  int gath_pf[kMaxCluster][3];
+  int gath_n[kMaxCluster][3];
+  // cluster-wide ranked breakpoint list, gathered into CTA 0 (DSMEM stores)
+  OsumBp gbp[kOsumGather];
 };
 
 // warp-shuffle helpers for the scan payloads
@@ -250,14 +258,21 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
   TRB_OSUM_MARK(1);
   cl.sync();
   TRB_OSUM_MARK(2);
+  // gather the lower CTAs' aggregates once (parallel DSMEM loads), then
   // exclusive prefix for this thread: carry(CTAs < rank) . warps < wid . lanes < lane
+  if (t < rank) {
+    const double* d = cl.map_shared_rank(&s.cta_d[buf][0], t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s.gath_d[t][q] = d[q];
+  }
+  __syncthreads();
   double xP[L];
   {
     int f = 0;
 #pragma unroll
     for (int l = 0; l < L; ++l) xP[l] = 0.0;
     for (int r = 0; r < rank; ++r) {
-      const double* d = cl.map_shared_rank(&s.cta_d[buf][0], r);
+      const double* d = s.gath_d[r];
       if (d[0] != 0.0) {
         f = 1;
 #pragma unroll
@@ -420,17 +435,24 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
     TRB_OSUM_MARK(3);
     cl.sync();
     TRB_OSUM_MARK(4);
-    // carry from lower CTAs, breakpoint bases, cluster-final piece
+    // carry from lower CTAs, breakpoint bases, cluster-final piece: gather
+    // every CTA's aggregate with parallel DSMEM loads, then combine locally
+    if (t < G * L) {
+      const int r = t / L, l = t - r * L;
+      s.gath_p[r][l] = *cl.map_shared_rank(&s.cta_p[buf][l], r);
+      s.gath_pf[r][l] = *cl.map_shared_rank(&s.cta_pf[buf][l], r);
+      s.gath_n[r][l] = *cl.map_shared_rank(&s.nbp[l], r);
+    }
+    __syncthreads();
     if (t < L) {
       const int l = t;
       Piece a = piece_identity();
       int base = 0, bad = 0;
       for (int r = 0; r < G; ++r) {
         if (r == rank) s.carry_p[l] = a, s.bp_base[l] = base;
-        const Piece rp = *cl.map_shared_rank(&s.cta_p[buf][l], r);
-        const int rf = *cl.map_shared_rank(&s.cta_pf[buf][l], r);
-        base += min(*cl.map_shared_rank(&s.nbp[l], r), cap_lane);
-        if (rf) a = rp;
+        const Piece rp = s.gath_p[r][l];
+        base += min(s.gath_n[r][l], cap_lane);
+        if (s.gath_pf[r][l]) a = rp;
         else a = compose(a, rp, &bad);
       }
       s.fin_p[l] = a;
@@ -470,17 +492,21 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
   }
   __syncthreads();
   // rank each CTA list by element index into the cluster list
+  // (DSMEM stores straight into CTA 0's gathered list)
+  const int cap_g = kOsumGather / L;
   for (int l = 0; l < L; ++l) {
     const int n = min(s.nbp[l], cap_lane);
-    OsumBp* out = scr.sorted + static_cast<size_t>(l) * G * cap_lane + s.bp_base[l];
+    OsumBp* out = cl.map_shared_rank(&s.gbp[0], 0) + l * cap_g;
     for (int i = t; i < n; i += NT) {
       const int ji = s.bp[l * cap_lane + i].j;
       int rk = 0;
       for (int q = 0; q < n; ++q) rk += s.bp[l * cap_lane + q].j < ji;
-      TRB_CHECK(s.bp_base[l] + rk < G * cap_lane, "sorted list write", s.bp_base[l], rk);
-      out[rk] = s.bp[l * cap_lane + i];
+      const int pos = s.bp_base[l] + rk;
+      if (pos < cap_g) out[pos] = s.bp[l * cap_lane + i];
+      else atomicOr(&s.bad[0], 4);
     }
   }
+  __syncthreads();
   if (t == 0 && s.bad[0] && rank != 0) atomicOr(cl.map_shared_rank(&s.bad[0], 0), s.bad[0]);
   TRB_OSUM_MARK(5);
   cl.sync();
@@ -494,8 +520,9 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
     if (SEG) {  // segment -> first breakpoint position
       for (int k = t; k <= nseg; k += NT) s.segpos[k] = -1;
       __syncthreads();
-      const OsumBp* list = scr.sorted;
-      for (int q = t; q < s.nbp_total[0]; q += NT)
+      const OsumBp* list = s.gbp;
+      const int n0 = min(s.nbp_total[0], cap_g);
+      for (int q = t; q < n0; q += NT)
         if (list[q].start) {
           TRB_CHECK(list[q].seg >= 0 && list[q].seg < nseg, "segment id", list[q].seg, q);
           s.segpos[list[q].seg] = q;
@@ -504,8 +531,8 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
     }
     for (int k = t; k < nlanes; k += NT) {
       const int l = SEG ? 0 : k;
-      const OsumBp* list = scr.sorted + static_cast<size_t>(l) * G * cap_lane;
-      const int n = s.nbp_total[l];
+      const OsumBp* list = s.gbp + l * cap_g;
+      const int n = min(s.nbp_total[l], cap_g);
       int q0 = 0, q1 = n;
       if (SEG) {
         q0 = s.segpos[k];
@@ -531,7 +558,7 @@ __device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const O
         S = xmul(static_cast<double>(X2), osum_pow2(pe - 52));
       };
       for (int q = q0; q < q1; ++q) {
-        TRB_CHECK(q >= 0 && q < G * cap_lane, "replay read", q, n);
+        TRB_CHECK(q >= 0 && q < cap_g, "replay read", q, n);
         const OsumBp b = list[q];
         if (q > q0 || !SEG) run_piece(b.p);  // a segment start's piece belongs to the previous segment
         S = xadd(S, b.v);

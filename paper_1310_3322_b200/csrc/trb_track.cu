@@ -104,20 +104,23 @@ struct TrackSmem {
   int* cnt;      // [K+1][NT] per-thread segment counts, then scatter cursors
   int* binoff;   // [K+2] segment offsets in the partitioned sequence
   int* bincta;   // [K+1] this CTA's per-segment totals
+  int* gcnt;     // [kMaxCluster][K+1] gathered per-CTA segment totals
   int* iscal;    // [16]
   uint8_t* lut;  // [256]
   static size_t bytes(int K, int W, int H) {
-    return sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT +
-           sizeof(int) * ((K + 1) * NT + 2 * K + 3 + 16) + 256 + 16 * 16;
+    return sizeof(OsumShared) + 16 + sizeof(double) * (W + H + 9 * K + 16) + sizeof(long long) * 2 * NT +
+           sizeof(int) * ((K + 1) * NT + 2 * K + 3 + 16 + kMaxCluster * (K + 1)) + 256 + 16 * 16;
   }
-  __device__ void carve(void* base, OsumShared* osh, int K, int W, int H) {
-    os = osh;
+  __device__ void carve(void* base, OsumShared* /*unused*/, int K, int W, int H) {
     char* p_ = static_cast<char*>(base);
     auto take = [&](size_t n) {
       char* r = p_;
       p_ += (n + 15) & ~size_t(15);
       return r;
     };
+    // the engine's workspace (> 48 KB, so it must be dynamic shared memory)
+    OsumShared* osh = reinterpret_cast<OsumShared*>(take(sizeof(OsumShared)));
+    os = osh;
     ux2 = reinterpret_cast<double*>(take(sizeof(double) * W));
     uy2 = reinterpret_cast<double*>(take(sizeof(double) * H));
     cen = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
@@ -130,6 +133,7 @@ struct TrackSmem {
     cnt = reinterpret_cast<int*>(take(sizeof(int) * (K + 1) * NT));
     binoff = reinterpret_cast<int*>(take(sizeof(int) * (K + 2)));
     bincta = reinterpret_cast<int*>(take(sizeof(int) * (K + 1)));
+    gcnt = reinterpret_cast<int*>(take(sizeof(int) * kMaxCluster * (K + 1)));
     iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
     lut = reinterpret_cast<uint8_t*>(take(256));
     if (threadIdx.x == 0) osh->phase = 0;
@@ -280,12 +284,15 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   }
   cl.sync();
   // segment offsets (cluster totals) and this CTA's carry per segment
+  // (parallel DSMEM loads into gcnt[q][b], then one thread combines locally)
+  for (int i = t; i < G * NB; i += NT_) sm.gcnt[i] = *cl.map_shared_rank(&sm.bincta[i % NB], i / NB);
+  __syncthreads();
   if (t == 0) {
     int off = 0;
     for (int b = 0; b < NB; ++b) {
       int carry = 0, tot = 0;
       for (int q = 0; q < G; ++q) {
-        const int c = *cl.map_shared_rank(&sm.bincta[b], q);
+        const int c = sm.gcnt[q * NB + b];
         if (q < rank) carry += c;
         tot += c;
       }
@@ -610,22 +617,62 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
   return s;
 }
 
+// Work list of the active tracks, largest window first (longest processing
+// time first keeps the persistent clusters balanced).  One CTA.
+__global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
+  __shared__ int cnt[32], off[32];
+  const int t = threadIdx.x;
+  if (t < 32) cnt[t] = 0;
+  __syncthreads();
+  const int n = d.S * d.T;
+  auto bucket = [&](int item) -> int {
+    const int s = item / d.T, i = item - s * d.T;
+    if (i >= d.n_list[s]) return -1;
+    const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
+    if (d.status[g] != TRB_TRACK_ACTIVE) return -1;
+    const unsigned area = static_cast<unsigned>(max(1, d.w[g] * d.h[g]));
+    return __clz(area);  // small index = large window
+  };
+  for (int item = t; item < n; item += blockDim.x) {
+    const int b = bucket(item);
+    if (b >= 0) atomicAdd(&cnt[b], 1);
+  }
+  __syncthreads();
+  if (t == 0) {
+    int o = 0;
+    for (int b = 0; b < 32; ++b) off[b] = o, o += cnt[b];
+    *d.work_n = o;
+    *d.work_head = 0;
+  }
+  __syncthreads();
+  for (int item = t; item < n; item += blockDim.x) {
+    const int b = bucket(item);
+    if (b >= 0) d.work[atomicAdd(&off[b], 1)] = item;
+  }
+}
+
 __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ OsumShared osh;
+
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
-  sm.carve(smem_raw, &osh, d.K, d.W, d.H);
+  sm.carve(smem_raw, nullptr, d.K, d.W, d.H);
   const int K = d.K;
   const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
-  const int G = static_cast<int>(cl.num_blocks());
-  const int cid = blockIdx.x / G, ncl = gridDim.x / G;
   const bool gray = d.CH == 1;
   const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
-  for (int item = cid; item < d.S * d.T; item += ncl) {
+  // dynamic work queue, largest windows first (built by track_schedule_kernel):
+  // the cluster leader claims the next track and broadcasts it through DSMEM
+  const int n_work = *d.work_n;
+  for (;;) {
+    if (lead) sm.iscal[8] = atomicAdd(d.work_head, 1);
+    cl.sync();
+    const int q = *cl.map_shared_rank(&sm.iscal[8], 0);
+    cl.sync();  // the leader may overwrite iscal[8] only after everyone read it
+    if (q >= n_work) break;
+    const int item = d.work[q];
     const int s = item / d.T, i = item - s * d.T;
     TRB_PROGRESS(blockIdx.x, 1, item, -1, 0);
-    if (i >= d.n_list[s]) continue;
     const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
     const int64_t g = slot_index(d, s, slot);
     int status = d.status[g];
@@ -807,10 +854,10 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
 __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Mt64 rng;
-  __shared__ OsumShared osh;
+
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
-  sm.carve(smem_raw, &osh, d.K, d.W, d.H);
+  sm.carve(smem_raw, nullptr, d.K, d.W, d.H);
   const int K = d.K;
   const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
   const int G = static_cast<int>(cl.num_blocks());
@@ -865,9 +912,9 @@ struct OneArgs {
 __global__ void __launch_bounds__(NT) track_one_kernel(OneArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ OsumShared osh;
+
   TrackSmem sm;
-  sm.carve(smem_raw, &osh, a.K, a.W, a.H);
+  sm.carve(smem_raw, nullptr, a.K, a.W, a.H);
   const TrackScratch scr = cluster_scratch(a.scratch, a.scratch_stride, a.maxN);
   for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
   if (a.target)
@@ -894,9 +941,9 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
                                                       double* out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Mt64 rng;
-  __shared__ OsumShared osh;
+
   TrackSmem sm;
-  sm.carve(smem_raw, &osh, K, 1, 1);
+  sm.carve(smem_raw, nullptr, K, 1, 1);
   kmeans_device(ListSrc{px}, n, K, iters, seed, sm, &rng);
   for (int k = threadIdx.x; k < 3 * K; k += NT) out[k] = sm.cen[k];
 }
@@ -1018,6 +1065,10 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   d_.log = log_.as<trb_track_log_entry>();
   d_.log_cap = log_cap_;
   d_.n_log = nlog_.as<int64_t>();
+  work_.alloc(sizeof(int32_t) * (n + 2));
+  d_.work = work_.as<int32_t>();
+  d_.work_n = d_.work + n;
+  d_.work_head = d_.work + n + 1;
   // next_id starts at 1 (tracking.hpp:239)
   std::vector<int32_t> ones(S, 1);
   TRB_CUDA(cudaMemcpy(d_.next_id, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
@@ -1044,17 +1095,21 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     prepare_cluster_kernel(track_spawn_kernel, smem, G);
     const int64_t items = static_cast<int64_t>(S_) * T_;
     grid_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift_kernel, smem, G)));
+    if (getenv("TRB_VERBOSE"))
+      fprintf(stderr, "[trb] tracker: cluster %d, %d clusters, %zu B dynamic smem per CTA\n", G, grid_, smem);
     d_.maxN = static_cast<int64_t>(w) * h;
     d_.scratch_stride = (TrackScratch::bytes(G, d_.maxN) + 255) & ~size_t(255);
     bp_.alloc(d_.scratch_stride * static_cast<size_t>(grid_), false);
     d_.scratch = bp_.as<unsigned char>();
     smem_set_ = smem;
   }
+  track_schedule_kernel<<<1, 1024, 0, st>>>(d_);
+  TRB_LAUNCH_CHECK("track_schedule_kernel");
   launch_cluster(track_meanshift_kernel, grid_, G, smem, st, d_);
   track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
   launch_cluster(track_spawn_kernel, grid_, G, smem, st, d_);
-  *launches += 3;
+  *launches += 4;
 }
 
 void TrackerState::check_errors(cudaStream_t st) {

@@ -51,6 +51,10 @@ struct TrackDev {
   trb_track_log_entry* log;
   int64_t log_cap;
   int64_t* n_log;  // [S]
+  // meanshift work queue (largest window first)
+  int32_t* work;       // [S*T]
+  int32_t* work_n;
+  int32_t* work_head;
   // per-cluster scratch (breakpoint list, partitioned weights, bin cache)
   unsigned char* scratch;
   size_t scratch_stride;
@@ -78,7 +82,7 @@ class TrackerState {
   trb_tracker_config cfg_;
   int S_, T_, K_;
   int64_t log_cap_;
-  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_;
+  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_;
   TrackDev d_{};
   int64_t matched_cap_ = 0;
   int grid_ = 0;
