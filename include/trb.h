@@ -190,6 +190,11 @@ int trb_streams_device_planes(trb_streams* s, int stream, uint8_t** mask, int32_
  * overwrite earlier ones.  out: DEVICE buffer w*h*channels. */
 int trb_synth_raster(uint8_t* out_device, int width, int height, int channels, uint8_t background,
                      const int32_t* rects, const uint8_t* colors, int n_shapes, void* cuda_stream);
+/* n_frames frames in one launch: rects is n_frames * n_shapes * 4, frame f
+ * is written at out_device + f*frame_stride. */
+int trb_synth_raster_frames(uint8_t* out_device, int64_t frame_stride, int n_frames, int width, int height,
+                            int channels, uint8_t background, const int32_t* rects, const uint8_t* colors,
+                            int n_shapes, void* cuda_stream);
 
 
 /* ---- standalone tracker operations (public reference functions) ----

@@ -132,6 +132,7 @@ def _declare(L):
         "trb_streams_profile": [vp, i32],
         "trb_streams_profile_read": [vp, vp, C.POINTER(C.c_int)],
         "trb_synth_raster": [vp, i32, i32, i32, C.c_uint8, vp, vp, i32, vp],
+        "trb_synth_raster_frames": [vp, i64, i32, i32, i32, i32, C.c_uint8, vp, vp, i32, vp],
         "trb_meanshift_step": [vp, i32, i32, i32, C.POINTER(dbl), C.POINTER(dbl), i32, i32, vp, vp, i32, i32, dbl,
                                C.POINTER(C.c_int), i32],
         "trb_histogram": [vp, i32, i32, i32, dbl, dbl, i32, i32, vp, i32, i32, vp, i32],
@@ -455,6 +456,16 @@ def debug_progress(n_ctas: int = 4096):
     p = C.POINTER(C.c_int)()
     _check(lib().trb_debug_progress(n_ctas, C.byref(p)))
     return np.ctypeslib.as_array(p, shape=(n_ctas, 4))
+
+
+def synth_raster_frames(out_device_ptr: int, frame_stride: int, width: int, height: int, channels: int,
+                        background: int, rects_per_frame, colors, cuda_stream: int = 0) -> None:
+    """Device raster of many frames of one clip in a single launch."""
+    r = np.ascontiguousarray(np.asarray(rects_per_frame, dtype=np.int32))
+    n_frames = r.shape[0]
+    c = np.ascontiguousarray(np.asarray(colors, dtype=np.uint8).reshape(-1))
+    _check(lib().trb_synth_raster_frames(C.c_void_p(out_device_ptr), frame_stride, n_frames, width, height, channels,
+                                         background, _ptr(r), _ptr(c), r.shape[1], C.c_void_p(cuda_stream)))
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

@@ -602,6 +602,28 @@ int trb_synth_raster(uint8_t* out_device, int width, int height, int channels, u
   });
 }
 
+int trb_synth_raster_frames(uint8_t* out_device, int64_t frame_stride, int n_frames, int width, int height,
+                            int channels, uint8_t background, const int32_t* rects, const uint8_t* colors,
+                            int n_shapes, void* cuda_stream) {
+  return guard([&] {
+    need(out_device != nullptr && n_frames >= 1, "bad argument");
+    need(channels == 1 || channels == 3, "clip channels must be 1 or 3");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    DevBuf d;
+    const size_t nr = static_cast<size_t>(4) * n_shapes * n_frames;
+    d.alloc(sizeof(int32_t) * nr + 3 * n_shapes + 16, false);
+    int32_t* dr = d.as<int32_t>();
+    uint8_t* dc = reinterpret_cast<uint8_t*>(dr + nr);
+    if (n_shapes > 0) {
+      TRB_CUDA(cudaMemcpyAsync(dr, rects, sizeof(int32_t) * nr, cudaMemcpyHostToDevice, st));
+      TRB_CUDA(cudaMemcpyAsync(dc, colors, 3 * n_shapes, cudaMemcpyHostToDevice, st));
+    }
+    trb::launch_synth_raster(out_device, width, height, channels, background, dr, dc, n_shapes, st, n_frames,
+                             frame_stride);
+    TRB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 // ----------------------------------------------------- standalone ops
 int trb_meanshift_step(const uint8_t* frame, int width, int height, int channels, double* cx, double* cy, int w,
                        int h, const double* centers, const double* target_hist, int k, int max_iters, double eps,

@@ -39,7 +39,7 @@ void launch_mean_background(const void* sums, int64_t px, int W, bool wide_sums,
 // returns the number of launches issued
 int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int op, cudaStream_t st);
 void launch_synth_raster(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects, const uint8_t* colors,
-                         int n, cudaStream_t st);
+                         int n, cudaStream_t st, int n_frames = 1, int64_t frame_stride = 0);
 
 // ------------------------------------------------------------------- CCL
 // Per-stream slot table: one slot per tile-local component ("tile

@@ -206,10 +206,13 @@ __global__ void __launch_bounds__(256) morph3x3_kernel(const uint8_t* __restrict
 
 // Synthetic frame raster (synth.hpp:295-328): background fill, then every
 // shape's rectangle in order (later shapes overwrite earlier ones).
+// grid.y = frame: frame f uses rects + f*n*4 and writes out + f*frame_stride.
 __global__ void synth_raster_kernel(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects,
-                                    const uint8_t* colors, int n) {
+                                    const uint8_t* colors, int n, int64_t frame_stride) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= static_cast<int64_t>(w) * h) return;
+  out += frame_stride * blockIdx.y;
+  rects += static_cast<int64_t>(4) * n * blockIdx.y;
   const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
   int hit = -1;
   for (int k = 0; k < n; ++k) {
@@ -292,10 +295,10 @@ int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int o
 }
 
 void launch_synth_raster(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects, const uint8_t* colors,
-                         int n, cudaStream_t st) {
+                         int n, cudaStream_t st, int n_frames, int64_t frame_stride) {
   const int64_t px = static_cast<int64_t>(w) * h;
-  synth_raster_kernel<<<static_cast<unsigned>(ceil_div64(px, 256)), 256, 0, st>>>(out, w, h, ch, bg, rects, colors,
-                                                                                 n);
+  dim3 grid(static_cast<unsigned>(ceil_div64(px, 256)), n_frames);
+  synth_raster_kernel<<<grid, 256, 0, st>>>(out, w, h, ch, bg, rects, colors, n, frame_stride);
   TRB_LAUNCH_CHECK("synth_raster_kernel");
 }
 
