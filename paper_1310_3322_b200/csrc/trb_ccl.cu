@@ -114,27 +114,40 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
   const int tx0 = blockIdx.x * kTileW, ty0 = blockIdx.y * kTileH;
-  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
-  const int gx = tx0 + c;
+  // thread -> (row r, 4 consecutive columns c0..c0+3): one 32-bit mask load
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+  const int gy = ty0 + r, gx0 = tx0 + c0;
   if (threadIdx.x == 0) n_comp = 0;
 
   // 1. load: every foreground pixel starts as its own root
   bool fg[4];
+  uint32_t word = 0;
+  if (gy < a.h) {
+    const uint8_t* row = mask + static_cast<int64_t>(gy) * a.w;
+    if (a.w % 4 == 0 && gx0 + 4 <= a.w) {
+      word = *reinterpret_cast<const uint32_t*>(row + gx0);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (gx0 + k < a.w && row[gx0 + k]) word |= 1u << (8 * k);
+    }
+  }
+  bool any = false;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int r = r0 + 8 * k, gy = ty0 + r;
-    const int i = r * kTileW + c;
-    fg[k] = gx < a.w && gy < a.h && mask[static_cast<int64_t>(gy) * a.w + gx] != 0;
-    lab[i] = fg[k] ? i : -1;
+    fg[k] = ((word >> (8 * k)) & 0xffu) != 0;
+    any |= fg[k];
+    lab[r * kTileW + c0 + k] = fg[k] ? r * kTileW + c0 + k : -1;
   }
-  __syncthreads();
+  // most tiles are pure background: leave at once
+  if (!__syncthreads_or(any)) return;
 
   // 2. merge with the already-visited neighbours inside the tile
   //    (label_window's left / up / up-left / up-right, segmentation.hpp:169-174)
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (!fg[k]) continue;
-    const int r = r0 + 8 * k, i = r * kTileW + c;
+    const int c = c0 + k, i = r * kTileW + c;
     if (c > 0 && lab[i - 1] >= 0) sunion(lab, i, i - 1);
     if (r > 0) {
       if (lab[i - kTileW] >= 0) {
@@ -150,14 +163,11 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   // 3. flatten; number the local roots
   int root[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int i = (r0 + 8 * k) * kTileW + c;
-    root[k] = fg[k] ? sfind(lab, i) : -1;
-  }
+  for (int k = 0; k < 4; ++k) root[k] = fg[k] ? sfind(lab, r * kTileW + c0 + k) : -1;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int i = (r0 + 8 * k) * kTileW + c;
+    const int i = r * kTileW + c0 + k;
     if (fg[k]) lab[i] = root[k];
     if (fg[k] && root[k] == i) {
       const int id = atomicAdd(&n_comp, 1);
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (!fg[k]) continue;
-    const int gy = ty0 + r0 + 8 * k;
+    const int gx = gx0 + k;
     const int id = cid[root[k]];
     atomicAdd(&st_area[id], 1);
     atomicMin(&st_x0[id], gx);
@@ -185,24 +195,19 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
     atomicAdd(&st_sy[id], gy);
   }
   __syncthreads();
-  if (n_comp == 0) return;
   const int base = slot_base_id;
 
   // 5. slot id per foreground pixel; slot records per tile component
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (!fg[k]) continue;
-    const int gy = ty0 + r0 + 8 * k;
-    labg[static_cast<int64_t>(gy) * a.w + gx] = base + cid[root[k]];
-  }
+  for (int k = 0; k < 4; ++k)
+    if (fg[k]) labg[static_cast<int64_t>(gy) * a.w + gx0 + k] = base + cid[root[k]];
   SlotTable t = slot_base(a, s);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int i = (r0 + 8 * k) * kTileW + c;
+    const int i = r * kTileW + c0 + k;
     if (!fg[k] || root[k] != i) continue;
     const int id = cid[i];
     const int slot = base + id;
-    const int gy = ty0 + r0 + 8 * k;
     t.parent[slot] = slot;
     t.area[slot] = st_area[id];
     t.x0[slot] = st_x0[id];
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
     t.y1[slot] = st_y1[id];
     t.sx[slot] = static_cast<unsigned long long>(st_sx[id]);
     t.sy[slot] = static_cast<unsigned long long>(st_sy[id]);
-    t.minpix[slot] = gy * a.w + gx;
+    t.minpix[slot] = gy * a.w + gx0 + k;
   }
 }
 
