@@ -227,6 +227,9 @@ int trb_debug_stats(uint64_t* out32, int reset);
 /* hang diagnostics: tracker CTAs publish {kernel, item, iteration, stage}
  * into host-mapped memory; *host_out points at n_ctas*4 ints. */
 int trb_debug_progress(int n_ctas, int** host_out);
+/* per mean-shift-iteration timing log: enable (1/0, -1 = keep), read up to
+ * cap {window pixels, SM cycles} pairs */
+int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus
 }

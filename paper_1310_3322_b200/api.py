@@ -140,6 +140,7 @@ def _declare(L):
         "trb_selftest_hypot": [vp, vp, i64, vp, i32],
         "trb_debug_stats": [vp, i32],
         "trb_debug_progress": [i32, vp],
+        "trb_debug_itlog": [i32, vp, i64, C.POINTER(C.c_int64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -466,6 +467,14 @@ def synth_raster_frames(out_device_ptr: int, frame_stride: int, width: int, heig
     c = np.ascontiguousarray(np.asarray(colors, dtype=np.uint8).reshape(-1))
     _check(lib().trb_synth_raster_frames(C.c_void_p(out_device_ptr), frame_stride, n_frames, width, height, channels,
                                          background, _ptr(r), _ptr(c), r.shape[1], C.c_void_p(cuda_stream)))
+
+
+def debug_itlog(enable=None):
+    """enable=True/False toggles; returns the (pixels, cycles) pairs so far."""
+    out = np.zeros((1 << 16, 2), np.int64)
+    n = C.c_int64(0)
+    _check(lib().trb_debug_itlog(-1 if enable is None else int(enable), _ptr(out), 1 << 16, C.byref(n)))
+    return out[:n.value]
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

@@ -715,3 +715,11 @@ extern "C" int trb_debug_progress(int n_ctas, int** host_out) {
     *host_out = trb::enable_progress(n_ctas);
   });
 }
+
+extern "C" int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n) {
+  return guard([&] {
+    use_device(0);
+    if (out_pairs && n) *n = trb::read_itlog(reinterpret_cast<long long*>(out_pairs), cap);
+    if (enable >= 0) trb::enable_itlog(enable != 0);
+  });
+}

@@ -149,6 +149,28 @@ struct OsumShared {
   OsumBp gbp[kOsumGather];
 };
 
+// The CTA group one engine run spans: the whole thread-block cluster, or a
+// single CTA acting alone ("split mode": each CTA of a cluster runs its own
+// small track; barriers degrade to __syncthreads, DSMEM maps to itself).
+struct Grp {
+  int rank_, size_;
+  __device__ static Grp cluster() {
+    cg::cluster_group c = cg::this_cluster();
+    return Grp{static_cast<int>(c.block_rank()), static_cast<int>(c.num_blocks())};
+  }
+  __device__ static Grp single() { return Grp{0, 1}; }
+  __device__ unsigned block_rank() const { return static_cast<unsigned>(rank_); }
+  __device__ unsigned num_blocks() const { return static_cast<unsigned>(size_); }
+  __device__ void sync() const {
+    if (size_ > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  }
+  template <class T>
+  __device__ T* map_shared_rank(T* p, int r) const {
+    return size_ > 1 ? cg::this_cluster().map_shared_rank(p, r) : p;
+  }
+};
+
 // warp-shuffle helpers for the scan payloads
 __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
   Piece r;
@@ -168,9 +190,8 @@ __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
 // stats (optional, global): [0] runs, [1] lanes/segments, [2] fallbacks,
 // [3] breakpoints, [4] elements, [16+bit] failure reasons.
 template <int L, bool SEG, class Src>
-__device__ void osum_run(int N, int nseg, const Src& src, OsumShared& s, const OsumScratch& scr,
+__device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumShared& s, const OsumScratch& scr,
                          unsigned long long* stats = nullptr) {
-  cg::cluster_group cl = cg::this_cluster();
   const int NT = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int GT = G * NT, gt = rank * NT + t;

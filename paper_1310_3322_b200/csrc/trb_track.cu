@@ -22,6 +22,9 @@ namespace trb {
 // point passes, [9] tracks advanced.
 // [16..25] ordered_sums failure reasons (bit index of the `bad` mask).
 __device__ unsigned long long g_trb_stats[32];
+// Optional per-iteration timing log: {window pixels, cycles} pairs.
+__device__ long long* g_itlog;
+__device__ unsigned long long g_itlog_n;
 #define TRB_PROGRESS(slot, a, b, c, d)                                                      \
   do {                                                                                      \
     if (g_progress && threadIdx.x == 0) {                                                   \
@@ -92,6 +95,7 @@ struct TrackScratch {
 // OsumShared is static).
 struct TrackSmem {
   OsumShared* os;
+  Grp grp;       // the CTAs sharing this track (cluster, or this CTA alone)
   double* ux2;   // [W]
   double* uy2;   // [H]
   double* cen;   // [K*3]
@@ -121,6 +125,7 @@ struct TrackSmem {
     // the engine's workspace (> 48 KB, so it must be dynamic shared memory)
     OsumShared* osh = reinterpret_cast<OsumShared*>(take(sizeof(OsumShared)));
     os = osh;
+    grp = Grp::cluster();
     ux2 = reinterpret_cast<double*>(take(sizeof(double) * W));
     uy2 = reinterpret_cast<double*>(take(sizeof(double) * H));
     cen = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
@@ -239,11 +244,11 @@ __device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int 
 // order.  Returns the number of positive-weight pixels.
 __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win& r, int K, int epan, bool use_lut,
                                 TrackSmem& sm, const TrackScratch& scr) {
+  const Grp& cl = sm.grp;
   // Segments of the partitioned sequence: bins 0..K-1 (positive weights of
   // each bin, raster order), then segment K = all positive weights in raster
   // order (the histogram total, tracking.hpp:96).  One engine run then
   // yields hist[0..K-1] and total.
-  cg::cluster_group cl = cg::this_cluster();
   const int NT_ = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
@@ -336,7 +341,7 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
   // sequential sum in its reference order
   if (nseq == 0) return false;  // no positive weight: total == 0
   BinsSrc bs{scr.vals, sm.binoff, K + 1};
-  osum_run<1, true>(nseq, K + 1, bs, *sm.os, scr.os, g_trb_stats);
+  osum_run<1, true>(sm.grp, nseq, K + 1, bs, *sm.os, scr.os, g_trb_stats);
   const double total = sm.os->result[K];
   if (!(total > 0.0)) return false;
   for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os->result[b], total);
@@ -349,11 +354,13 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
 __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, double& cx, double& cy, int w, int h,
                                  int& status, int K, int max_iters, double eps, bool use_lut, TrackSmem& sm,
                                  const TrackScratch& scr) {
+  if (threadIdx.x == 0) sm.iscal[10] = 0;
   if (status != TRB_TRACK_ACTIVE) return;
   if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
   for (int it = 0; it < max_iters; ++it) {
-    if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull), sm.iscal[10] = it + 1;
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 1);
+    const long long t_it0 = clock64();
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 2);
     if (threadIdx.x == 0) {
@@ -374,7 +381,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     // the window is the same (same cx, cy); its bins are cached in scr.bins
     const Win r = clip_window(fw, fh, cx, cy, w, h);
     CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0};
-    osum_run<3, false>((r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, scr.os, g_trb_stats);
+    osum_run<3, false>(sm.grp, (r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, scr.os, g_trb_stats);
     const double sw = sm.os->result[0], sx = sm.os->result[1], sy = sm.os->result[2];
     __syncthreads();
     if (sw <= 0.0) {
@@ -385,6 +392,13 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
     cx = nx;
     cy = ny;
+    if (g_itlog && threadIdx.x == 0 && sm.grp.block_rank() == 0) {
+      const unsigned long long k = atomicAdd(&g_itlog_n, 1ull);
+      if (k < (1u << 16))
+        g_itlog[2 * k] = (static_cast<long long>(sm.iscal[9]) << 32) |
+                         (static_cast<long long>(sm.grp.size_) << 24) | ((r.x1 - r.x0) * (r.y1 - r.y0)),
+        g_itlog[2 * k + 1] = clock64() - t_it0;
+    }
     if (shift < eps) break;
   }
 }
@@ -617,12 +631,21 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
   return s;
 }
 
+// Tracks cheap enough to run on one CTA (estimated from the last frame's
+// iteration count: iters x (30 us + 14.1 us per kpx)) whose window fits the
+// CTA's 1/G share of the cluster scratch.
+__device__ __forceinline__ bool split_class(const TrackDev& d, int64_t g) {
+  const int64_t area = static_cast<int64_t>(d.w[g]) * d.h[g];
+  const double est = max(1, d.iters[g]) * (30.0 + 0.0141 * static_cast<double>(area));
+  return d.G > 1 && est < d.split_us && area * d.G <= d.maxN;
+}
+
 // Work list of the active tracks, largest window first (longest processing
 // time first keeps the persistent clusters balanced).  One CTA.
 __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
-  __shared__ int cnt[32], off[32];
+  __shared__ int cnt[256], off[256];
   const int t = threadIdx.x;
-  if (t < 32) cnt[t] = 0;
+  if (t < 256) cnt[t] = 0;
   __syncthreads();
   const int n = d.S * d.T;
   auto bucket = [&](int item) -> int {
@@ -630,8 +653,14 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     if (i >= d.n_list[s]) return -1;
     const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
     if (d.status[g] != TRB_TRACK_ACTIVE) return -1;
-    const unsigned area = static_cast<unsigned>(max(1, d.w[g] * d.h[g]));
-    return __clz(area);  // small index = large window
+    // estimated cost: previous frame's iteration count x (fixed overhead
+    // ~30k px + window area); 4 buckets per octave, small index = costly.
+    // Split-class tracks go after every cluster-class one.
+    const unsigned cost =
+        static_cast<unsigned>(max(1, d.iters[g])) * static_cast<unsigned>(30000 + max(1, d.w[g] * d.h[g]));
+    const int lz = __clz(cost);
+    const int sub = lz <= 29 ? static_cast<int>((cost >> (29 - lz)) & 3u) : 0;
+    return (split_class(d, g) ? 128 : 0) + 4 * lz + (3 - sub);
   };
   for (int item = t; item < n; item += blockDim.x) {
     const int b = bucket(item);
@@ -640,7 +669,7 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
   __syncthreads();
   if (t == 0) {
     int o = 0;
-    for (int b = 0; b < 32; ++b) off[b] = o, o += cnt[b];
+    for (int b = 0; b < 256; ++b) off[b] = o, o += cnt[b];
     *d.work_n = o;
     *d.work_head = 0;
   }
@@ -651,46 +680,82 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
   }
 }
 
+__device__ void meanshift_item(const TrackDev& d, int q, TrackSmem& sm, const TrackScratch& scr, bool lead) {
+  const int K = d.K;
+  const bool gray = d.CH == 1;
+  const int item = d.work[q];
+  const int s = item / d.T, i = item - s * d.T;
+  TRB_PROGRESS(blockIdx.x, 1, item, -1, 0);
+  const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
+  const int64_t g = slot_index(d, s, slot);
+  int status = d.status[g];
+  if (status != TRB_TRACK_ACTIVE) return;
+  if (threadIdx.x == 0) sm.iscal[9] = item;  // (diagnostics: iteration log)
+  for (int k = threadIdx.x; k < 3 * K; k += NT) sm.cen[k] = d.centers[g * 3 * K + k];
+  for (int k = threadIdx.x; k < K; k += NT) sm.q[k] = d.hist[g * K + k];
+  if (gray)
+    for (int k = threadIdx.x; k < 256; k += NT) sm.lut[k] = d.lut[g * 256 + k];
+  __syncthreads();
+  double cx = d.cx[g], cy = d.cy[g];
+  meanshift_device(d.frames[s], d.W, d.H, d.CH, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, gray, sm, scr);
+  sm.grp.sync();  // every CTA has read the track before the leader updates it
+  if (lead) {
+    d.cx[g] = cx;
+    d.cy[g] = cy;
+    d.status[g] = status;
+    d.iters[g] = sm.iscal[10];  // scheduling hint for the next frame
+  }
+}
+
+// Persistent clusters over the costliest-first queue.  A cluster works on
+// one track with all its CTAs while the tracks are expensive; once it draws
+// a track whose estimated single-CTA time is below d.split_us (and whose
+// window fits 1/G of the scratch) it switches to split mode, where every CTA
+// claims and runs small tracks on its own (single-CTA barriers, no DSMEM).
 __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
   sm.carve(smem_raw, nullptr, d.K, d.W, d.H);
-  const int K = d.K;
   const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
-  const bool gray = d.CH == 1;
-  const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
-  // dynamic work queue, largest windows first (built by track_schedule_kernel):
-  // the cluster leader claims the next track and broadcasts it through DSMEM
+  const int G = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int n_work = *d.work_n;
-  for (;;) {
-    if (lead) sm.iscal[8] = atomicAdd(d.work_head, 1);
+  bool split = false;
+  for (;;) {  // cluster mode
+    if (rank == 0 && threadIdx.x == 0) {
+      const int q = atomicAdd(d.work_head, 1);
+      sm.iscal[8] = q < n_work ? q : -1;
+    }
     cl.sync();
     const int q = *cl.map_shared_rank(&sm.iscal[8], 0);
     cl.sync();  // the leader may overwrite iscal[8] only after everyone read it
-    if (q >= n_work) break;
+    if (q < 0) break;
     const int item = d.work[q];
     const int s = item / d.T, i = item - s * d.T;
-    TRB_PROGRESS(blockIdx.x, 1, item, -1, 0);
-    const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
-    const int64_t g = slot_index(d, s, slot);
-    int status = d.status[g];
-    if (status != TRB_TRACK_ACTIVE) continue;
-    for (int k = threadIdx.x; k < 3 * K; k += NT) sm.cen[k] = d.centers[g * 3 * K + k];
-    for (int k = threadIdx.x; k < K; k += NT) sm.q[k] = d.hist[g * K + k];
-    if (gray)
-      for (int k = threadIdx.x; k < 256; k += NT) sm.lut[k] = d.lut[g * 256 + k];
-    __syncthreads();
-    double cx = d.cx[g], cy = d.cy[g];
-    meanshift_device(d.frames[s], d.W, d.H, d.CH, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, gray, sm,
-                     scr);
-    cl.sync();  // every CTA has read the track before the leader updates it
-    if (lead) {
-      d.cx[g] = cx;
-      d.cy[g] = cy;
-      d.status[g] = status;
+    const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
+    const bool to_split = split_class(d, g);  // read before the leader updates iters
+    meanshift_item(d, q, sm, scr, rank == 0 && threadIdx.x == 0);
+    if (to_split) {  // every later item is split-class too
+      split = true;
+      break;
     }
+  }
+  if (!split) return;
+  // split mode: this CTA alone, with its 1/G share of the cluster scratch
+  sm.grp = Grp::single();
+  TrackScratch mine = scr;
+  mine.vals = scr.vals + static_cast<int64_t>(rank) * (2 * d.maxN / G);
+  mine.bins = scr.bins + static_cast<int64_t>(rank) * (d.maxN / G);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int q = atomicAdd(d.work_head, 1);
+      sm.iscal[8] = q < n_work ? q : -1;
+    }
+    __syncthreads();
+    const int q = sm.iscal[8];
+    __syncthreads();
+    if (q < 0) break;
+    meanshift_item(d, q, sm, mine, threadIdx.x == 0);
   }
 }
 
@@ -949,6 +1014,28 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
 }
 
 // ------------------------------------------------------------- host side
+// Per-iteration timing log (diagnostics): enable with a device buffer of
+// 2^16 pairs; read back with read_itlog().
+void enable_itlog(bool on) {
+  static long long* buf = nullptr;
+  if (on && !buf) TRB_CUDA(cudaMalloc(&buf, sizeof(long long) * 2 * (1 << 16)));
+  long long* p = on ? buf : nullptr;
+  TRB_CUDA(cudaMemcpyToSymbol(g_itlog, &p, sizeof(p)));
+  unsigned long long z = 0;
+  TRB_CUDA(cudaMemcpyToSymbol(g_itlog_n, &z, sizeof(z)));
+}
+
+int64_t read_itlog(long long* out, int64_t cap) {
+  long long* p = nullptr;
+  unsigned long long n = 0;
+  TRB_CUDA(cudaMemcpyFromSymbol(&p, g_itlog, sizeof(p)));
+  TRB_CUDA(cudaMemcpyFromSymbol(&n, g_itlog_n, sizeof(n)));
+  n = std::min<unsigned long long>(n, 1u << 16);
+  n = std::min<unsigned long long>(n, static_cast<unsigned long long>(cap));
+  if (p && n) TRB_CUDA(cudaMemcpy(out, p, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost));
+  return static_cast<int64_t>(n);
+}
+
 // Hang diagnostics: progress records of every CTA in host-mapped memory.
 int* enable_progress(int n_ctas) {
   static int* host = nullptr;
@@ -1023,8 +1110,9 @@ static int max_clusters(Kern kern, size_t smem, int G) {
   return std::max(1, n);
 }
 
-template <typename Arg>
-static void launch_cluster(void (*kern)(Arg), int n_clusters, int G, size_t smem, cudaStream_t st, Arg arg) {
+template <typename... KArgs, typename... Args>
+static void launch_cluster(void (*kern)(KArgs...), int n_clusters, int G, size_t smem, cudaStream_t st,
+                           Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_clusters * G);
   cfg.blockDim = dim3(NT);
@@ -1037,7 +1125,7 @@ static void launch_cluster(void (*kern)(Arg), int n_clusters, int G, size_t smem
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TRB_CUDA(cudaLaunchKernelEx(&cfg, kern, arg));
+  TRB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, int64_t log_cap)
@@ -1045,7 +1133,7 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   validate_tracker(cfg);
   const int64_t n = static_cast<int64_t>(S) * T_;
   // int32 block: n_list,next_id,frame_no,err (4*S) + list, id,w,h,status,lost,used,pending (8*n)
-  i32_.alloc(sizeof(int32_t) * (4 * S + 8 * n));
+  i32_.alloc(sizeof(int32_t) * (4 * S + 9 * n));
   f64_.alloc(sizeof(double) * n * (2 + 4 * K_));
   lut_.alloc(static_cast<size_t>(n) * 256);
   log_.alloc(sizeof(trb_track_log_entry) * log_cap_ * S, false);
@@ -1058,7 +1146,7 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   d_.n_list = p, d_.next_id = p + S, d_.frame_no = p + 2 * S, d_.err = p + 3 * S;
   p += 4 * S;
   d_.list = p, d_.id = p + n, d_.w = p + 2 * n, d_.h = p + 3 * n, d_.status = p + 4 * n, d_.lost = p + 5 * n;
-  d_.used = p + 6 * n, d_.pending = p + 7 * n;
+  d_.used = p + 6 * n, d_.pending = p + 7 * n, d_.iters = p + 8 * n;
   double* f = f64_.as<double>();
   d_.cx = f, d_.cy = f + n, d_.centers = f + 2 * n, d_.hist = f + 2 * n + 3 * K_ * n;
   d_.lut = lut_.as<uint8_t>();
@@ -1095,9 +1183,15 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     prepare_cluster_kernel(track_spawn_kernel, smem, G);
     const int64_t items = static_cast<int64_t>(S_) * T_;
     grid_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift_kernel, smem, G)));
-    if (getenv("TRB_VERBOSE"))
-      fprintf(stderr, "[trb] tracker: cluster %d, %d clusters, %zu B dynamic smem per CTA\n", G, grid_, smem);
     d_.maxN = static_cast<int64_t>(w) * h;
+    // cheap tracks run on single CTAs (split mode); a CTA then owns 1/G of
+    // its cluster's scratch
+    const char* es = getenv("TRB_SPLIT_US");
+    d_.split_us = es ? atof(es) : 1500.0;
+    d_.G = G;
+    if (getenv("TRB_VERBOSE"))
+      fprintf(stderr, "[trb] tracker: %d clusters of %d CTAs, split below %.0f us, %zu B dynamic smem per CTA\n",
+              grid_, G, d_.split_us, smem);
     d_.scratch_stride = (TrackScratch::bytes(G, d_.maxN) + 255) & ~size_t(255);
     bp_.alloc(d_.scratch_stride * static_cast<size_t>(grid_), false);
     d_.scratch = bp_.as<unsigned char>();

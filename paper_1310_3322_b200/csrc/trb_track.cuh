@@ -38,6 +38,7 @@ struct TrackDev {
   int32_t* err;  // bit0 track-capacity overflow, bit1 log overflow
   // per slot [S][T]
   int32_t *id, *w, *h, *status, *lost, *used, *pending;
+  int32_t* iters;  // mean-shift iterations of the last frame (scheduling hint)
   double *cx, *cy;
   double* centers;  // [S][T][K][3]
   double* hist;     // [S][T][K]
@@ -55,6 +56,8 @@ struct TrackDev {
   int32_t* work;       // [S*T]
   int32_t* work_n;
   int32_t* work_head;
+  int G;               // CTAs per cluster
+  double split_us;     // tracks estimated below this (single-CTA us) run in split mode
   // per-cluster scratch (breakpoint list, partitioned weights, bin cache)
   unsigned char* scratch;
   size_t scratch_stride;
@@ -109,4 +112,6 @@ void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, u
 namespace trb {
 // hang diagnostics: host-mapped progress records [n_ctas][4]
 int* enable_progress(int n_ctas);
+void enable_itlog(bool on);
+int64_t read_itlog(long long* out, int64_t cap);
 }  // namespace trb

@@ -1,0 +1,56 @@
+"""Per mean-shift-iteration latency vs window size (diagnostics)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_1310_3322_b200 as trb  # noqa: E402
+from paper_1310_3322_b200 import api  # noqa: E402
+from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
+from paper_1310_3322_b200.synth import recipe  # noqa: E402
+
+S = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+steps = 4
+stream = torch.cuda.Stream()
+clips = [recipe("C5", s) for s in range(S)]
+n = 93 + steps
+frames = bench.make_frames(trb, clips, n, stream)
+st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+for t in range(93):
+    st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
+torch.cuda.synchronize()
+api.debug_itlog(True)
+for t in range(93, n):
+    st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
+torch.cuda.synchronize()
+a = api.debug_itlog(False)
+item = (a[:, 0] >> 32)
+N, cyc = (a[:, 0] & 0xffffff).astype(float), a[:, 1].astype(float)
+grp = (a[:, 0] >> 24) & 0xff
+# per-track totals (a track = item within a step; steps are not separated, so
+# report per (item) sums divided by steps as a proxy)
+tot = {}
+for it, c, n_ in zip(item, cyc, N):
+    t = tot.setdefault(int(it), [0.0, 0, 0.0])
+    t[0] += c
+    t[1] += 1
+    t[2] = max(t[2], n_)
+top = sorted(tot.items(), key=lambda kv: -kv[1][0])[:8]
+for it, (c, k, n_) in top:
+    print(f"track item {it}: {k/steps:5.1f} iters/step, {c/1.9e3/steps:8.1f} us/step, max N {n_:.0f}")
+print("iterations", len(a), "per step", len(a) / steps)
+for gs in sorted(set(grp.tolist())):
+    m = grp == gs
+    A = np.vstack([np.ones_like(N[m]), N[m]]).T
+    coef, *_ = np.linalg.lstsq(A, cyc[m], rcond=None)
+    print(f"group of {gs} CTAs: {m.sum()} iters, cycles ~= {coef[0]:.0f} + {coef[1]:.3f} * N"
+          f"   (us: {coef[0]/1.9e3:.1f} + {coef[1]/1.9e3*1e3:.3f}/kpx)")
+for lo, hi in [(0, 5e3), (5e3, 2e4), (2e4, 6e4), (6e4, 1.5e5), (1.5e5, 1e7)]:
+    m = (N >= lo) & (N < hi)
+    if m.any():
+        print(f"N in [{lo:.0f},{hi:.0f}): {m.sum():5d} iters, mean N {N[m].mean():9.0f}, mean {cyc[m].mean()/1.9e3:8.1f} us")
+print("total iteration-time (cluster-us) per step:", cyc.sum() / 1.9e3 / steps, " max N", N.max())
