@@ -1187,7 +1187,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     // cheap tracks run on single CTAs (split mode); a CTA then owns 1/G of
     // its cluster's scratch
     const char* es = getenv("TRB_SPLIT_US");
-    d_.split_us = es ? atof(es) : 1500.0;
+    d_.split_us = es ? atof(es) : 300.0;
     d_.G = G;
     if (getenv("TRB_VERBOSE"))
       fprintf(stderr, "[trb] tracker: %d clusters of %d CTAs, split below %.0f us, %zu B dynamic smem per CTA\n",
