@@ -230,6 +230,9 @@ int trb_debug_progress(int n_ctas, int** host_out);
 /* per mean-shift-iteration timing log: enable (1/0, -1 = keep), read up to
  * cap {window pixels, SM cycles} pairs */
 int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n);
+/* per-phase SM cycles of the mean-shift iterations while the log is on:
+ * [phase] cluster runs, [32 + phase] single-CTA runs (64 entries) */
+int trb_debug_phases(uint64_t* out64);
 
 #ifdef __cplusplus
 }

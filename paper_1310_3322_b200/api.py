@@ -141,6 +141,7 @@ def _declare(L):
         "trb_debug_stats": [vp, i32],
         "trb_debug_progress": [i32, vp],
         "trb_debug_itlog": [i32, vp, i64, C.POINTER(C.c_int64)],
+        "trb_debug_phases": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -475,6 +476,14 @@ def debug_itlog(enable=None):
     n = C.c_int64(0)
     _check(lib().trb_debug_itlog(-1 if enable is None else int(enable), _ptr(out), 1 << 16, C.byref(n)))
     return out[:n.value]
+
+
+def debug_phases() -> np.ndarray:
+    """Per-phase SM cycles of the logged mean-shift iterations ([2, 32]:
+    cluster runs, single-CTA runs)."""
+    out = np.zeros(64, np.uint64)
+    _check(lib().trb_debug_phases(_ptr(out)))
+    return out.reshape(2, 32)
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

@@ -723,3 +723,11 @@ extern "C" int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int6
     if (enable >= 0) trb::enable_itlog(enable != 0);
   });
 }
+
+extern "C" int trb_debug_phases(uint64_t* out64) {
+  return guard([&] {
+    need(out64 != nullptr, "null argument");
+    use_device(0);
+    trb::read_phases(reinterpret_cast<unsigned long long*>(out64));
+  });
+}

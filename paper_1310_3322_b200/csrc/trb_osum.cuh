@@ -330,11 +330,18 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   }
 
   // ---------------- phase B: classify every step
+  // A lane is "armed" for binade e once a step has been verified safe there:
+  // P only grows inside a segment, so later steps stay safe while P_next <=
+  // hi (= the highm bound of binade e) and only that one compare is needed.
+  // The rounding of a step a to the grid u = 2^(e-52) is read off
+  // y = fl(2^e + a) (exact for 0 <= a < 2^e, round-half-even like the sum);
+  // a tie shows as |a - (y - 2^e)| == u/2.
   Piece pc[L];
   int hadbp[L], firstbp[L];
+  double hi[L], M[L];
   int tbad = 0, tover = 0;
 #pragma unroll
-  for (int l = 0; l < L; ++l) pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1;
+  for (int l = 0; l < L; ++l) pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1, hi[l] = -1.0, M[l] = 1.0;
   {
     double P[L];
 #pragma unroll
@@ -355,40 +362,42 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         const double Pp = P[l];
         const double Pn = xadd(Pp, vl);
         P[l] = Pn;
-        // a zero step never changes S — except at a segment start, where it
-        // must still open the segment (S = +0 + 0)
-        if (vl == 0.0 && !(SEG && start)) continue;
-        bool safe = false;
-        if (Pp > 0.0 && !(SEG && start)) {
-          // P and P_next in one binade with relative margin delta on both
-          // sides, checked on the raw bits: P(1-delta) >= 2^e and
-          // P_next(1+delta) < 2^(e+1)  <=  mantissa(P) >= lowm, mantissa(P_next) <= highm
-          const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
-          const int eb = static_cast<int>(bp_ >> 52);
-          if (eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm &&
-              (bn_ & kMant) <= highm) {
-            const int e = eb - 1023;
-            const double qv = xmul(vl, osum_pow2(52 - e));  // exact (qv < 2^53)
-            const long long qi = __double2ll_rz(qv);       // floor (qv >= 0)
-            const double fr = xsub(qv, static_cast<double>(qi));
-            safe = true;
-            if (fr == 0.5) {
-              Piece q;
-              q.e = e, q.tie = 1, q.A = qi, q.B = 0;
-              pc[l] = compose(pc[l], q, &tbad);
-            } else {
-              const long long r = qi + (fr > 0.5 ? 1 : 0);
-              if (pc[l].e == e) {
-                pc[l].B += r;  // fast path: same binade, plain add
-              } else {
-                Piece q;
-                q.e = e, q.tie = 0, q.A = 0, q.B = r;
-                pc[l] = compose(pc[l], q, &tbad);
-              }
+        bool safe = !(SEG && start) && Pn <= hi[l];
+        if (!safe) {
+          // a zero step never changes S — except at a segment start, where it
+          // must still open the segment (S = +0 + 0)
+          if (vl == 0.0 && !(SEG && start)) continue;
+          if (Pp > 0.0 && !(SEG && start)) {
+            // P and P_next in one binade with relative margin delta on both
+            // sides, checked on the raw bits: P(1-delta) >= 2^e and
+            // P_next(1+delta) < 2^(e+1)  <=  mantissa(P) >= lowm, mantissa(P_next) <= highm
+            const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
+            const int eb = static_cast<int>(bp_ >> 52);
+            if (eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm &&
+                (bn_ & kMant) <= highm) {
+              hi[l] = __longlong_as_double((static_cast<long long>(eb) << 52) | highm);
+              M[l] = osum_pow2(eb - 1023);
+              safe = true;
             }
           }
         }
-        if (!safe) {
+        if (safe) {
+          const double y = xadd(M[l], vl);
+          const double d = xsub(vl, xsub(y, M[l]));
+          const long long r = __double_as_longlong(y) - __double_as_longlong(M[l]);
+          const double hu = __longlong_as_double(__double_as_longlong(M[l]) - (53LL << 52));  // u/2
+          if (fabs(d) == hu) {  // a/u = k + 1/2
+            Piece q;
+            q.e = static_cast<int>(__double_as_longlong(M[l]) >> 52) - 1023, q.tie = 1;
+            q.A = d > 0.0 ? r : r - 1, q.B = 0;
+            pc[l] = compose(pc[l], q, &tbad);
+          } else if (pc[l].e != kEmptyE) {
+            pc[l].B += r;  // same binade (binade changes are breakpoints)
+          } else {
+            pc[l].e = static_cast<int>(__double_as_longlong(M[l]) >> 52) - 1023, pc[l].tie = 0;
+            pc[l].A = 0, pc[l].B = r;
+          }
+        } else {
           const int idx = atomicAdd(&s.nbp[l], 1);
           if (idx < cap_lane) {
             OsumBp& b = s.bp[l * cap_lane + idx];
@@ -405,6 +414,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
           }
           hadbp[l] = 1;
           pc[l] = piece_identity();
+          hi[l] = -1.0;
         }
       }
     }

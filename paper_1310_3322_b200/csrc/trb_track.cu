@@ -7,10 +7,27 @@ namespace trb {
 // Optional hang diagnostics: host-mapped [cta][4] = {kernel, item, iter, stage}.
 __device__ int* g_progress;
 }  // namespace trb
+namespace trb {
+// Optional per-phase cycle accounting (enabled with the iteration log):
+// [phase] for cluster runs, [32 + phase] for single-CTA runs; thread 0 of
+// the group's rank-0 CTA adds the cycles since its previous mark.
+__device__ unsigned long long g_phase[64];
+__device__ int g_phase_on;
+__shared__ long long s_ph_last;
+}  // namespace trb
+#define TRB_PHASE(k, rank_, G_)                                                                  \
+  do {                                                                                           \
+    if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                 \
+      const long long n_ = clock64();                                                            \
+      if ((k) >= 0) atomicAdd(&::trb::g_phase[(k) + ((G_) == 1 ? 32 : 0)], n_ - ::trb::s_ph_last); \
+      ::trb::s_ph_last = n_;                                                                     \
+    }                                                                                            \
+  } while (0)
 #define TRB_OSUM_MARK(stage)                                                                   \
   do {                                                                                         \
     if (::trb::g_progress && threadIdx.x == 0)                                                 \
       (reinterpret_cast<volatile int*>(::trb::g_progress))[4 * blockIdx.x + 3] = 100 + (stage); \
+    TRB_PHASE((L == 1 ? 8 : 17) + (stage), rank, G);                                           \
   } while (0)
 
 #include "trb_track.cuh"
@@ -166,42 +183,35 @@ __device__ __forceinline__ double epan_weight(const TrackSmem& sm, int xx, int y
 }
 
 // --- element sources for the engine (cursor walks from j0 upward) ---
-// histogram total: every window pixel in raster order, weight > 0
-struct TotalSrc {
-  const TrackSmem* sm;
-  int ww, epan;
-  struct Cursor {
-    const TotalSrc* s;
-    int xx, yy;
-    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
-      const double w = epan_weight(*s->sm, xx, yy, s->epan);
-      start = false, seg = 0, has = w > 0.0, v[0] = w;
-      if (++xx == s->ww) xx = 0, ++yy;
-    }
-  };
-  __device__ Cursor begin(int j0) const { return Cursor{this, j0 % ww, j0 / ww}; }
-};
-
 // histogram bins: the positive weights stably partitioned by bin; one
 // segment per non-empty bin
 struct BinsSrc {
   const double* vals;
   const int* off;  // [K+1]
   int K;
+  // vals[j], vals[j+1] are loaded two steps ahead (the scratch has slack
+  // past the last element)
   struct Cursor {
     const BinsSrc* s;
-    int j, b;
+    int j, b, sb, nb;  // current segment b = [sb, nb)
+    double n0, n1;
     __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
-      while (j >= s->off[b + 1]) ++b;
+      if (j >= nb) {
+        do ++b;
+        while (j >= s->off[b + 1]);
+        sb = s->off[b], nb = s->off[b + 1];
+      }
       TRB_CHECK(b < s->K, "BinsSrc segment", b, j);
-      start = (j == s->off[b]), seg = b, has = true, v[0] = s->vals[j];
+      start = (j == sb), seg = b, has = true, v[0] = n0;
+      n0 = n1;
+      n1 = s->vals[j + 2];
       ++j;
     }
   };
   __device__ Cursor begin(int j0) const {
     int b = 0;
     while (b < K - 1 && off[b + 1] <= j0) ++b;
-    return Cursor{this, j0, b};
+    return Cursor{this, j0, b, off[b], off[b + 1], vals[j0], vals[j0 + 1]};
   }
 };
 
@@ -212,18 +222,28 @@ struct CentroidSrc {
   int x0, y0, ww;
   struct Cursor {
     const CentroidSrc* s;
-    int j, xx, yy;
+    int j, xx;
+    double xd, yd;  // pixel coordinates as doubles (exact integers)
+    unsigned word, wnext;  // bins[j & ~3 .. +3], the next word (loaded ahead)
     __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
-      const double w = s->wsq[s->bins[j]];
+      if ((j & 3) == 0) word = wnext, wnext = *reinterpret_cast<const unsigned*>(s->bins + j + 4);
+      const double w = s->wsq[(word >> (8 * (j & 3))) & 0xffu];
       start = false, seg = 0, has = w >= 0.0;
       v[0] = w;
-      v[1] = xmul(w, static_cast<double>(s->x0 + xx));
-      v[2] = xmul(w, static_cast<double>(s->y0 + yy));
+      v[1] = xmul(w, xd);
+      v[2] = xmul(w, yd);
       ++j;
-      if (++xx == s->ww) xx = 0, ++yy;
+      xd = xadd(xd, 1.0);
+      if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0);
     }
   };
-  __device__ Cursor begin(int j0) const { return Cursor{this, j0, j0 % ww, j0 / ww}; }
+  // bins must be 4-byte aligned
+  __device__ Cursor begin(int j0) const {
+    const int xx = j0 % ww, yy = j0 / ww;
+    const unsigned* wp = reinterpret_cast<const unsigned*>(bins + (j0 & ~3));
+    return Cursor{this, j0, xx, static_cast<double>(x0 + xx), static_cast<double>(y0 + yy), wp[0],
+                  (j0 & 3) ? wp[1] : wp[0]};
+  }
 };
 
 __device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int x, int y, const TrackSmem& sm, int K,
@@ -252,21 +272,41 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   const int NT_ = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
-  const int GT = G * NT_, C = (N + GT - 1) / GT;
+  // chunks of a multiple of 4 pixels: every thread owns whole words of bins
+  const int GT = G * NT_, C = ((N + GT - 1) / GT + 3) & ~3;
   const int j0 = min(N, (rank * NT_ + t) * C), j1 = min(N, j0 + C);
   const int NB = K + 1;
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] = 0;
   {
     int xx = j0 % ww, yy = j0 / ww, npos = 0;
-    for (int j = j0; j < j1; ++j) {
-      const int b = bin_of(frame, fw, ch, r.x0 + xx, r.y0 + yy, sm, K, use_lut);
-      scr.bins[j] = static_cast<uint8_t>(b);
-      if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1, ++npos;
-      if (++xx == ww) xx = 0, ++yy;
+    unsigned wacc = 0;
+    unsigned* bw = reinterpret_cast<unsigned*>(scr.bins);
+    if (ch == 1 && use_lut) {
+      // gray + LUT (the tracker's case): pixels are loaded one step ahead
+      const uint8_t* row = frame + static_cast<int64_t>(r.y0 + yy) * fw + r.x0;
+      int pix = j0 < j1 ? row[xx] : 0;
+      for (int j = j0; j < j1; ++j) {
+        const int b = sm.lut[pix];
+        const bool pos = epan_weight(sm, xx, yy, epan) > 0.0;
+        if (++xx == ww) xx = 0, ++yy, row += fw;
+        if (j + 1 < j1) pix = row[xx];
+        wacc |= static_cast<unsigned>(b) << (8 * (j & 3));
+        if ((j & 3) == 3 || j + 1 == j1) bw[j >> 2] = wacc, wacc = 0;
+        if (pos) sm.cnt[b * NT_ + t] += 1, ++npos;
+      }
+    } else {
+      for (int j = j0; j < j1; ++j) {
+        const int b = bin_of(frame, fw, ch, r.x0 + xx, r.y0 + yy, sm, K, use_lut);
+        wacc |= static_cast<unsigned>(b) << (8 * (j & 3));
+        if ((j & 3) == 3 || j + 1 == j1) bw[j >> 2] = wacc, wacc = 0;
+        if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1, ++npos;
+        if (++xx == ww) xx = 0, ++yy;
+      }
     }
     sm.cnt[K * NT_ + t] = npos;
   }
   __syncthreads();
+  TRB_PHASE(2, rank, G);
   // exclusive scan of the counts of every segment over the CTA's threads
   const int lane = t & 31, wid = t >> 5, nw = NT_ >> 5, per = NT_ >> 5;
   for (int b = wid; b < NB; b += nw) {
@@ -288,6 +328,7 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     }
   }
   cl.sync();
+  TRB_PHASE(3, rank, G);
   // segment offsets (cluster totals) and this CTA's carry per segment
   // (parallel DSMEM loads into gcnt[q][b], then one thread combines locally)
   for (int i = t; i < G * NB; i += NT_) sm.gcnt[i] = *cl.map_shared_rank(&sm.bincta[i % NB], i / NB);
@@ -308,13 +349,17 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     sm.binoff[NB] = off;
   }
   __syncthreads();
+  TRB_PHASE(4, rank, G);
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
   {
     int xx = j0 % ww, yy = j0 / ww;
+    const unsigned* bw = reinterpret_cast<const unsigned*>(scr.bins);
+    unsigned word = bw[j0 >> 2], wnext = bw[(j0 >> 2) + 1];  // (slack past N)
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
+      const int b = (word >> (8 * (j & 3))) & 0xffu;
+      if ((j & 3) == 3) word = wnext, wnext = bw[(j >> 2) + 2];
       if (w > 0.0) {
-        const int b = scr.bins[j];
         TRB_CHECK(b < K && sm.cnt[b * NT_ + t] < 2 * N && sm.cnt[K * NT_ + t] < 2 * N, "partition scatter", b,
                   sm.cnt[K * NT_ + t]);
         scr.vals[sm.cnt[b * NT_ + t]++] = w;
@@ -324,6 +369,7 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     }
   }
   cl.sync();  // every CTA reads the other CTAs' bincta before it is reused; vals complete
+  TRB_PHASE(5, rank, G);
   return sm.binoff[NB];
 }
 
@@ -332,10 +378,12 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
 // returns false for std::nullopt.  Cluster-uniform.
 __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, double cx, double cy, int w, int h,
                                  int K, int epan, bool use_lut, TrackSmem& sm, const TrackScratch& scr, double* out) {
+  TRB_PHASE(-1, sm.grp.rank_, sm.grp.size_);
   const Win r = clip_window(fw, fh, cx, cy, w, h);
   if (r.empty()) return false;
   fill_u2(sm, r, cx, cy, w, h);
   __syncthreads();
+  TRB_PHASE(1, sm.grp.rank_, sm.grp.size_);
   const int nseq = partition_window(frame, fw, ch, r, K, epan, use_lut, sm, scr);
   // per-bin sums (segments 0..K-1) and the total (segment K), each a
   // sequential sum in its reference order
@@ -361,19 +409,27 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull), sm.iscal[10] = it + 1;
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 1);
     const long long t_it0 = clock64();
+    TRB_PHASE(-1, sm.grp.rank_, sm.grp.size_);
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 2);
+    double* bct = reinterpret_cast<double*>(sm.red);  // per-bin bhattacharyya terms
+    if (ok)
+      for (int b = threadIdx.x; b < K; b += blockDim.x) {
+        bct[b] = xsqrt(xmul(sm.p[b], sm.q[b]));
+        sm.wsq[b] = sm.p[b] <= 0.0 ? -1.0 : xsqrt(xdiv(sm.q[b], sm.p[b]));
+      }
+    __syncthreads();
     if (threadIdx.x == 0) {
       int lost = !ok;
       if (ok) {
-        double bc = 0.0;  // bhattacharyya, tracking.hpp:114-119
-        for (int i = 0; i < K; ++i) bc = xadd(bc, xsqrt(xmul(sm.p[i], sm.q[i])));
+        double bc = 0.0;  // bhattacharyya, tracking.hpp:114-119 (in bin order)
+        for (int i = 0; i < K; ++i) bc = xadd(bc, bct[i]);
         lost = !(bc > 0.0);
-        for (int b = 0; b < K; ++b) sm.wsq[b] = sm.p[b] <= 0.0 ? -1.0 : xsqrt(xdiv(sm.q[b], sm.p[b]));
       }
       sm.iscal[0] = lost;
     }
     __syncthreads();
+    TRB_PHASE(17, sm.grp.rank_, sm.grp.size_);
     if (sm.iscal[0]) {
       status = TRB_TRACK_LOST;
       return;
@@ -392,6 +448,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
     cx = nx;
     cy = ny;
+    TRB_PHASE(26, sm.grp.rank_, sm.grp.size_);
     if (g_itlog && threadIdx.x == 0 && sm.grp.block_rank() == 0) {
       const unsigned long long k = atomicAdd(&g_itlog_n, 1ull);
       if (k < (1u << 16))
@@ -637,7 +694,7 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
 __device__ __forceinline__ bool split_class(const TrackDev& d, int64_t g) {
   const int64_t area = static_cast<int64_t>(d.w[g]) * d.h[g];
   const double est = max(1, d.iters[g]) * (30.0 + 0.0141 * static_cast<double>(area));
-  return d.G > 1 && est < d.split_us && area * d.G <= d.maxN;
+  return d.G > 1 && est < d.split_us && area <= ((d.maxN / d.G) & ~15LL);
 }
 
 // Work list of the active tracks, largest window first (longest processing
@@ -712,7 +769,7 @@ __device__ void meanshift_item(const TrackDev& d, int q, TrackSmem& sm, const Tr
 // a track whose estimated single-CTA time is below d.split_us (and whose
 // window fits 1/G of the scratch) it switches to split mode, where every CTA
 // claims and runs small tracks on its own (single-CTA barriers, no DSMEM).
-__global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
+__global__ void __launch_bounds__(NT, 2) track_meanshift_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
@@ -745,7 +802,7 @@ __global__ void __launch_bounds__(NT) track_meanshift_kernel(TrackDev d) {
   sm.grp = Grp::single();
   TrackScratch mine = scr;
   mine.vals = scr.vals + static_cast<int64_t>(rank) * (2 * d.maxN / G);
-  mine.bins = scr.bins + static_cast<int64_t>(rank) * (d.maxN / G);
+  mine.bins = scr.bins + static_cast<int64_t>(rank) * ((d.maxN / G) & ~15LL);  // 16-byte aligned shares
   for (;;) {
     if (threadIdx.x == 0) {
       const int q = atomicAdd(d.work_head, 1);
@@ -1023,7 +1080,13 @@ void enable_itlog(bool on) {
   TRB_CUDA(cudaMemcpyToSymbol(g_itlog, &p, sizeof(p)));
   unsigned long long z = 0;
   TRB_CUDA(cudaMemcpyToSymbol(g_itlog_n, &z, sizeof(z)));
+  const int ph = on ? 1 : 0;
+  TRB_CUDA(cudaMemcpyToSymbol(g_phase_on, &ph, sizeof(ph)));
+  unsigned long long zz[64] = {};
+  if (on) TRB_CUDA(cudaMemcpyToSymbol(g_phase, zz, sizeof(zz)));
 }
+
+void read_phases(unsigned long long* out64) { TRB_CUDA(cudaMemcpyFromSymbol(out64, g_phase, 64 * sizeof(*out64))); }
 
 int64_t read_itlog(long long* out, int64_t cap) {
   long long* p = nullptr;

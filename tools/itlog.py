@@ -27,6 +27,7 @@ api.debug_itlog(True)
 for t in range(93, n):
     st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
 torch.cuda.synchronize()
+ph = api.debug_phases()
 a = api.debug_itlog(False)
 item = (a[:, 0] >> 32)
 N, cyc = (a[:, 0] & 0xffffff).astype(float), a[:, 1].astype(float)
@@ -54,3 +55,20 @@ for lo, hi in [(0, 5e3), (5e3, 2e4), (2e4, 6e4), (6e4, 1.5e5), (1.5e5, 1e7)]:
     if m.any():
         print(f"N in [{lo:.0f},{hi:.0f}): {m.sum():5d} iters, mean N {N[m].mean():9.0f}, mean {cyc[m].mean()/1.9e3:8.1f} us")
 print("total iteration-time (cluster-us) per step:", cyc.sum() / 1.9e3 / steps, " max N", N.max())
+
+names = {1: "fill_u2", 2: "bin+count", 3: "count scan+sync", 4: "bin offsets", 5: "scatter+sync",
+         17: "bhattacharyya/wsq"}
+for b, nm in ((8, "hist"), (17, "cent")):
+    for st, what in enumerate(["A local", "A sync", "A gather+B", "C sync", "C+fold+rank", "rank sync",
+                               "D replay", "end sync"], start=1):
+        if b + st != 17:
+            names[b + st] = f"{nm} {what}"
+names[26] = "centroid div/hypot"
+for gi, gname in enumerate(("cluster", "single")):
+    tot = ph[gi].sum()
+    if not tot:
+        continue
+    print(f"--- {gname} runs: {tot / 1.9e3 / steps:.0f} us/step of rank-0 time")
+    for k in range(32):
+        if ph[gi, k]:
+            print(f"  {k:2d} {names.get(k, '?'):24s} {100 * ph[gi, k] / tot:5.1f}%")
