@@ -231,8 +231,9 @@ int trb_debug_progress(int n_ctas, int** host_out);
  * cap {window pixels, SM cycles} pairs */
 int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n);
 /* per-phase SM cycles of the mean-shift iterations while the log is on:
- * [phase] cluster runs, [32 + phase] single-CTA runs (64 entries) */
-int trb_debug_phases(uint64_t* out64);
+ * [bucket][32] by window size (<5k, <50k, <150k, larger pixels); entry 0 of
+ * a bucket counts its iterations (128 entries) */
+int trb_debug_phases(uint64_t* out128);
 
 #ifdef __cplusplus
 }

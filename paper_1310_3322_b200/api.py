@@ -27,7 +27,8 @@ from .abi import (BLOB, BLOB_DTYPE, LOG_DTYPE, LOGE, MOTION_CFG, SEG_CFG, TRACK,
                   log_to_array)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libtrb.so")
+# TRB_LIB selects another in-tree build of the library (A/B experiments)
+LIB_PATH = os.environ.get("TRB_LIB") or os.path.join(PKG_DIR, "libtrb.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 MotionConfig = MOTION_CFG
@@ -441,7 +442,7 @@ def synth_raster(out_device_ptr: int, width: int, height: int, channels: int, ba
 
 STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints", "osum_elements",
               "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced",
-              "", "", "", "", "", "",
+              "uniform_chunks_L1", "uniform_chunks_L3", "chunks_L1", "chunks_L3", "", "",
               "bad_scan_merge", "bad_phaseB_merge", "bad_bp_overflow", "bad_cross_cta", "bad_fold_carry",
               "bad_fold_merge", "bad_verify_start", "bad_verify_end", "bad_final_start", "bad_final_end",
               "many_bp_centroid", "many_bp_total", "many_bp_bin", "max_bp")
@@ -479,11 +480,11 @@ def debug_itlog(enable=None):
 
 
 def debug_phases() -> np.ndarray:
-    """Per-phase SM cycles of the logged mean-shift iterations ([2, 32]:
-    cluster runs, single-CTA runs)."""
-    out = np.zeros(64, np.uint64)
+    """Per-phase SM cycles of the logged mean-shift iterations, [4, 32] by
+    window-size bucket (<5k, <50k, <150k, larger); [:, 0] = iterations."""
+    out = np.zeros(128, np.uint64)
     _check(lib().trb_debug_phases(_ptr(out)))
-    return out.reshape(2, 32)
+    return out.reshape(4, 32)
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

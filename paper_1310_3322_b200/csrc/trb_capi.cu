@@ -724,10 +724,10 @@ extern "C" int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int6
   });
 }
 
-extern "C" int trb_debug_phases(uint64_t* out64) {
+extern "C" int trb_debug_phases(uint64_t* out128) {
   return guard([&] {
-    need(out64 != nullptr, "null argument");
+    need(out128 != nullptr, "null argument");
     use_device(0);
-    trb::read_phases(reinterpret_cast<unsigned long long*>(out64));
+    trb::read_phases(reinterpret_cast<unsigned long long*>(out128));
   });
 }

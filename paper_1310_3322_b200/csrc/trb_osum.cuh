@@ -115,12 +115,6 @@ struct OsumBp {
   int pad;
 };
 
-// Global scratch of one cluster: the ranked cluster-wide breakpoint list.
-struct OsumScratch {
-  OsumBp* sorted;  // [L][G*kOsumBpRecs]
-  static __host__ __device__ size_t records(int G) { return static_cast<size_t>(3) * G * kOsumBpRecs; }
-};
-
 // Shared memory of the engine (static size).
 struct OsumShared {
   OsumBp bp[kOsumBpRecs];
@@ -145,9 +139,27 @@ struct OsumShared {
   Piece gath_p[kMaxCluster][3];
   int gath_pf[kMaxCluster][3];
   int gath_n[kMaxCluster][3];
-  // cluster-wide ranked breakpoint list, gathered into CTA 0 (DSMEM stores)
-  OsumBp gbp[kOsumGather];
+  // cluster-wide ranked breakpoint list, gathered into CTA 0 (DSMEM stores).
+  // Free while phases A/B walk the elements: the element sources use it as
+  // their cp.async staging ring (osum_stage()).
+  alignas(16) OsumBp gbp[kOsumGather];
 };
+constexpr int kOsumStageBytes = kOsumGather * static_cast<int>(sizeof(OsumBp));
+__device__ __forceinline__ uint4* osum_stage(OsumShared& s) { return reinterpret_cast<uint4*>(&s.gbp[0]); }
+
+// cp.async (global -> shared, 16 bytes, bypassing registers): the element
+// sources stage read-ahead data in shared memory, because a register that a
+// pending load targets stalls every instruction that touches it (including
+// the compiler's own moves), which defeats register read-ahead.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // The CTA group one engine run spans: the whole thread-block cluster, or a
 // single CTA acting alone ("split mode": each CTA of a cluster runs its own
@@ -182,20 +194,23 @@ __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
 }
 
 // One run of the engine.
-//   Src::Cursor cur = src.begin(j0);  cur.next(start, seg, has, v)  walks
-//   elements j0, j0+1, ...; `start` marks a segment start (SEG only), `has`
+//   C = Src::chunk(N, GT) elements per cluster thread;
+//   Src::Cursor cur = src.begin(j0, gt, C, GT);  cur.next(k, start, seg, has, v)
+//   walks elements j0 = gt*C, j0+1, ... of thread gt's chunk, k = (j - j0) %
+//   Src::kUnroll (the loops unroll by kUnroll so k is static) (the source may
+//   store chunks interleaved: element gt*C + i at i*GT + gt); `start` marks a segment start (SEG only), `has`
 //   whether the element contributes, v[L] its values (>= 0).
 //   results: SEG -> s.result[seg] for seg < nseg (0 for empty segments);
 //            else s.result[lane].  Visible in every CTA on return.
 // stats (optional, global): [0] runs, [1] lanes/segments, [2] fallbacks,
 // [3] breakpoints, [4] elements, [16+bit] failure reasons.
 template <int L, bool SEG, class Src>
-__device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumShared& s, const OsumScratch& scr,
+__device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumShared& s,
                          unsigned long long* stats = nullptr) {
   const int NT = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int GT = G * NT, gt = rank * NT + t;
-  const int C = (N + GT - 1) / GT;
+  const int C = Src::chunk(N, GT);
   const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
   const double delta = static_cast<double>(N + 2 * C + 96 + G) * 2.220446049250313e-16;
   // mantissa bounds (units of 2^-52 of the binade) equivalent to a relative
@@ -218,12 +233,17 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
 #pragma unroll
   for (int l = 0; l < L; ++l) aP[l] = 0.0;
   {
-    auto cur = src.begin(j0);
-    for (int j = j0; j < j1; ++j) {
+    auto cur = src.begin(j0, gt, C, GT);
+    // unrolled so the cursor's read-ahead slots are static registers
+    for (int jb = j0; jb < j1; jb += Src::kUnroll)
+#pragma unroll
+    for (int k = 0; k < Src::kUnroll; ++k) {
+      const int j = jb + k;
+      if (j >= j1) break;
       bool start, has;
       int seg;
       double v[L];
-      cur.next(start, seg, has, v);
+      cur.next(k, start, seg, has, v);
       if (SEG && start) {
         af = 1;
 #pragma unroll
@@ -329,6 +349,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
     (void)f;
   }
 
+  TRB_OSUM_MARK(3);
   // ---------------- phase B: classify every step
   // A lane is "armed" for binade e once a step has been verified safe there:
   // P only grows inside a segment, so later steps stay safe while P_next <=
@@ -346,12 +367,17 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
     double P[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) P[l] = xP[l];
-    auto cur = src.begin(j0);
-    for (int j = j0; j < j1; ++j) {
+    auto cur = src.begin(j0, gt, C, GT);
+    // unrolled so the cursor's read-ahead slots are static registers
+    for (int jb = j0; jb < j1; jb += Src::kUnroll)
+#pragma unroll
+    for (int k = 0; k < Src::kUnroll; ++k) {
+      const int j = jb + k;
+      if (j >= j1) break;
       bool start, has;
       int seg;
       double v[L];
-      cur.next(start, seg, has, v);
+      cur.next(k, start, seg, has, v);
       if (SEG && start)
 #pragma unroll
         for (int l = 0; l < L; ++l) P[l] = 0.0;
@@ -419,6 +445,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       }
     }
   }
+  TRB_OSUM_MARK(4);
   if (tbad) atomicOr(&s.bad[0], 2);
   if (tover) atomicOr(&s.bad[0], 4);
 
@@ -463,9 +490,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       }
       if (bad) atomicOr(&s.bad[0], 8);
     }
-    TRB_OSUM_MARK(3);
+    TRB_OSUM_MARK(5);
     cl.sync();
-    TRB_OSUM_MARK(4);
+    TRB_OSUM_MARK(6);
     // carry from lower CTAs, breakpoint bases, cluster-final piece: gather
     // every CTA's aggregate with parallel DSMEM loads, then combine locally
     if (t < G * L) {
@@ -522,6 +549,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
     }
   }
   __syncthreads();
+  TRB_OSUM_MARK(7);
   // rank each CTA list by element index into the cluster list
   // (DSMEM stores straight into CTA 0's gathered list)
   const int cap_g = kOsumGather / L;
@@ -539,9 +567,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   }
   __syncthreads();
   if (t == 0 && s.bad[0] && rank != 0) atomicOr(cl.map_shared_rank(&s.bad[0], 0), s.bad[0]);
-  TRB_OSUM_MARK(5);
+  TRB_OSUM_MARK(8);
   cl.sync();
-  TRB_OSUM_MARK(6);
+  TRB_OSUM_MARK(9);
 
   // ---------------- phase D: replay on CTA 0
   if (rank == 0) {
@@ -616,21 +644,27 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         double S[L];
 #pragma unroll
         for (int l = 0; l < L; ++l) S[l] = 0.0;
-        auto cur = src.begin(0);
         int cs = -1;
-        for (int j = 0; j < N; ++j) {
-          bool start, has;
-          int seg;
-          double v[L];
-          cur.next(start, seg, has, v);
-          if (SEG && start) {
-            if (cs >= 0) s.result[cs] = S[0];
-            cs = seg;
-            S[0] = 0.0;
-          }
-          if (!has) continue;
+        for (int g = 0; g * C < N; ++g) {  // chunk by chunk, in order
+          const int a0 = g * C, a1 = min(N, a0 + C);
+          auto cur = src.begin(a0, g, C, GT);
+          for (int jb = a0; jb < a1; jb += Src::kUnroll)
 #pragma unroll
-          for (int l = 0; l < L; ++l) S[l] = xadd(S[l], v[l]);
+            for (int k = 0; k < Src::kUnroll; ++k) {
+              if (jb + k >= a1) break;
+              bool start, has;
+              int seg;
+              double v[L];
+              cur.next(k, start, seg, has, v);
+              if (SEG && start) {
+                if (cs >= 0) s.result[cs] = S[0];
+                cs = seg;
+                S[0] = 0.0;
+              }
+              if (!has) continue;
+#pragma unroll
+              for (int l = 0; l < L; ++l) S[l] = xadd(S[l], v[l]);
+            }
         }
         if (SEG) {
           for (int k = 0; k < nseg; ++k)
@@ -647,9 +681,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       for (int k = t; k < nlanes; k += NT) *cl.map_shared_rank(&s.result[k], r) = s.result[k];
   }
   if (t == 0) s.phase = buf ^ 1;
-  TRB_OSUM_MARK(7);
+  TRB_OSUM_MARK(10);
   cl.sync();
-  TRB_OSUM_MARK(8);
+  TRB_OSUM_MARK(11);
 }
 
 }  // namespace trb

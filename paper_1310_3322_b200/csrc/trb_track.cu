@@ -9,25 +9,36 @@ __device__ int* g_progress;
 }  // namespace trb
 namespace trb {
 // Optional per-phase cycle accounting (enabled with the iteration log):
-// [phase] for cluster runs, [32 + phase] for single-CTA runs; thread 0 of
-// the group's rank-0 CTA adds the cycles since its previous mark.
-__device__ unsigned long long g_phase[64];
+// [bucket][phase], bucket = window-size class of the iteration (<5k, <50k,
+// <150k, larger pixels); thread 0 of the group's rank-0 CTA adds the cycles
+// since its previous mark; [bucket][0] counts iterations.
+__device__ unsigned long long g_phase[128];
 __device__ int g_phase_on;
 __shared__ long long s_ph_last;
+__shared__ int s_ph_bucket;
 }  // namespace trb
-#define TRB_PHASE(k, rank_, G_)                                                                  \
-  do {                                                                                           \
-    if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                 \
-      const long long n_ = clock64();                                                            \
-      if ((k) >= 0) atomicAdd(&::trb::g_phase[(k) + ((G_) == 1 ? 32 : 0)], n_ - ::trb::s_ph_last); \
-      ::trb::s_ph_last = n_;                                                                     \
-    }                                                                                            \
+#define TRB_PHASE(k, rank_, G_)                                                                   \
+  do {                                                                                            \
+    if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                  \
+      const long long n_ = clock64();                                                             \
+      if ((k) >= 0) atomicAdd(&::trb::g_phase[(k) + 32 * ::trb::s_ph_bucket], n_ - ::trb::s_ph_last); \
+      ::trb::s_ph_last = n_;                                                                      \
+    }                                                                                             \
+  } while (0)
+#define TRB_PHASE_BEGIN(n_px, rank_)                                                              \
+  do {                                                                                            \
+    if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                  \
+      const int b_ = (n_px) < 5000 ? 0 : (n_px) < 50000 ? 1 : (n_px) < 150000 ? 2 : 3;            \
+      ::trb::s_ph_bucket = b_;                                                                    \
+      atomicAdd(&::trb::g_phase[32 * b_], 1ull);                                                  \
+      ::trb::s_ph_last = clock64();                                                               \
+    }                                                                                             \
   } while (0)
 #define TRB_OSUM_MARK(stage)                                                                   \
   do {                                                                                         \
     if (::trb::g_progress && threadIdx.x == 0)                                                 \
       (reinterpret_cast<volatile int*>(::trb::g_progress))[4 * blockIdx.x + 3] = 100 + (stage); \
-    TRB_PHASE((L == 1 ? 8 : 17) + (stage), rank, G);                                           \
+    TRB_PHASE((L == 1 ? 7 : 18) + (stage), rank, G);                                           \
   } while (0)
 
 #include "trb_track.cuh"
@@ -99,12 +110,17 @@ __device__ __forceinline__ int q_assign(const double* c, int k, double r, double
 }
 
 // Per-cluster global scratch of the tracker kernels.
+// Both arrays hold thread chunks INTERLEAVED (element gt*C + i at i*GT + gt,
+// 4-pixel words for bins), so a warp's loads at step i are coalesced; the
+// slack covers chunk rounding and the cursors' read-ahead.
+constexpr int64_t kValsSlack = 32768;  // doubles
+constexpr int64_t kBinsSlack = 262144;  // bytes
 struct TrackScratch {
-  OsumScratch os;
-  double* vals;    // [2*maxN] positive Epanechnikov weights, partitioned by bin, then raster
-  uint8_t* bins;   // [maxN] bin of every window pixel (raster order)
+  double* vals;    // [2*maxN + slack] positive Epanechnikov weights, partitioned by bin, then raster
+  uint8_t* bins;   // [maxN + slack] bin of every window pixel (raster order, as words)
   static __host__ __device__ size_t bytes(int G, int64_t maxN) {
-    return sizeof(OsumBp) * OsumScratch::records(G) + sizeof(double) * 2 * maxN + maxN + 256;
+    (void)G;
+    return sizeof(double) * (2 * maxN + kValsSlack) + maxN + kBinsSlack + 256;
   }
 };
 
@@ -184,65 +200,123 @@ __device__ __forceinline__ double epan_weight(const TrackSmem& sm, int xx, int y
 
 // --- element sources for the engine (cursor walks from j0 upward) ---
 // histogram bins: the positive weights stably partitioned by bin; one
-// segment per non-empty bin
+// segment per non-empty bin.  vals holds thread chunks interleaved in
+// 2-element blocks: block b of thread gt is the double2 at b*GT + gt.  The
+// cursor streams blocks through a ring of kRing cp.async slots per thread.
 struct BinsSrc {
+  static constexpr int kUnroll = 2;
+  static constexpr int kRing = 5;
   const double* vals;
   const int* off;  // [K+1]
   int K;
-  // vals[j], vals[j+1] are loaded two steps ahead (the scratch has slack
-  // past the last element)
+  uint4* stage;    // [kRing][blockDim.x] 16-byte slots
+  static __device__ __forceinline__ int chunk(int N, int GT) { return (N + GT - 1) / GT; }
   struct Cursor {
     const BinsSrc* s;
-    int j, b, sb, nb;  // current segment b = [sb, nb)
-    double n0, n1;
-    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
+    const double2* p;  // next block to request
+    int j, b, sb, nb, GT, blk;  // current segment b = [sb, nb); blk = block being consumed
+    double c0, c1;
+    __device__ __forceinline__ void next(int k, bool& start, int& seg, bool& has, double* v) {
+      if (k == 0) {
+        cp_async_wait<kRing - 2>();  // block blk has landed
+        const uint4* slot = s->stage + (blk % kRing) * blockDim.x + threadIdx.x;
+        const double2 d = *reinterpret_cast<const double2*>(slot);
+        c0 = d.x, c1 = d.y;
+        cp_async16(s->stage + ((blk + kRing - 1) % kRing) * blockDim.x + threadIdx.x, p);
+        cp_async_commit();
+        p += GT, ++blk;
+      }
       if (j >= nb) {
         do ++b;
         while (j >= s->off[b + 1]);
         sb = s->off[b], nb = s->off[b + 1];
       }
       TRB_CHECK(b < s->K, "BinsSrc segment", b, j);
-      start = (j == sb), seg = b, has = true, v[0] = n0;
-      n0 = n1;
-      n1 = s->vals[j + 2];
+      start = (j == sb), seg = b, has = true, v[0] = k == 0 ? c0 : c1;
       ++j;
     }
   };
-  __device__ Cursor begin(int j0) const {
+  __device__ Cursor begin(int j0, int gt, int /*C*/, int GT) const {
     int b = 0;
     while (b < K - 1 && off[b + 1] <= j0) ++b;
-    return Cursor{this, j0, b, off[b], off[b + 1], vals[j0], vals[j0 + 1]};
+    Cursor c;
+    c.s = this, c.j = j0, c.b = b, c.sb = off[b], c.nb = off[b + 1], c.GT = GT, c.blk = 0;
+    c.c0 = c.c1 = 0.0;
+    cp_async_wait<0>();  // nothing of an earlier walk is still landing
+    const double2* p = reinterpret_cast<const double2*>(vals) + gt;
+#pragma unroll
+    for (int r = 0; r < kRing - 1; ++r, p += GT) {
+      cp_async16(stage + r * blockDim.x + threadIdx.x, p);
+      cp_async_commit();
+    }
+    c.p = p;
+    return c;
   }
 };
+static_assert(BinsSrc::kRing * 16 * NT <= kOsumStageBytes, "staging ring exceeds the gather list");
+// physical index (in doubles) of partitioned element `pos` for chunk size C
+__device__ __forceinline__ int64_t bins_src_index(int pos, const UDiv32& divC, int C, int GT) {
+  const int g = static_cast<int>(divC.div(static_cast<uint32_t>(pos)));
+  const int i = pos - g * C;
+  return (static_cast<int64_t>(i >> 1) * GT + g) * 2 + (i & 1);
+}
 
-// mean-shift centroid: every window pixel, weight sqrt(q/p) of its bin
+__device__ __forceinline__ unsigned u4_byte(const uint4& u, int k) {
+  const unsigned lo = (k & 4) ? u.y : u.x, hi = (k & 4) ? u.w : u.z;
+  return (((k & 8) ? hi : lo) >> (8 * (k & 3))) & 0xffu;
+}
+
+// mean-shift centroid: every window pixel, weight sqrt(q/p) of its bin;
+// bins are 16-pixel units (uint4), chunk-interleaved, streamed through two
+// cp.async slots per thread.  The loop stays rolled (kUnroll 1).
 struct CentroidSrc {
+  static constexpr int kUnroll = 1;
   const uint8_t* bins;
   const double* wsq;  // < 0 when p[b] <= 0
   int x0, y0, ww;
+  uint4* stage;       // [2][blockDim.x]
+  static __device__ __forceinline__ int chunk(int N, int GT) { return ((N + GT - 1) / GT + 15) & ~15; }
   struct Cursor {
     const CentroidSrc* s;
-    int j, xx;
-    double xd, yd;  // pixel coordinates as doubles (exact integers)
-    unsigned word, wnext;  // bins[j & ~3 .. +3], the next word (loaded ahead)
-    __device__ __forceinline__ void next(bool& start, int& seg, bool& has, double* v) {
-      if ((j & 3) == 0) word = wnext, wnext = *reinterpret_cast<const unsigned*>(s->bins + j + 4);
-      const double w = s->wsq[(word >> (8 * (j & 3))) & 0xffu];
+    const uint4* p;  // next unit to request
+    int i, xx, GT;   // i = element index inside the chunk
+    double xd, yd;   // pixel coordinates as doubles (exact integers)
+    uint4 cur;
+    __device__ __forceinline__ void next(int /*k*/, bool& start, int& seg, bool& has, double* v) {
+      const int k = i & 15;
+      if (k == 0) {
+        cp_async_wait<1>();  // this unit has landed (the next may still fly)
+        uint4* slot = s->stage + ((i >> 4) & 1) * blockDim.x + threadIdx.x;
+        cur = *slot;
+        cp_async16(slot, p);  // the unit after next
+        cp_async_commit();
+        p += GT;
+      }
+      const double w = s->wsq[u4_byte(cur, k)];
       start = false, seg = 0, has = w >= 0.0;
       v[0] = w;
       v[1] = xmul(w, xd);
       v[2] = xmul(w, yd);
-      ++j;
+      ++i;
       xd = xadd(xd, 1.0);
       if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0);
     }
   };
-  // bins must be 4-byte aligned
-  __device__ Cursor begin(int j0) const {
+  // j0 = gt * C with C a multiple of 16
+  __device__ Cursor begin(int j0, int gt, int /*C*/, int GT) const {
     const int xx = j0 % ww, yy = j0 / ww;
-    const unsigned* wp = reinterpret_cast<const unsigned*>(bins + (j0 & ~3));
-    return Cursor{this, j0, xx, static_cast<double>(x0 + xx), static_cast<double>(y0 + yy), wp[0],
-                  (j0 & 3) ? wp[1] : wp[0]};
+    const uint4* p = reinterpret_cast<const uint4*>(bins) + gt;
+    Cursor c;
+    c.s = this, c.i = 0, c.xx = xx, c.GT = GT;
+    c.xd = static_cast<double>(x0 + xx), c.yd = static_cast<double>(y0 + yy);
+    c.cur = make_uint4(0, 0, 0, 0);
+    cp_async_wait<0>();
+    cp_async16(stage + threadIdx.x, p);
+    cp_async_commit();
+    cp_async16(stage + blockDim.x + threadIdx.x, p + GT);
+    cp_async_commit();
+    c.p = p + 2 * GT;
+    return c;
   }
 };
 
@@ -272,15 +346,27 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   const int NT_ = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
-  // chunks of a multiple of 4 pixels: every thread owns whole words of bins
-  const int GT = G * NT_, C = ((N + GT - 1) / GT + 3) & ~3;
-  const int j0 = min(N, (rank * NT_ + t) * C), j1 = min(N, j0 + C);
+  // chunks of a multiple of 4 pixels (CentroidSrc's chunking): every thread
+  // owns whole words of bins, stored chunk-interleaved
+  const int GT = G * NT_, gt = rank * NT_ + t, C = CentroidSrc::chunk(N, GT);
+  const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
   const int NB = K + 1;
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] = 0;
   {
     int xx = j0 % ww, yy = j0 / ww, npos = 0;
     unsigned wacc = 0;
-    unsigned* bw = reinterpret_cast<unsigned*>(scr.bins);
+    uint4 uacc = make_uint4(0, 0, 0, 0);
+    uint4* bw = reinterpret_cast<uint4*>(scr.bins) + gt;
+    // word (j >> 2) & 3 of the unit is complete: place it, store full units
+    auto put_word = [&](int j, bool last) {
+      const int q = (j >> 2) & 3;
+      if (q == 0) uacc.x = wacc;
+      else if (q == 1) uacc.y = wacc;
+      else if (q == 2) uacc.z = wacc;
+      else uacc.w = wacc;
+      wacc = 0;
+      if (q == 3 || last) *bw = uacc, bw += GT, uacc = make_uint4(0, 0, 0, 0);
+    };
     if (ch == 1 && use_lut) {
       // gray + LUT (the tracker's case): pixels are loaded one step ahead
       const uint8_t* row = frame + static_cast<int64_t>(r.y0 + yy) * fw + r.x0;
@@ -291,14 +377,14 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
         if (++xx == ww) xx = 0, ++yy, row += fw;
         if (j + 1 < j1) pix = row[xx];
         wacc |= static_cast<unsigned>(b) << (8 * (j & 3));
-        if ((j & 3) == 3 || j + 1 == j1) bw[j >> 2] = wacc, wacc = 0;
+        if ((j & 3) == 3 || j + 1 == j1) put_word(j, j + 1 == j1);
         if (pos) sm.cnt[b * NT_ + t] += 1, ++npos;
       }
     } else {
       for (int j = j0; j < j1; ++j) {
         const int b = bin_of(frame, fw, ch, r.x0 + xx, r.y0 + yy, sm, K, use_lut);
         wacc |= static_cast<unsigned>(b) << (8 * (j & 3));
-        if ((j & 3) == 3 || j + 1 == j1) bw[j >> 2] = wacc, wacc = 0;
+        if ((j & 3) == 3 || j + 1 == j1) put_word(j, j + 1 == j1);
         if (epan_weight(sm, xx, yy, epan) > 0.0) sm.cnt[b * NT_ + t] += 1, ++npos;
         if (++xx == ww) xx = 0, ++yy;
       }
@@ -353,17 +439,21 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
   {
     int xx = j0 % ww, yy = j0 / ww;
-    const unsigned* bw = reinterpret_cast<const unsigned*>(scr.bins);
-    unsigned word = bw[j0 >> 2], wnext = bw[(j0 >> 2) + 1];  // (slack past N)
+    const uint4* bw = reinterpret_cast<const uint4*>(scr.bins) + gt;
+    uint4 unit = bw[0], unext = bw[GT];  // (slack past N)
+    bw += 2 * GT;
+    // vals in BinsSrc's interleaved layout for its chunk size
+    const int nseq = sm.binoff[NB], Cv = BinsSrc::chunk(nseq, GT);
+    const UDiv32 divC = UDiv32::make(static_cast<uint32_t>(max(1, Cv)));
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
-      const int b = (word >> (8 * (j & 3))) & 0xffu;
-      if ((j & 3) == 3) word = wnext, wnext = bw[(j >> 2) + 2];
+      const int b = u4_byte(unit, j & 15);
+      if ((j & 15) == 15) unit = unext, unext = *bw, bw += GT;
       if (w > 0.0) {
         TRB_CHECK(b < K && sm.cnt[b * NT_ + t] < 2 * N && sm.cnt[K * NT_ + t] < 2 * N, "partition scatter", b,
                   sm.cnt[K * NT_ + t]);
-        scr.vals[sm.cnt[b * NT_ + t]++] = w;
-        scr.vals[sm.cnt[K * NT_ + t]++] = w;
+        scr.vals[bins_src_index(sm.cnt[b * NT_ + t]++, divC, Cv, GT)] = w;
+        scr.vals[bins_src_index(sm.cnt[K * NT_ + t]++, divC, Cv, GT)] = w;
       }
       if (++xx == ww) xx = 0, ++yy;
     }
@@ -378,9 +468,9 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
 // returns false for std::nullopt.  Cluster-uniform.
 __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, double cx, double cy, int w, int h,
                                  int K, int epan, bool use_lut, TrackSmem& sm, const TrackScratch& scr, double* out) {
-  TRB_PHASE(-1, sm.grp.rank_, sm.grp.size_);
   const Win r = clip_window(fw, fh, cx, cy, w, h);
   if (r.empty()) return false;
+  TRB_PHASE_BEGIN((r.x1 - r.x0) * (r.y1 - r.y0), sm.grp.rank_);
   fill_u2(sm, r, cx, cy, w, h);
   __syncthreads();
   TRB_PHASE(1, sm.grp.rank_, sm.grp.size_);
@@ -388,8 +478,8 @@ __device__ bool window_histogram(const uint8_t* frame, int fw, int fh, int ch, d
   // per-bin sums (segments 0..K-1) and the total (segment K), each a
   // sequential sum in its reference order
   if (nseq == 0) return false;  // no positive weight: total == 0
-  BinsSrc bs{scr.vals, sm.binoff, K + 1};
-  osum_run<1, true>(sm.grp, nseq, K + 1, bs, *sm.os, scr.os, g_trb_stats);
+  BinsSrc bs{scr.vals, sm.binoff, K + 1, osum_stage(*sm.os)};
+  osum_run<1, true>(sm.grp, nseq, K + 1, bs, *sm.os, g_trb_stats);
   const double total = sm.os->result[K];
   if (!(total > 0.0)) return false;
   for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.os->result[b], total);
@@ -409,7 +499,6 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull), sm.iscal[10] = it + 1;
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 1);
     const long long t_it0 = clock64();
-    TRB_PHASE(-1, sm.grp.rank_, sm.grp.size_);
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 2);
     double* bct = reinterpret_cast<double*>(sm.red);  // per-bin bhattacharyya terms
@@ -429,15 +518,15 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
       sm.iscal[0] = lost;
     }
     __syncthreads();
-    TRB_PHASE(17, sm.grp.rank_, sm.grp.size_);
+    TRB_PHASE(6, sm.grp.rank_, sm.grp.size_);
     if (sm.iscal[0]) {
       status = TRB_TRACK_LOST;
       return;
     }
     // the window is the same (same cx, cy); its bins are cached in scr.bins
     const Win r = clip_window(fw, fh, cx, cy, w, h);
-    CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0};
-    osum_run<3, false>(sm.grp, (r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, scr.os, g_trb_stats);
+    CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0, osum_stage(*sm.os)};
+    osum_run<3, false>(sm.grp, (r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, g_trb_stats);
     const double sw = sm.os->result[0], sx = sm.os->result[1], sy = sm.os->result[2];
     __syncthreads();
     if (sw <= 0.0) {
@@ -448,7 +537,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
     cx = nx;
     cy = ny;
-    TRB_PHASE(26, sm.grp.rank_, sm.grp.size_);
+    TRB_PHASE(30, sm.grp.rank_, sm.grp.size_);
     if (g_itlog && threadIdx.x == 0 && sm.grp.block_rank() == 0) {
       const unsigned long long k = atomicAdd(&g_itlog_n, 1ull);
       if (k < (1u << 16))
@@ -682,9 +771,8 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
   const int cid = blockIdx.x / G;
   unsigned char* p = base + static_cast<size_t>(cid) * stride;
   TrackScratch s;
-  s.os.sorted = reinterpret_cast<OsumBp*>(p);
-  s.vals = reinterpret_cast<double*>(p + sizeof(OsumBp) * OsumScratch::records(G));
-  s.bins = reinterpret_cast<uint8_t*>(s.vals + 2 * maxN);
+  s.vals = reinterpret_cast<double*>(p);
+  s.bins = reinterpret_cast<uint8_t*>(s.vals + 2 * maxN + kValsSlack);
   return s;
 }
 
@@ -769,7 +857,10 @@ __device__ void meanshift_item(const TrackDev& d, int q, TrackSmem& sm, const Tr
 // a track whose estimated single-CTA time is below d.split_us (and whose
 // window fits 1/G of the scratch) it switches to split mode, where every CTA
 // claims and runs small tracks on its own (single-CTA barriers, no DSMEM).
-__global__ void __launch_bounds__(NT, 2) track_meanshift_kernel(TrackDev d) {
+#ifndef TRB_MS_MINBLOCKS
+#define TRB_MS_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(TrackDev d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
@@ -801,8 +892,8 @@ __global__ void __launch_bounds__(NT, 2) track_meanshift_kernel(TrackDev d) {
   // split mode: this CTA alone, with its 1/G share of the cluster scratch
   sm.grp = Grp::single();
   TrackScratch mine = scr;
-  mine.vals = scr.vals + static_cast<int64_t>(rank) * (2 * d.maxN / G);
-  mine.bins = scr.bins + static_cast<int64_t>(rank) * ((d.maxN / G) & ~15LL);  // 16-byte aligned shares
+  mine.vals = scr.vals + static_cast<int64_t>(rank) * ((2 * d.maxN + kValsSlack) / G);
+  mine.bins = scr.bins + static_cast<int64_t>(rank) * (((d.maxN + kBinsSlack) / G) & ~15LL);  // 16-byte aligned
   for (;;) {
     if (threadIdx.x == 0) {
       const int q = atomicAdd(d.work_head, 1);
@@ -1082,11 +1173,13 @@ void enable_itlog(bool on) {
   TRB_CUDA(cudaMemcpyToSymbol(g_itlog_n, &z, sizeof(z)));
   const int ph = on ? 1 : 0;
   TRB_CUDA(cudaMemcpyToSymbol(g_phase_on, &ph, sizeof(ph)));
-  unsigned long long zz[64] = {};
+  unsigned long long zz[128] = {};
   if (on) TRB_CUDA(cudaMemcpyToSymbol(g_phase, zz, sizeof(zz)));
 }
 
-void read_phases(unsigned long long* out64) { TRB_CUDA(cudaMemcpyFromSymbol(out64, g_phase, 64 * sizeof(*out64))); }
+void read_phases(unsigned long long* out128) {
+  TRB_CUDA(cudaMemcpyFromSymbol(out128, g_phase, 128 * sizeof(*out128)));
+}
 
 int64_t read_itlog(long long* out, int64_t cap) {
   long long* p = nullptr;

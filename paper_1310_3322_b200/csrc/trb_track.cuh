@@ -114,5 +114,5 @@ namespace trb {
 int* enable_progress(int n_ctas);
 void enable_itlog(bool on);
 int64_t read_itlog(long long* out, int64_t cap);
-void read_phases(unsigned long long* out64);
+void read_phases(unsigned long long* out128);
 }  // namespace trb

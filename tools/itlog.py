@@ -57,18 +57,17 @@ for lo, hi in [(0, 5e3), (5e3, 2e4), (2e4, 6e4), (6e4, 1.5e5), (1.5e5, 1e7)]:
 print("total iteration-time (cluster-us) per step:", cyc.sum() / 1.9e3 / steps, " max N", N.max())
 
 names = {1: "fill_u2", 2: "bin+count", 3: "count scan+sync", 4: "bin offsets", 5: "scatter+sync",
-         17: "bhattacharyya/wsq"}
-for b, nm in ((8, "hist"), (17, "cent")):
-    for st, what in enumerate(["A local", "A sync", "A gather+B", "C sync", "C+fold+rank", "rank sync",
-                               "D replay", "end sync"], start=1):
-        if b + st != 17:
-            names[b + st] = f"{nm} {what}"
-names[26] = "centroid div/hypot"
-for gi, gname in enumerate(("cluster", "single")):
-    tot = ph[gi].sum()
-    if not tot:
-        continue
-    print(f"--- {gname} runs: {tot / 1.9e3 / steps:.0f} us/step of rank-0 time")
-    for k in range(32):
-        if ph[gi, k]:
-            print(f"  {k:2d} {names.get(k, '?'):24s} {100 * ph[gi, k] / tot:5.1f}%")
+         6: "bhattacharyya/wsq", 30: "centroid div/hypot"}
+for b, nm in ((7, "hist"), (18, "cent")):
+    for st, what in enumerate(["A local", "A sync", "A gather+xP", "B walk", "C scan", "C sync", "C fold",
+                               "rank", "rank sync", "D replay", "end sync"], start=1):
+        names[b + st] = f"{nm} {what}"
+bnames = ("<5k px", "5k-50k px", "50k-150k px", ">150k px")
+print("phase us per iteration by window-size bucket:")
+print(f"  {'phase':24s}" + "".join(f"{b:>13s}" for b in bnames))
+cnt = np.maximum(ph[:, 0].astype(float), 1)
+print(f"  {'iterations/step':24s}" + "".join(f"{c / steps:13.1f}" for c in ph[:, 0]))
+for k in range(1, 32):
+    if ph[:, k].any():
+        print(f"  {k:2d} {names.get(k, '?'):21s}" + "".join(f"{ph[b, k] / cnt[b] / 1.9e3:13.2f}" for b in range(4)))
+print(f"  {'total':24s}" + "".join(f"{ph[b, 1:].sum() / cnt[b] / 1.9e3:13.2f}" for b in range(4)))
