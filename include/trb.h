@@ -231,9 +231,9 @@ int trb_debug_progress(int n_ctas, int** host_out);
  * cap {window pixels, SM cycles} pairs */
 int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n);
 /* per-phase SM cycles of the mean-shift iterations while the log is on:
- * [bucket][32] by window size (<5k, <50k, <150k, larger pixels); entry 0 of
- * a bucket counts its iterations (128 entries) */
-int trb_debug_phases(uint64_t* out128);
+ * [bucket][64] by window size (<5k, <50k, <150k, larger pixels); entry 0 of
+ * a bucket counts its iterations (256 entries) */
+int trb_debug_phases(uint64_t* out256);
 
 #ifdef __cplusplus
 }

@@ -482,9 +482,9 @@ def debug_itlog(enable=None):
 def debug_phases() -> np.ndarray:
     """Per-phase SM cycles of the logged mean-shift iterations, [4, 32] by
     window-size bucket (<5k, <50k, <150k, larger); [:, 0] = iterations."""
-    out = np.zeros(128, np.uint64)
+    out = np.zeros(256, np.uint64)
     _check(lib().trb_debug_phases(_ptr(out)))
-    return out.reshape(4, 32)
+    return out.reshape(4, 64)
 
 
 def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:

@@ -46,6 +46,10 @@
 
 #include "trb_exact.cuh"
 
+#ifndef TRB_OSUM_WALK_BEGIN
+#define TRB_OSUM_WALK_BEGIN()
+#define TRB_OSUM_WALK_END()
+#endif
 #ifndef TRB_OSUM_MARK
 #define TRB_OSUM_MARK(stage) ((void)0)
 #endif
@@ -212,11 +216,13 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   const int GT = G * NT, gt = rank * NT + t;
   const int C = Src::chunk(N, GT);
   const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
-  const double delta = static_cast<double>(N + 2 * C + 96 + G) * 2.220446049250313e-16;
+  // relative error bound of every approximate prefix P:
+  //   delta = (N + 2C + 96 + G) * 2^-52
   // mantissa bounds (units of 2^-52 of the binade) equivalent to a relative
-  // margin of >= 2*delta on each side
+  // margin of >= 2*delta on each side: 2*delta*2^52 = 2*(N + 2C + 96 + G)
+  // (integer arithmetic, so it stays cheap wherever the compiler re-derives it)
   constexpr long long kMant = (1LL << 52) - 1;
-  const long long marg = static_cast<long long>(delta * 4503599627370496.0 * 2.0) + 4;
+  const long long marg = 2LL * (N + 2 * C + 96 + G) + 4;
   const long long lowm = marg, highm = kMant - 2 * marg;
   const int cap_lane = kOsumBpRecs / L;
   const int buf = s.phase;  // double-buffer index for the CTA aggregates
@@ -350,6 +356,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   }
 
   TRB_OSUM_MARK(3);
+  TRB_OSUM_WALK_BEGIN();
   // ---------------- phase B: classify every step
   // A lane is "armed" for binade e once a step has been verified safe there:
   // P only grows inside a segment, so later steps stay safe while P_next <=
@@ -445,6 +452,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       }
     }
   }
+  TRB_OSUM_WALK_END();
   TRB_OSUM_MARK(4);
   if (tbad) atomicOr(&s.bad[0], 2);
   if (tover) atomicOr(&s.bad[0], 4);
@@ -474,7 +482,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       for (int l = 0; l < L; ++l) s.warp_p[wid][l] = sp[l], s.warp_pf[wid][l] = spf[l];
       s.warp_pbad[wid] = wbad;
     }
+    TRB_OSUM_MARK(20);
     __syncthreads();
+    TRB_OSUM_MARK(21);
     if (t == 0) {
       int bad = 0;
       for (int l = 0; l < L; ++l) {

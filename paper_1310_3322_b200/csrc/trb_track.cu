@@ -12,16 +12,20 @@ namespace trb {
 // [bucket][phase], bucket = window-size class of the iteration (<5k, <50k,
 // <150k, larger pixels); thread 0 of the group's rank-0 CTA adds the cycles
 // since its previous mark; [bucket][0] counts iterations.
-__device__ unsigned long long g_phase[128];
+__device__ unsigned long long g_phase[256];
 __device__ int g_phase_on;
 __shared__ long long s_ph_last;
 __shared__ int s_ph_bucket;
 }  // namespace trb
+// The device-side instrumentation below compiles only into the diagnostics
+// build (make diag -> libtrb_diag.so, -DTRB_DIAG); the product build has no
+// progress/phase/iteration-log code in its kernels.
+#ifdef TRB_DIAG
 #define TRB_PHASE(k, rank_, G_)                                                                   \
   do {                                                                                            \
     if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                  \
       const long long n_ = clock64();                                                             \
-      if ((k) >= 0) atomicAdd(&::trb::g_phase[(k) + 32 * ::trb::s_ph_bucket], n_ - ::trb::s_ph_last); \
+      if ((k) >= 0) atomicAdd(&::trb::g_phase[(k) + 64 * ::trb::s_ph_bucket], n_ - ::trb::s_ph_last); \
       ::trb::s_ph_last = n_;                                                                      \
     }                                                                                             \
   } while (0)
@@ -30,16 +34,34 @@ __shared__ int s_ph_bucket;
     if (::trb::g_phase_on && threadIdx.x == 0 && (rank_) == 0) {                                  \
       const int b_ = (n_px) < 5000 ? 0 : (n_px) < 50000 ? 1 : (n_px) < 150000 ? 2 : 3;            \
       ::trb::s_ph_bucket = b_;                                                                    \
-      atomicAdd(&::trb::g_phase[32 * b_], 1ull);                                                  \
+      atomicAdd(&::trb::g_phase[64 * b_], 1ull);                                                  \
       ::trb::s_ph_last = clock64();                                                               \
     }                                                                                             \
+  } while (0)
+// per-thread phase-B walk cycles of rank-0 CTAs: [40 + 2*(L==3)] max, [41 + 2*(L==3)] sum
+#define TRB_OSUM_WALK_BEGIN() const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0
+#define TRB_OSUM_WALK_END()                                                                        \
+  do {                                                                                             \
+    if (::trb::g_phase_on && rank == 0 && j0 < j1) {                                               \
+      const unsigned long long d_ = clock64() - walk_t0_;                                          \
+      atomicMax(&::trb::g_phase[64 * ::trb::s_ph_bucket + 40 + 2 * (L == 3)], d_);                 \
+      atomicAdd(&::trb::g_phase[64 * ::trb::s_ph_bucket + 41 + 2 * (L == 3)], d_);                 \
+    }                                                                                              \
   } while (0)
 #define TRB_OSUM_MARK(stage)                                                                   \
   do {                                                                                         \
     if (::trb::g_progress && threadIdx.x == 0)                                                 \
       (reinterpret_cast<volatile int*>(::trb::g_progress))[4 * blockIdx.x + 3] = 100 + (stage); \
-    TRB_PHASE((L == 1 ? 7 : 18) + (stage), rank, G);                                           \
+    TRB_PHASE((stage) >= 20 ? ((L == 1 ? 11 : 13) + (stage)) : ((L == 1 ? 7 : 18) + (stage)), rank, G); \
   } while (0)
+
+#else
+#define TRB_PHASE(k, rank_, G_) ((void)0)
+#define TRB_PHASE_BEGIN(n_px, rank_) ((void)0)
+#define TRB_OSUM_WALK_BEGIN()
+#define TRB_OSUM_WALK_END() ((void)0)
+#define TRB_OSUM_MARK(stage) ((void)0)
+#endif
 
 #include "trb_track.cuh"
 
@@ -53,6 +75,7 @@ __device__ unsigned long long g_trb_stats[32];
 // Optional per-iteration timing log: {window pixels, cycles} pairs.
 __device__ long long* g_itlog;
 __device__ unsigned long long g_itlog_n;
+#ifdef TRB_DIAG
 #define TRB_PROGRESS(slot, a, b, c, d)                                                      \
   do {                                                                                      \
     if (g_progress && threadIdx.x == 0) {                                                   \
@@ -60,6 +83,9 @@ __device__ unsigned long long g_itlog_n;
       p_[0] = (a), p_[1] = (b), p_[2] = (c), p_[3] = (d);                                   \
     }                                                                                       \
   } while (0)
+#else
+#define TRB_PROGRESS(slot, a, b, c, d) ((void)0)
+#endif
 
 namespace {
 
@@ -538,6 +564,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     cx = nx;
     cy = ny;
     TRB_PHASE(30, sm.grp.rank_, sm.grp.size_);
+#ifdef TRB_DIAG
     if (g_itlog && threadIdx.x == 0 && sm.grp.block_rank() == 0) {
       const unsigned long long k = atomicAdd(&g_itlog_n, 1ull);
       if (k < (1u << 16))
@@ -545,6 +572,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
                          (static_cast<long long>(sm.grp.size_) << 24) | ((r.x1 - r.x0) * (r.y1 - r.y0)),
         g_itlog[2 * k + 1] = clock64() - t_it0;
     }
+#endif
     if (shift < eps) break;
   }
 }
@@ -1173,12 +1201,12 @@ void enable_itlog(bool on) {
   TRB_CUDA(cudaMemcpyToSymbol(g_itlog_n, &z, sizeof(z)));
   const int ph = on ? 1 : 0;
   TRB_CUDA(cudaMemcpyToSymbol(g_phase_on, &ph, sizeof(ph)));
-  unsigned long long zz[128] = {};
+  unsigned long long zz[256] = {};
   if (on) TRB_CUDA(cudaMemcpyToSymbol(g_phase, zz, sizeof(zz)));
 }
 
 void read_phases(unsigned long long* out128) {
-  TRB_CUDA(cudaMemcpyFromSymbol(out128, g_phase, 128 * sizeof(*out128)));
+  TRB_CUDA(cudaMemcpyFromSymbol(out128, g_phase, 256 * sizeof(*out128)));
 }
 
 int64_t read_itlog(long long* out, int64_t cap) {

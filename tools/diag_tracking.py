@@ -5,6 +5,12 @@ python tools/diag_tracking.py --streams 8 --steps 10
 import argparse
 import os
 import sys
+
+# the diagnostics build of the library (make -C paper_1310_3322_b200/csrc diag)
+_DIAG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1310_3322_b200",
+                     "libtrb_diag.so")
+if os.path.exists(_DIAG):
+    os.environ.setdefault("TRB_LIB", _DIAG)
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

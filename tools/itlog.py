@@ -2,6 +2,12 @@
 import os
 import sys
 
+# the diagnostics build of the library (make -C paper_1310_3322_b200/csrc diag)
+_DIAG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1310_3322_b200",
+                     "libtrb_diag.so")
+if os.path.exists(_DIAG):
+    os.environ.setdefault("TRB_LIB", _DIAG)
+
 import numpy as np
 import torch
 
@@ -62,12 +68,19 @@ for b, nm in ((7, "hist"), (18, "cent")):
     for st, what in enumerate(["A local", "A sync", "A gather+xP", "B walk", "C scan", "C sync", "C fold",
                                "rank", "rank sync", "D replay", "end sync"], start=1):
         names[b + st] = f"{nm} {what}"
+names.update({31: "hist C warp scan", 32: "hist C barrier", 33: "cent C warp scan", 34: "cent C barrier"})
+walk = ph[:, 40:44].copy()
+ph[:, 40:44] = 0
 bnames = ("<5k px", "5k-50k px", "50k-150k px", ">150k px")
 print("phase us per iteration by window-size bucket:")
 print(f"  {'phase':24s}" + "".join(f"{b:>13s}" for b in bnames))
 cnt = np.maximum(ph[:, 0].astype(float), 1)
 print(f"  {'iterations/step':24s}" + "".join(f"{c / steps:13.1f}" for c in ph[:, 0]))
-for k in range(1, 32):
+for k in range(1, 64):
     if ph[:, k].any():
         print(f"  {k:2d} {names.get(k, '?'):21s}" + "".join(f"{ph[b, k] / cnt[b] / 1.9e3:13.2f}" for b in range(4)))
 print(f"  {'total':24s}" + "".join(f"{ph[b, 1:].sum() / cnt[b] / 1.9e3:13.2f}" for b in range(4)))
+print("per-thread B walk (rank-0 CTA threads with work): max cycles over the run, sum")
+for b in range(4):
+    print(f"  {bnames[b]:12s} hist max {walk[b,0]/1.9e3:9.1f} us  cent max {walk[b,2]/1.9e3:9.1f} us  "
+          f"hist sum/iter {walk[b,1]/cnt[b]/1.9e3:9.1f}  cent sum/iter {walk[b,3]/cnt[b]/1.9e3:9.1f} us")
