@@ -215,6 +215,30 @@ def reference_main(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------ multi-rank plumbing
+def shard(rank: int, streams_per_rank: int):
+    """Streams owned by `rank` (weak scaling: every rank owns the same number
+    of independent streams; no data-path collective)."""
+    return list(range(rank * streams_per_rank, (rank + 1) * streams_per_rank))
+
+
+def max_over_ranks(x: float, world: int, device="cpu") -> float:
+    """The job's time is the slowest rank's (all_reduce MAX; nccl tensors on
+    the rank's GPU, gloo on the host)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_fps(streams_per_rank: int, world: int, steps: int, seconds: float) -> float:
+    """Whole-job frames/s: every rank advanced its streams `steps` frames."""
+    return streams_per_rank * world * steps / seconds
+
+
 # -------------------------------------------------------------------- ours
 def make_frames(trb, clips, n_frames, stream):
     """Device-rasterised clip frames: uint8 [S, n_frames, px]."""
@@ -241,7 +265,7 @@ def ours_main(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
-    clips = [recipe("C5", rank * S + s) for s in range(S)]
+    clips = [recipe("C5", s) for s in shard(rank, S)]
     fill = W_DEFAULT - 1
     e2e_steps = 0 if args.no_e2e else K
     n_frames = fill + Wm + K + K + e2e_steps
@@ -276,12 +300,8 @@ def ours_main(args, rank, world, local_rank):
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world, dev)
     clk = clocks.stop()
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
 
     # ---- per-stage kernel times (second pass of K steps, events per stage)
     st.profile(True)
@@ -304,17 +324,13 @@ def ours_main(args, rank, world, local_rank):
         for k in range(e2e_steps):
             st.step_host(host[k], res, stream.cuda_stream)
         torch.cuda.synchronize()
-        secs = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([secs], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            secs = float(tt.item())
+        secs = max_over_ranks(time.perf_counter() - t0, world, dev)
         t += e2e_steps
-        e2e = {"value": S * world * e2e_steps / secs, "unit": "frames/s", "h2d_bytes_per_step": S * PX,
+        e2e = {"value": aggregate_fps(S, world, e2e_steps, secs), "unit": "frames/s", "h2d_bytes_per_step": S * PX,
                "d2h_bytes_per_step": 4 * S}
     st.synchronize()
 
-    value = S * world * K / (ms / 1e3)
+    value = aggregate_fps(S, world, K, ms / 1e3)
     peak, peak_kind = measured_peaks()
     motion_ms = stage_ms[0]
     achieved = MOTION_BYTES_PER_PX * S * PX / (motion_ms / 1e3) / 1e9

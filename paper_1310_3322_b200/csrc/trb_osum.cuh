@@ -49,6 +49,7 @@
 #ifndef TRB_OSUM_WALK_BEGIN
 #define TRB_OSUM_WALK_BEGIN()
 #define TRB_OSUM_WALK_END()
+#define TRB_OSUM_COUNT(v)
 #endif
 #ifndef TRB_OSUM_MARK
 #define TRB_OSUM_MARK(stage) ((void)0)
@@ -397,6 +398,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         P[l] = Pn;
         bool safe = !(SEG && start) && Pn <= hi[l];
         if (!safe) {
+          TRB_OSUM_COUNT(nslow_);
           // a zero step never changes S — except at a segment start, where it
           // must still open the segment (S = +0 + 0)
           if (vl == 0.0 && !(SEG && start)) continue;
@@ -431,6 +433,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
             pc[l].A = 0, pc[l].B = r;
           }
         } else {
+          TRB_OSUM_COUNT(nbp_);
           const int idx = atomicAdd(&s.nbp[l], 1);
           if (idx < cap_lane) {
             OsumBp& b = s.bp[l * cap_lane + idx];

@@ -39,13 +39,22 @@ __shared__ int s_ph_bucket;
     }                                                                                             \
   } while (0)
 // per-thread phase-B walk cycles of rank-0 CTAs: [40 + 2*(L==3)] max, [41 + 2*(L==3)] sum
-#define TRB_OSUM_WALK_BEGIN() const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0
+#define TRB_OSUM_WALK_BEGIN() \
+  const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0; \
+  unsigned long long nslow_ = 0, nbp_ = 0
+#define TRB_OSUM_COUNT(v) ++(v)
 #define TRB_OSUM_WALK_END()                                                                        \
   do {                                                                                             \
     if (::trb::g_phase_on && rank == 0 && j0 < j1) {                                               \
       const unsigned long long d_ = clock64() - walk_t0_;                                          \
-      atomicMax(&::trb::g_phase[64 * ::trb::s_ph_bucket + 40 + 2 * (L == 3)], d_);                 \
-      atomicAdd(&::trb::g_phase[64 * ::trb::s_ph_bucket + 41 + 2 * (L == 3)], d_);                 \
+      unsigned long long* ph_ = ::trb::g_phase + 64 * ::trb::s_ph_bucket;                         \
+      atomicMax(&ph_[40 + 2 * (L == 3)], d_);                                                      \
+      atomicAdd(&ph_[41 + 2 * (L == 3)], d_);                                                      \
+      atomicMax(&ph_[44 + 4 * (L == 3)], nslow_);                                                  \
+      atomicAdd(&ph_[45 + 4 * (L == 3)], nslow_);                                                  \
+      atomicMax(&ph_[46 + 4 * (L == 3)], nbp_);                                                    \
+      atomicAdd(&ph_[47 + 4 * (L == 3)], nbp_);                                                    \
+      atomicAdd(&ph_[52 + (L == 3)], 1ull);                                                        \
     }                                                                                              \
   } while (0)
 #define TRB_OSUM_MARK(stage)                                                                   \
@@ -60,6 +69,7 @@ __shared__ int s_ph_bucket;
 #define TRB_PHASE_BEGIN(n_px, rank_) ((void)0)
 #define TRB_OSUM_WALK_BEGIN()
 #define TRB_OSUM_WALK_END() ((void)0)
+#define TRB_OSUM_COUNT(v) ((void)0)
 #define TRB_OSUM_MARK(stage) ((void)0)
 #endif
 
