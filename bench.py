@@ -316,13 +316,17 @@ def ours_main(args, rank, world, local_rank):
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H timed
     e2e = None
     if e2e_steps:
+        # pinned host frames and per-step pinned result rows; the pipelined
+        # API overlaps step k+1's H2D with step k's kernels, every step's
+        # result (S blob counts) is read back to the host
         host = [[frames[s, t + k].cpu().pin_memory().numpy() for s in range(S)] for k in range(e2e_steps)]
-        res = np.zeros(S, np.int32)
+        res = torch.zeros((e2e_steps, S), dtype=torch.int32).pin_memory().numpy()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for k in range(e2e_steps):
-            st.step_host(host[k], res, stream.cuda_stream)
+            st.step_host_async(host[k], res[k], stream.cuda_stream)
+        st.synchronize()
         torch.cuda.synchronize()
         secs = max_over_ranks(time.perf_counter() - t0, world, dev)
         t += e2e_steps

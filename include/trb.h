@@ -164,6 +164,13 @@ int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* 
  * the H2D copy is part of the call.  If result_host is not NULL it
  * receives n_streams int32 blob counts (the D2H read of the step). */
 int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t* result_host, void* cuda_stream);
+/* Pipelined step_host: returns once the work is queued.  The frames' H2D
+ * copy runs on the handle's copy stream into one of two staging buffers and
+ * overlaps the previous step's kernels; result_host (if not NULL) is written
+ * when cuda_stream reaches this step.  frames and result_host must stay
+ * valid until trb_streams_synchronize (or a later synchronous call). */
+int trb_streams_step_host_async(trb_streams* s, const uint8_t* const* frames, int32_t* result_host,
+                                void* cuda_stream);
 int trb_streams_synchronize(trb_streams* s);
 int trb_streams_frames_seen(const trb_streams* s, int* n);
 /* 1 once the window is full (a mask/labels/blobs exist for the last step) */

@@ -119,6 +119,7 @@ def _declare(L):
         "trb_streams_destroy": [vp],
         "trb_streams_step_device": [vp, vp, vp],
         "trb_streams_step_host": [vp, vp, vp, vp],
+        "trb_streams_step_host_async": [vp, vp, vp, vp],
         "trb_streams_synchronize": [vp],
         "trb_streams_frames_seen": [vp, C.POINTER(C.c_int)],
         "trb_streams_has_output": [vp, C.POINTER(C.c_int)],
@@ -370,6 +371,16 @@ class Streams:
             self._ptrs[i] = f.ctypes.data
         rp = _ptr(result) if result is not None else None
         _check(lib().trb_streams_step_host(self._h, self._ptrs, rp, C.c_void_p(cuda_stream)))
+
+    def step_host_async(self, frames: Sequence[np.ndarray], result: Optional[np.ndarray] = None,
+                        cuda_stream: int = 0) -> None:
+        """Pipelined step_host: queued work only; `frames` and `result` must
+        stay alive (and unmodified) until synchronize()."""
+        ptrs = (C.c_void_p * len(frames))()
+        for i, f in enumerate(frames):
+            ptrs[i] = f.ctypes.data
+        rp = _ptr(result) if result is not None else None
+        _check(lib().trb_streams_step_host_async(self._h, ptrs, rp, C.c_void_p(cuda_stream)))
 
     def synchronize(self) -> None:
         _check(lib().trb_streams_synchronize(self._h))

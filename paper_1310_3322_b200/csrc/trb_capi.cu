@@ -461,6 +461,15 @@ int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t*
   });
 }
 
+int trb_streams_step_host_async(trb_streams* s, const uint8_t* const* frames, int32_t* result_host,
+                                void* cuda_stream) {
+  return guard([&] {
+    need(s && frames, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->step_host_async(frames, result_host, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
 int trb_streams_synchronize(trb_streams* s) {
   return guard([&] {
     need(s != nullptr, "null argument");

@@ -202,6 +202,11 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   for (int i = 0; i < kPtrSlots; ++i) TRB_CUDA(cudaEventCreateWithFlags(&slot_ev_[i], cudaEventDisableTiming));
   for (int i = 0; i < kStages + 1; ++i) TRB_CUDA(cudaEventCreate(&prof_ev_[i]));
   TRB_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
+  TRB_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    TRB_CUDA(cudaEventCreateWithFlags(&copied_[i], cudaEventDisableTiming));
+    TRB_CUDA(cudaEventCreateWithFlags(&consumed_[i], cudaEventDisableTiming));
+  }
 }
 
 Streams::~Streams() {
@@ -209,6 +214,11 @@ Streams::~Streams() {
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev_)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (copied_[i]) cudaEventDestroy(copied_[i]);
+    if (consumed_[i]) cudaEventDestroy(consumed_[i]);
+  }
+  if (copy_) cudaStreamDestroy(copy_);
   if (own_) cudaStreamDestroy(own_);
 }
 
@@ -260,25 +270,66 @@ void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
   TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
 }
 
-void Streams::step_host(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
+namespace {
+struct ResultCopy {
+  const int32_t* src;
+  int32_t* dst;
+  size_t bytes;
+};
+void CUDART_CB copy_result(void* p) {
+  auto* r = static_cast<ResultCopy*>(p);
+  std::memcpy(r->dst, r->src, r->bytes);
+  delete r;
+}
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
   if (!st) st = own_;
   const size_t fb = static_cast<size_t>(px_) * ch_;
-  if (!staging_.p) staging_.alloc(fb * S_, false);
+  const int b = host_step_++ & 1;
+  if (!staging_[b].p) staging_[b].alloc(fb * S_, false);
+  uint8_t* stage = staging_[b].as<uint8_t>();
+  // the copy may start once the step two back (same buffer) is done with it
+  TRB_CUDA(cudaStreamWaitEvent(copy_, consumed_[b], 0));
+  for (int s = 0; s < S_; ++s)
+    TRB_CUDA(cudaMemcpyAsync(stage + fb * s, frames[s], fb, cudaMemcpyHostToDevice, copy_));
+  TRB_CUDA(cudaEventRecord(copied_[b], copy_));
   std::vector<const uint8_t*> dev(S_);
-  for (int s = 0; s < S_; ++s) dev[s] = staging_.as<uint8_t>() + fb * s;
+  for (int s = 0; s < S_; ++s) dev[s] = stage + fb * s;
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(dev.data(), st);
-  for (int s = 0; s < S_; ++s)
-    TRB_CUDA(cudaMemcpyAsync(staging_.as<uint8_t>() + fb * s, frames[s], fb, cudaMemcpyHostToDevice, st));
+  TRB_CUDA(cudaStreamWaitEvent(st, copied_[b], 0));
   run_(dp, st);
   TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
+  TRB_CUDA(cudaEventRecord(consumed_[b], st));  // tracking read the frames too
   if (result_host) {
-    if (has_output_)
-      TRB_CUDA(cudaMemcpyAsync(result_host, ccl_->nblobs(), sizeof(int32_t) * S_, cudaMemcpyDeviceToHost, st));
-    else
-      std::memset(result_host, 0, sizeof(int32_t) * S_);
-    TRB_CUDA(cudaStreamSynchronize(st));
+    const size_t rb = sizeof(int32_t) * S_;
+    if (!has_output_) {
+      TRB_CUDA(cudaMemsetAsync(ccl_->nblobs(), 0, rb, st));
+    }
+    if (is_pinned(result_host)) {
+      TRB_CUDA(cudaMemcpyAsync(result_host, ccl_->nblobs(), rb, cudaMemcpyDeviceToHost, st));
+    } else {  // pageable: through a pinned buffer, copied out when the stream gets there
+      if (!result_pinned_.p) result_pinned_.alloc(rb);
+      TRB_CUDA(cudaMemcpyAsync(result_pinned_.p, ccl_->nblobs(), rb, cudaMemcpyDeviceToHost, st));
+      TRB_CUDA(cudaLaunchHostFunc(st, copy_result,
+                                  new ResultCopy{static_cast<const int32_t*>(result_pinned_.p), result_host, rb}));
+    }
   }
+}
+
+void Streams::step_host(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
+  if (!st) st = own_;
+  step_host_async(frames, result_host, st);
+  TRB_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace trb

@@ -108,7 +108,13 @@ class Streams {
           const trb_tracker_config& tc, bool with_tracker);
   ~Streams();
   void step_device(const uint8_t* const* frames_host_array_of_dev_ptrs, cudaStream_t st);
+  // synchronous: result_host (S blob counts) valid on return
   void step_host(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
+  // pipelined: the H2D copy of this step's frames runs on a copy stream
+  // (overlapping the previous step's kernels) into one of two staging
+  // buffers; result_host is written when `st` reaches this step (valid after
+  // synchronize()); frames_host must stay untouched until then.
+  void step_host_async(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
   cudaStream_t stream() const { return own_; }
   int S() const { return S_; }
   int w() const { return w_; }
@@ -137,7 +143,11 @@ class Streams {
   std::unique_ptr<MotionState> motion_;
   std::unique_ptr<CclState> ccl_;
   std::unique_ptr<TrackerState> tracker_;
-  DevBuf mask_, mask_tmp_, frame_ptrs_, staging_;
+  DevBuf mask_, mask_tmp_, frame_ptrs_, staging_[2];
+  PinnedBuf result_pinned_;
+  cudaStream_t copy_ = nullptr;
+  cudaEvent_t copied_[2] = {}, consumed_[2] = {};
+  int host_step_ = 0;
   PinnedBuf ptrs_host_;
   cudaStream_t own_ = nullptr;
   bool has_output_ = false;

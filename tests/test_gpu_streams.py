@@ -72,3 +72,29 @@ def test_streams_distinct_c5_streams_device_inputs(gpu):
         assert per[s]["mask_sha"] == [sha(m) for _, m, _, _ in out]
         assert per[s]["label_sha"] == [sha(l_) for _, _, l_, _ in out]
         assert per[s]["log"].tobytes() == log.tobytes()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_streams_pipelined_host_steps_match_golden(gpu, pinned):
+    """step_host_async (H2D on the copy stream into double-buffered staging,
+    overlapping the previous step; results land asynchronously): per-step
+    blob counts and the final track logs equal the reference's."""
+    import torch
+    name, clip, n, window = "c1_pipeline", recipe("C1"), 160, 91
+    g = np.load(os.path.join(GOLD, name + ".npz"))
+    frames = O.orc_frames(clip, n)[0]
+    if pinned:
+        host = [torch.from_numpy(frames[t]).pin_memory().numpy() for t in range(n)]
+        res = torch.zeros((n, 2), dtype=torch.int32).pin_memory().numpy()
+    else:
+        host = [frames[t].copy() for t in range(n)]
+        res = np.zeros((n, 2), np.int32)
+    st = gpu.Streams(2, clip.width, clip.height, clip.channels, MOTION_CFG(window=window), SEG_CFG(), TRACKER_CFG())
+    for t in range(n):
+        st.step_host_async([host[t], host[t]], res[t])
+    st.synchronize()
+    emitted = res[window - 1:]
+    for s in range(2):
+        assert (emitted[:, s] == g["nblobs"]).all()
+        assert st.log(s).tobytes() == g["log"].tobytes()
+    assert (res[:window - 1] == 0).all()
