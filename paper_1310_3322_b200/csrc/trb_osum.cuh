@@ -127,6 +127,8 @@ struct OsumShared {
   double cta_d[2][4];         // phase A CTA aggregate (double-buffered)
   Piece warp_p[32][3];
   int warp_pf[32][3];
+  Piece wpre_p[32][3];  // phase C: exclusive prefix of the warps before w (inside the CTA)
+  int wpre_f[32][3];
   int warp_pbad[32];
   Piece cta_p[2][3];
   int cta_pf[2][3];
@@ -494,6 +496,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         Piece a = piece_identity();
         int f = 0;
         for (int w = 0; w < nw; ++w) {
+          s.wpre_p[w][l] = a, s.wpre_f[w][l] = f;
           bad |= s.warp_pbad[w];
           if (s.warp_pf[w][l]) a = s.warp_p[w][l], f = 1;
           else a = compose(a, s.warp_p[w][l], &bad);
@@ -536,10 +539,8 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
     for (int l = 0; l < L; ++l) {
       Piece a = s.carry_p[l];
       int bad = 0;
-      for (int w = 0; w < wid; ++w) {
-        if (s.warp_pf[w][l]) a = s.warp_p[w][l];
-        else a = compose(a, s.warp_p[w][l], &bad);
-      }
+      if (s.wpre_f[wid][l]) a = s.wpre_p[wid][l];
+      else a = compose(a, s.wpre_p[wid][l], &bad);
       const Piece lp = shfl_up_piece(sp[l], 1);
       const int lf = __shfl_up_sync(0xffffffffu, spf[l], 1);
       if (lane > 0) {
@@ -624,10 +625,11 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         if (p.e == kEmptyE) return;
         const int pe = (p.e > -1000 && p.e < 1000) ? p.e : 0;
         ok &= osum_exp(S) == pe;
-        const long long X = static_cast<long long>(xmul(S, osum_pow2(52 - pe)));
+        // S = X * 2^(pe-52) with X its 53-bit significand: integer ops only
+        const long long X = (__double_as_longlong(S) & kMant) | (1LL << 52);
         const long long X2 = apply(p, X);
         ok &= X2 >= (1LL << 52) && X2 < (1LL << 53);
-        S = xmul(static_cast<double>(X2), osum_pow2(pe - 52));
+        S = __longlong_as_double((static_cast<long long>(pe + 1023) << 52) | (X2 & kMant));
       };
       for (int q = q0; q < q1; ++q) {
         TRB_CHECK(q >= 0 && q < cap_g, "replay read", q, n);

@@ -455,18 +455,22 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   // (parallel DSMEM loads into gcnt[q][b], then one thread combines locally)
   for (int i = t; i < G * NB; i += NT_) sm.gcnt[i] = *cl.map_shared_rank(&sm.bincta[i % NB], i / NB);
   __syncthreads();
+  for (int b = t; b < NB; b += NT_) {  // per segment: this CTA's carry and the cluster total
+    int carry = 0, tot = 0;
+    for (int q = 0; q < G; ++q) {
+      const int c = sm.gcnt[q * NB + b];
+      if (q < rank) carry += c;
+      tot += c;
+    }
+    sm.red[b] = carry, sm.red[NT_ + b] = tot;
+  }
+  __syncthreads();
   if (t == 0) {
     int off = 0;
     for (int b = 0; b < NB; ++b) {
-      int carry = 0, tot = 0;
-      for (int q = 0; q < G; ++q) {
-        const int c = sm.gcnt[q * NB + b];
-        if (q < rank) carry += c;
-        tot += c;
-      }
       sm.binoff[b] = off;
-      sm.red[b] = off + carry;  // where this CTA's segment-b run starts
-      off += tot;
+      sm.red[b] += off;  // where this CTA's segment-b run starts
+      off += static_cast<int>(sm.red[NT_ + b]);
     }
     sm.binoff[NB] = off;
   }
@@ -754,6 +758,176 @@ __device__ void kmeans_device(const Src& src, int n, int K, int iters, uint64_t 
         __shared__ double w_d[NT];
         __shared__ int w_i[NT];
         w_d[t] = (j0 < j1) ? bd : -2.0;
+        w_i[t] = bi;
+        __syncthreads();
+        for (int o = NT / 2; o > 0; o >>= 1) {
+          if (t < o) {
+            const double d2 = w_d[t + o];
+            const int i2 = w_i[t + o];
+            if (d2 > w_d[t] || (d2 == w_d[t] && i2 < w_i[t])) w_d[t] = d2, w_i[t] = i2;
+          }
+          __syncthreads();
+        }
+        int r, g, b;
+        src.get(w_i[0], r, g, b);
+        nc3[0] = r, nc3[1] = g, nc3[2] = b;
+        __syncthreads();
+      } else {
+        const double m = static_cast<double>(cnt[c]);
+        nc3[0] = xdiv(static_cast<double>(sum[3 * c]), m);
+        nc3[1] = xdiv(static_cast<double>(sum[3 * c + 1]), m);
+        nc3[2] = xdiv(static_cast<double>(sum[3 * c + 2]), m);
+      }
+      if (t == 0) {
+        if (nc3[0] != cen[3 * c] || nc3[1] != cen[3 * c + 1] || nc3[2] != cen[3 * c + 2]) sm.iscal[2] = 1;
+        cen[3 * c] = nc3[0], cen[3 * c + 1] = nc3[1], cen[3 * c + 2] = nc3[2];
+      }
+      __syncthreads();
+    }
+    if (!sm.iscal[2]) break;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+// quantize_colors for a GRAY window (r = g = b): every per-sample quantity
+// of kmeans_device depends on the sample's gray value only, so after one
+// pass that builds the window's 256-bin histogram and the first raster
+// index of every value, the Lloyd sums, the assignments and the
+// empty-cluster farthest point are O(256) per pass instead of O(n).  The
+// k-means++ prefix search still walks the samples in raster order (with a
+// 256-entry D^2 table).  Same integers, same fp64 operations, same RNG
+// draws as kmeans_device: identical centres.  Needs 1024 ints of sm.cnt.
+__device__ void kmeans_gray_device(const FrameWindowSrc& src, int n, int K, int iters, uint64_t seed, TrackSmem& sm,
+                                   Mt64* rng) {
+  const int t = threadIdx.x;
+  const int C = (n + NT - 1) / NT;
+  const int j0 = min(n, t * C), j1 = min(n, j0 + C);
+  double* cen = sm.cen;
+  int* hist = sm.cnt;          // [256] samples per gray value
+  int* firsti = sm.cnt + 256;  // [256] first raster index of the value
+  int* dtab = sm.cnt + 512;    // [256] D^2 to the nearest seed
+  int* asg = sm.cnt + 768;     // [256] Lloyd assignment
+  const int ww = src.ww;
+  // walk samples j0..j1-1 of the window in raster order: f(i, gray)
+  auto walk = [&](auto&& f) {
+    if (j0 >= j1) return;
+    int xx = j0 % ww;
+    const uint8_t* row = src.frame + static_cast<int64_t>(src.y0 + j0 / ww) * src.fw + src.x0;
+    for (int i = j0; i < j1; ++i) {
+      if (!f(i, static_cast<int>(row[xx]))) return;
+      if (++xx == ww) xx = 0, row += src.fw;
+    }
+  };
+  for (int v = t; v < 256; v += NT) hist[v] = 0, firsti[v] = INT_MAX;
+  __syncthreads();
+  {
+    int cur = -1, run = 0;
+    walk([&](int i, int v) {
+      if (v != cur) {
+        if (run) atomicAdd(&hist[cur], run);
+        cur = v, run = 0;
+        atomicMin(&firsti[v], i);
+      }
+      ++run;
+      return true;
+    });
+    if (run) atomicAdd(&hist[cur], run);
+  }
+  if (t == 0) {
+    rng->seed(seed);
+    const int64_t first = rng->uniform_int(0, static_cast<int64_t>(n) - 1);
+    int r, g, b;
+    src.get(static_cast<int>(first), r, g, b);
+    cen[0] = r, cen[1] = g, cen[2] = b;
+  }
+  __syncthreads();
+  for (int nc = 1; nc < K; ++nc) {
+    for (int v = t; v < 256; v += NT) {
+      int best = INT_MAX;
+      for (int c = 0; c < nc; ++c) {
+        const int dr = v - static_cast<int>(cen[3 * c]), dg = v - static_cast<int>(cen[3 * c + 1]),
+                  db = v - static_cast<int>(cen[3 * c + 2]);
+        best = min(best, dr * dr + dg * dg + db * db);
+      }
+      dtab[v] = best;
+    }
+    __syncthreads();
+    long long local = 0;
+    walk([&](int, int v) {
+      local += dtab[v];
+      return true;
+    });
+    const long long pre = block_exscan_ll(local, sm.red);
+    const long long total = block_sum_ll(local, sm.red);
+    if (t == 0) {
+      sm.iscal[1] = n - 1;
+      if (total > 0) sm.scal[0] = xmul(rng->uniform(), static_cast<double>(total));
+      else sm.iscal[1] = 0;
+    }
+    __syncthreads();
+    if (total > 0) {
+      const double r = sm.scal[0];
+      if (static_cast<double>(pre + local) > r && (t == 0 || !(static_cast<double>(pre) > r))) {
+        long long acc = pre;
+        walk([&](int i, int v) {
+          acc += dtab[v];
+          if (static_cast<double>(acc) > r) {
+            sm.iscal[1] = i;
+            return false;
+          }
+          return true;
+        });
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      int r, g, b;
+      src.get(sm.iscal[1], r, g, b);
+      cen[3 * nc] = r, cen[3 * nc + 1] = g, cen[3 * nc + 2] = b;
+    }
+    __syncthreads();
+  }
+  long long* cnt = sm.red;      // [K]
+  long long* sum = sm.red + K;  // [3K]
+  double* old = sm.old;
+  __shared__ double w_d[NT];
+  __shared__ int w_i[NT];
+  if (t == 0) atomicAdd(&g_trb_stats[6], 1ull);
+  for (int it = 0; it < iters; ++it) {
+    if (t == 0) atomicAdd(&g_trb_stats[7], 1ull);
+    for (int i = t; i < 3 * K; i += NT) old[i] = cen[i];
+    for (int i = t; i < 4 * K; i += NT) sm.red[i] = 0;
+    __syncthreads();
+    for (int v = t; v < 256; v += NT) {
+      const int a = q_assign(old, K, v, v, v);
+      asg[v] = a;
+      if (hist[v]) {
+        const unsigned long long hv = static_cast<unsigned long long>(hist[v]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[a]), hv);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a]), hv * v);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a + 1]), hv * v);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sum[3 * a + 2]), hv * v);
+      }
+    }
+    __syncthreads();
+    if (t == 0) sm.iscal[2] = 0;
+    __syncthreads();
+    for (int c = 0; c < K; ++c) {
+      double nc3[3];
+      if (cnt[c] == 0) {
+        if (t == 0) atomicAdd(&g_trb_stats[8], 1ull);
+        // farthest sample (old assignment, current centres; first index on ties)
+        double bd = -2.0;
+        int bi = INT_MAX;
+        for (int v = t; v < 256; v += NT)
+          if (hist[v]) {
+            const int a = asg[v];
+            const double dr = xsub(v, cen[3 * a]), dg = xsub(v, cen[3 * a + 1]), db = xsub(v, cen[3 * a + 2]);
+            const double dd = xadd(xadd(xmul(dr, dr), xmul(dg, dg)), xmul(db, db));
+            if (dd > bd || (dd == bd && firsti[v] < bi)) bd = dd, bi = firsti[v];
+          }
+        w_d[t] = bd;
         w_i[t] = bi;
         __syncthreads();
         for (int o = NT / 2; o > 0; o >>= 1) {
@@ -1126,7 +1300,11 @@ __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
       const Win r = clip_window(d.W, d.H, cx, cy, w, h);
       FrameWindowSrc src{d.frames[s], d.W, d.CH, r.x0, r.y0, r.x1 - r.x0, UDiv32::make(r.x1 - r.x0)};
       const int n = (r.x1 - r.x0) * (r.y1 - r.y0);
-      kmeans_device(src, n, K, d.kmeans_iters, mix_seed(d.seed, static_cast<uint64_t>(d.id[g])), sm, &rng);
+      const uint64_t seed = mix_seed(d.seed, static_cast<uint64_t>(d.id[g]));
+      if (gray && (K + 1) * NT >= 1024)
+        kmeans_gray_device(src, n, K, d.kmeans_iters, seed, sm, &rng);
+      else
+        kmeans_device(src, n, K, d.kmeans_iters, seed, sm, &rng);
       for (int rr = 1; rr < G; ++rr)
         for (int k = threadIdx.x; k < 3 * K; k += NT) *cl.map_shared_rank(&sm.cen[k], rr) = sm.cen[k];
     }
