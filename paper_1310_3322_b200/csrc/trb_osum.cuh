@@ -37,8 +37,8 @@
 //   phase C  segmented cluster scan of the thread pieces (reset at
 //            breakpoints); the carried-in piece is folded into each thread's
 //            first breakpoint; breakpoints ranked into one cluster list
-//   phase D  CTA 0 replays each lane / segment serially and broadcasts the
-//            results through DSMEM.
+//   phase D  every CTA replays each lane / segment serially from its copy
+//            of the gathered list (no barrier after it).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -50,6 +50,7 @@
 #define TRB_OSUM_WALK_BEGIN()
 #define TRB_OSUM_WALK_END()
 #define TRB_OSUM_COUNT(v)
+#define TRB_OSUM_WALK_FIRST(cond, dep)
 #endif
 #ifndef TRB_OSUM_MARK
 #define TRB_OSUM_MARK(stage) ((void)0)
@@ -189,6 +190,24 @@ struct Grp {
     return size_ > 1 ? cg::this_cluster().map_shared_rank(p, r) : p;
   }
 };
+
+// A safe step a of binade e (M = 2^e) appended to the thread's piece.  The
+// identity piece is {B = 0, A = 0, tie = 0}, so a plain step needs no test of
+// emptiness: B += r and the binade is (re)stated.
+__device__ __forceinline__ void osum_step_safe(Piece& pc, double a, double M, int e, int& tbad) {
+  const double y = xadd(M, a);
+  const double d = xsub(a, xsub(y, M));
+  const long long r = __double_as_longlong(y) - __double_as_longlong(M);
+  const double hu = __longlong_as_double(__double_as_longlong(M) - (53LL << 52));  // u/2
+  if (fabs(d) == hu) {  // a/u = k + 1/2
+    Piece q;
+    q.e = e, q.tie = 1, q.A = d > 0.0 ? r : r - 1, q.B = 0;
+    pc = compose(pc, q, &tbad);
+  } else {
+    pc.B += r;
+    pc.e = e;
+  }
+}
 
 // warp-shuffle helpers for the scan payloads
 __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
@@ -370,9 +389,11 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   Piece pc[L];
   int hadbp[L], firstbp[L];
   double hi[L], M[L];
+  int ea[L];
   int tbad = 0, tover = 0;
 #pragma unroll
-  for (int l = 0; l < L; ++l) pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1, hi[l] = -1.0, M[l] = 1.0;
+  for (int l = 0; l < L; ++l)
+    pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1, hi[l] = -1.0, M[l] = 1.0, ea[l] = 0;
   {
     double P[L];
 #pragma unroll
@@ -388,6 +409,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       int seg;
       double v[L];
       cur.next(k, start, seg, has, v);
+      TRB_OSUM_WALK_FIRST(j == j0, v[0]);
       if (SEG && start)
 #pragma unroll
         for (int l = 0; l < L; ++l) P[l] = 0.0;
@@ -398,42 +420,31 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         const double Pp = P[l];
         const double Pn = xadd(Pp, vl);
         P[l] = Pn;
-        bool safe = !(SEG && start) && Pn <= hi[l];
-        if (!safe) {
-          TRB_OSUM_COUNT(nslow_);
-          // a zero step never changes S — except at a segment start, where it
-          // must still open the segment (S = +0 + 0)
-          if (vl == 0.0 && !(SEG && start)) continue;
-          if (Pp > 0.0 && !(SEG && start)) {
-            // P and P_next in one binade with relative margin delta on both
-            // sides, checked on the raw bits: P(1-delta) >= 2^e and
-            // P_next(1+delta) < 2^(e+1)  <=  mantissa(P) >= lowm, mantissa(P_next) <= highm
-            const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
-            const int eb = static_cast<int>(bp_ >> 52);
-            if (eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm &&
-                (bn_ & kMant) <= highm) {
-              hi[l] = __longlong_as_double((static_cast<long long>(eb) << 52) | highm);
-              M[l] = osum_pow2(eb - 1023);
-              safe = true;
-            }
+        if (!(SEG && start) && Pn <= hi[l]) {  // armed: a safe step of binade ea
+          osum_step_safe(pc[l], vl, M[l], ea[l], tbad);
+          continue;
+        }
+        TRB_OSUM_COUNT(nslow_);
+        // a zero step never changes S — except at a segment start, where it
+        // must still open the segment (S = +0 + 0)
+        if (vl == 0.0 && !(SEG && start)) continue;
+        bool safe = false;
+        if (Pp > 0.0 && !(SEG && start)) {
+          // P and P_next in one binade with relative margin delta on both
+          // sides, checked on the raw bits: P(1-delta) >= 2^e and
+          // P_next(1+delta) < 2^(e+1)  <=  mantissa(P) >= lowm, mantissa(P_next) <= highm
+          const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
+          const int eb = static_cast<int>(bp_ >> 52);
+          if (eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm &&
+              (bn_ & kMant) <= highm) {
+            hi[l] = __longlong_as_double((static_cast<long long>(eb) << 52) | highm);
+            M[l] = osum_pow2(eb - 1023);
+            ea[l] = eb - 1023;
+            safe = true;
           }
         }
         if (safe) {
-          const double y = xadd(M[l], vl);
-          const double d = xsub(vl, xsub(y, M[l]));
-          const long long r = __double_as_longlong(y) - __double_as_longlong(M[l]);
-          const double hu = __longlong_as_double(__double_as_longlong(M[l]) - (53LL << 52));  // u/2
-          if (fabs(d) == hu) {  // a/u = k + 1/2
-            Piece q;
-            q.e = static_cast<int>(__double_as_longlong(M[l]) >> 52) - 1023, q.tie = 1;
-            q.A = d > 0.0 ? r : r - 1, q.B = 0;
-            pc[l] = compose(pc[l], q, &tbad);
-          } else if (pc[l].e != kEmptyE) {
-            pc[l].B += r;  // same binade (binade changes are breakpoints)
-          } else {
-            pc[l].e = static_cast<int>(__double_as_longlong(M[l]) >> 52) - 1023, pc[l].tie = 0;
-            pc[l].A = 0, pc[l].B = r;
-          }
+          osum_step_safe(pc[l], vl, M[l], ea[l], tbad);
         } else {
           TRB_OSUM_COUNT(nbp_);
           const int idx = atomicAdd(&s.nbp[l], 1);
@@ -564,29 +575,35 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   }
   __syncthreads();
   TRB_OSUM_MARK(7);
-  // rank each CTA list by element index into the cluster list
-  // (DSMEM stores straight into CTA 0's gathered list)
+  // rank each CTA list by element index into the cluster list, stored
+  // (DSMEM) into EVERY CTA's gathered list: each CTA then replays locally and
+  // no barrier is needed after the replay
   const int cap_g = kOsumGather / L;
   for (int l = 0; l < L; ++l) {
     const int n = min(s.nbp[l], cap_lane);
-    OsumBp* out = cl.map_shared_rank(&s.gbp[0], 0) + l * cap_g;
     for (int i = t; i < n; i += NT) {
       const int ji = s.bp[l * cap_lane + i].j;
       int rk = 0;
       for (int q = 0; q < n; ++q) rk += s.bp[l * cap_lane + q].j < ji;
       const int pos = s.bp_base[l] + rk;
-      if (pos < cap_g) out[pos] = s.bp[l * cap_lane + i];
-      else atomicOr(&s.bad[0], 4);
+      if (pos < cap_g) {
+        const OsumBp rec = s.bp[l * cap_lane + i];
+        for (int dst = 0; dst < G; ++dst) cl.map_shared_rank(&s.gbp[0], dst)[l * cap_g + pos] = rec;
+      } else {
+        atomicOr(&s.bad[0], 4);
+      }
     }
   }
   __syncthreads();
-  if (t == 0 && s.bad[0] && rank != 0) atomicOr(cl.map_shared_rank(&s.bad[0], 0), s.bad[0]);
+  if (t == 0 && s.bad[0])
+    for (int dst = 0; dst < G; ++dst)
+      if (dst != rank) atomicOr(cl.map_shared_rank(&s.bad[0], dst), s.bad[0]);
   TRB_OSUM_MARK(8);
   cl.sync();
   TRB_OSUM_MARK(9);
 
-  // ---------------- phase D: replay on CTA 0
-  if (rank == 0) {
+  // ---------------- phase D: replay (every CTA, identical inputs)
+  {
     const int why = s.bad[0];
     if (why && t == 0) s.bad[1] = 1;
     const int nlanes = SEG ? nseg : L;
@@ -642,7 +659,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       if (!ok) atomicOr(&s.bad[1], 1);
     }
     __syncthreads();
-    if (stats && t == 0) {
+    if (stats && t == 0 && rank == 0) {
       atomicAdd(&stats[0], 1ull);
       atomicAdd(&stats[1], static_cast<unsigned long long>(nlanes));
       unsigned long long nb = 0;
@@ -692,12 +709,14 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       }
       __syncthreads();
     }
-    for (int r = 1; r < G; ++r)
-      for (int k = t; k < nlanes; k += NT) *cl.map_shared_rank(&s.result[k], r) = s.result[k];
   }
   if (t == 0) s.phase = buf ^ 1;
   TRB_OSUM_MARK(10);
-  cl.sync();
+  // No cluster barrier: the results are local.  A CTA that runs ahead
+  // cannot touch another CTA's shared memory or the element data before that
+  // CTA reaches the next run's barriers, and every remote read of this run
+  // happened before the barrier above.
+  __syncthreads();
   TRB_OSUM_MARK(11);
 }
 

@@ -41,7 +41,11 @@ __shared__ int s_ph_bucket;
 // per-thread phase-B walk cycles of rank-0 CTAs: [40 + 2*(L==3)] max, [41 + 2*(L==3)] sum
 #define TRB_OSUM_WALK_BEGIN() \
   const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0; \
+  long long walk_t1_ = walk_t0_;                                 \
   unsigned long long nslow_ = 0, nbp_ = 0
+// time to the first element's data (cursor start-up); `dep` forces the wait
+#define TRB_OSUM_WALK_FIRST(cond, dep) \
+  if ((cond) && ::trb::g_phase_on) walk_t1_ = clock64() + ((dep) != (dep) ? 1 : 0)
 #define TRB_OSUM_COUNT(v) ++(v)
 #define TRB_OSUM_WALK_END()                                                                        \
   do {                                                                                             \
@@ -55,6 +59,7 @@ __shared__ int s_ph_bucket;
       atomicMax(&ph_[46 + 4 * (L == 3)], nbp_);                                                    \
       atomicAdd(&ph_[47 + 4 * (L == 3)], nbp_);                                                    \
       atomicAdd(&ph_[52 + (L == 3)], 1ull);                                                        \
+      atomicAdd(&ph_[54 + (L == 3)], static_cast<unsigned long long>(walk_t1_ - walk_t0_));       \
     }                                                                                              \
   } while (0)
 #define TRB_OSUM_MARK(stage)                                                                   \
@@ -70,6 +75,7 @@ __shared__ int s_ph_bucket;
 #define TRB_OSUM_WALK_BEGIN()
 #define TRB_OSUM_WALK_END() ((void)0)
 #define TRB_OSUM_COUNT(v) ((void)0)
+#define TRB_OSUM_WALK_FIRST(cond, dep) ((void)0)
 #define TRB_OSUM_MARK(stage) ((void)0)
 #endif
 

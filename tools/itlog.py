@@ -69,8 +69,8 @@ for b, nm in ((7, "hist"), (18, "cent")):
                                "rank", "rank sync", "D replay", "end sync"], start=1):
         names[b + st] = f"{nm} {what}"
 names.update({31: "hist C warp scan", 32: "hist C barrier", 33: "cent C warp scan", 34: "cent C barrier"})
-walk = ph[:, 40:54].copy()
-ph[:, 40:54] = 0
+walk = ph[:, 40:56].copy()
+ph[:, 40:56] = 0
 bnames = ("<5k px", "5k-50k px", "50k-150k px", ">150k px")
 print("phase us per iteration by window-size bucket:")
 print(f"  {'phase':24s}" + "".join(f"{b:>13s}" for b in bnames))
@@ -90,3 +90,8 @@ for b in range(4):
     nt1, nt3 = max(1, w[12]), max(1, w[13])
     print(f"  {bnames[b]:12s} hist slow {w[4]:5d} / {w[5]/nt1:6.2f}  bp {w[6]:5d} / {w[7]/nt1:6.2f}   "
           f"cent slow {w[8]:5d} / {w[9]/nt3:6.2f}  bp {w[10]:5d} / {w[11]/nt3:6.2f}")
+print("cursor start-up (walk begin -> first element's data), mean per walking thread")
+for b in range(4):
+    w = walk[b]
+    nt1, nt3 = max(1, w[12]), max(1, w[13])
+    print(f"  {bnames[b]:12s} hist {w[14]/nt1/1.9e3:7.2f} us   cent {w[15]/nt3/1.9e3:7.2f} us")
