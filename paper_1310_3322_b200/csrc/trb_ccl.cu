@@ -103,9 +103,24 @@ __device__ __forceinline__ SlotTable slot_base(const CclArgs& a, int s) {
 }  // namespace
 
 // ------------------------------------------------------------------ local
+// Run-based: warp w loads rows w, w+8, w+16, w+24 (lane = column) and a
+// ballot turns each row into a 32-bit mask; horizontal runs are bit runs.
+// Only run-start pixels enter the union-find (a run's pixels share its
+// start), and only vertical run adjacencies are unioned; statistics are
+// accumulated per run (area = length, sum x = arithmetic series).
+__device__ __forceinline__ int run_len(uint32_t m, int c) {  // ones from bit c up
+  const uint32_t z = ~(m >> c);
+  return z ? __ffs(z) - 1 : 32 - c;
+}
+__device__ __forceinline__ int run_start_at(uint32_t starts, int p) {  // start of the run covering bit p
+  const uint32_t x = starts & (p == 31 ? 0xffffffffu : ((2u << p) - 1));
+  return 31 - __clz(x);
+}
+
 __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   __shared__ int lab[kTilePx];
   __shared__ int cid[kTilePx];  // compact component id of each local root
+  __shared__ uint32_t rowm[kTileH], starts[kTileH];
   __shared__ int st_area[kMaxTileComps], st_x0[kMaxTileComps], st_y0[kMaxTileComps], st_x1[kMaxTileComps],
       st_y1[kMaxTileComps], st_sx[kMaxTileComps], st_sy[kMaxTileComps];
   __shared__ int n_comp, slot_base_id;
@@ -114,62 +129,69 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
   const int tx0 = blockIdx.x * kTileW, ty0 = blockIdx.y * kTileH;
-  // thread -> (row r, 4 consecutive columns c0..c0+3): one 32-bit mask load
-  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
-  const int gy = ty0 + r, gx0 = tx0 + c0;
+  const int w = threadIdx.x >> 5, c = threadIdx.x & 31, gx = tx0 + c;
   if (threadIdx.x == 0) n_comp = 0;
 
-  // 1. load: every foreground pixel starts as its own root
-  bool fg[4];
-  uint32_t word = 0;
-  if (gy < a.h) {
-    const uint8_t* row = mask + static_cast<int64_t>(gy) * a.w;
-    if (a.w % 4 == 0 && gx0 + 4 <= a.w) {
-      word = *reinterpret_cast<const uint32_t*>(row + gx0);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (gx0 + k < a.w && row[gx0 + k]) word |= 1u << (8 * k);
-    }
-  }
+  // 1. rows as bit masks
   bool any = false;
+  uint32_t mine = 0;  // bit rr: pixel (row w + 8*rr, column c) is foreground
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    fg[k] = ((word >> (8 * k)) & 0xffu) != 0;
-    any |= fg[k];
-    lab[r * kTileW + c0 + k] = fg[k] ? r * kTileW + c0 + k : -1;
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr, gy = ty0 + r;
+    const bool fg = gy < a.h && gx < a.w && mask[static_cast<int64_t>(gy) * a.w + gx] != 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, fg);
+    if (c == 0) rowm[r] = m, starts[r] = m & ~(m << 1);
+    mine |= static_cast<uint32_t>(fg) << rr;
+    any |= fg;
   }
   // most tiles are pure background: leave at once
   if (!__syncthreads_or(any)) return;
 
-  // 2. merge with the already-visited neighbours inside the tile
-  //    (label_window's left / up / up-left / up-right, segmentation.hpp:169-174)
+  // 2. run starts are the union-find nodes
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (!fg[k]) continue;
-    const int c = c0 + k, i = r * kTileW + c;
-    if (c > 0 && lab[i - 1] >= 0) sunion(lab, i, i - 1);
-    if (r > 0) {
-      if (lab[i - kTileW] >= 0) {
-        sunion(lab, i, i - kTileW);
-      } else if (a.conn == TRB_CONN_EIGHT) {
-        if (c > 0 && lab[i - kTileW - 1] >= 0) sunion(lab, i, i - kTileW - 1);
-        if (c < kTileW - 1 && lab[i - kTileW + 1] >= 0) sunion(lab, i, i - kTileW + 1);
-      }
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr;
+    if ((starts[r] >> c) & 1u) lab[r * kTileW + c] = r * kTileW + c;
+  }
+  __syncthreads();
+  // 3. union every run with the runs of the row above that touch it
+  //    (label_window's up / up-left / up-right neighbours, segmentation.hpp:169-174)
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr;
+    if (r == 0 || !((starts[r] >> c) & 1u)) continue;
+    const uint32_t up = rowm[r - 1];
+    if (!up) continue;
+    const int b = c + run_len(rowm[r], c) - 1;
+    const int lo = a.conn == TRB_CONN_EIGHT ? max(c - 1, 0) : c;
+    const int hi = a.conn == TRB_CONN_EIGHT ? min(b + 1, 31) : b;
+    uint32_t ov = up & ((hi == 31 ? 0xffffffffu : ((2u << hi) - 1)) & ~((1u << lo) - 1));
+    const uint32_t sup = starts[r - 1];
+    while (ov) {
+      const int p = __ffs(ov) - 1;
+      const int sa = run_start_at(sup, p);
+      sunion(lab, r * kTileW + c, (r - 1) * kTileW + sa);
+      const int ea = sa + run_len(up, sa) - 1;  // skip the rest of that run
+      ov &= ea >= 31 ? 0u : ~((2u << ea) - 1);
     }
   }
   __syncthreads();
 
-  // 3. flatten; number the local roots
+  // 4. flatten; number the local roots (root = smallest local index, the
+  //    component's raster-first pixel)
   int root[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) root[k] = fg[k] ? sfind(lab, r * kTileW + c0 + k) : -1;
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr;
+    root[rr] = ((starts[r] >> c) & 1u) ? sfind(lab, r * kTileW + c) : -1;
+  }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int i = r * kTileW + c0 + k;
-    if (fg[k]) lab[i] = root[k];
-    if (fg[k] && root[k] == i) {
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr, i = r * kTileW + c;
+    if (root[rr] < 0) continue;
+    lab[i] = root[rr];
+    if (root[rr] == i) {
       const int id = atomicAdd(&n_comp, 1);
       cid[i] = id;
       st_area[id] = 0;
@@ -180,32 +202,37 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   __syncthreads();
   if (threadIdx.x == 0 && n_comp > 0) slot_base_id = atomicAdd(&a.nslots[s], n_comp);
 
-  // 4. tile-component statistics (integer, order-free)
+  // 5. tile-component statistics per run (integer, order-free)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (!fg[k]) continue;
-    const int gx = gx0 + k;
-    const int id = cid[root[k]];
-    atomicAdd(&st_area[id], 1);
+  for (int rr = 0; rr < 4; ++rr) {
+    if (root[rr] < 0) continue;
+    const int r = w + 8 * rr, gy = ty0 + r;
+    const int len = run_len(rowm[r], c);
+    const int id = cid[root[rr]];
+    atomicAdd(&st_area[id], len);
     atomicMin(&st_x0[id], gx);
     atomicMin(&st_y0[id], gy);
-    atomicMax(&st_x1[id], gx);
+    atomicMax(&st_x1[id], gx + len - 1);
     atomicMax(&st_y1[id], gy);
-    atomicAdd(&st_sx[id], gx);
-    atomicAdd(&st_sy[id], gy);
+    atomicAdd(&st_sx[id], len * gx + len * (len - 1) / 2);
+    atomicAdd(&st_sy[id], len * gy);
   }
   __syncthreads();
   const int base = slot_base_id;
 
-  // 5. slot id per foreground pixel; slot records per tile component
+  // 6. slot id per foreground pixel (its run start's root); slot records
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (fg[k]) labg[static_cast<int64_t>(gy) * a.w + gx0 + k] = base + cid[root[k]];
+  for (int rr = 0; rr < 4; ++rr) {
+    if (!((mine >> rr) & 1u)) continue;
+    const int r = w + 8 * rr, gy = ty0 + r;
+    const int sc = run_start_at(starts[r], c);
+    labg[static_cast<int64_t>(gy) * a.w + gx] = base + cid[lab[r * kTileW + sc]];
+  }
   SlotTable t = slot_base(a, s);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int i = r * kTileW + c0 + k;
-    if (!fg[k] || root[k] != i) continue;
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = w + 8 * rr, i = r * kTileW + c;
+    if (root[rr] != i) continue;
     const int id = cid[i];
     const int slot = base + id;
     t.parent[slot] = slot;
@@ -216,7 +243,7 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
     t.y1[slot] = st_y1[id];
     t.sx[slot] = static_cast<unsigned long long>(st_sx[id]);
     t.sy[slot] = static_cast<unsigned long long>(st_sy[id]);
-    t.minpix[slot] = gy * a.w + gx0 + k;
+    t.minpix[slot] = (ty0 + r) * a.w + gx;
   }
 }
 
