@@ -1110,7 +1110,7 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
   // split mode: this CTA alone, with its 1/G share of the cluster scratch
   sm.grp = Grp::single();
   TrackScratch mine = scr;
-  mine.vals = scr.vals + static_cast<int64_t>(rank) * ((2 * d.maxN + kValsSlack) / G);
+  mine.vals = scr.vals + static_cast<int64_t>(rank) * (((2 * d.maxN + kValsSlack) / G) & ~31LL);  // 256-byte aligned
   mine.bins = scr.bins + static_cast<int64_t>(rank) * (((d.maxN + kBinsSlack) / G) & ~15LL);  // 16-byte aligned
   for (;;) {
     if (threadIdx.x == 0) {
