@@ -304,6 +304,9 @@ def ours_main(args, rank, world, local_rank):
     clk = clocks.stop()
 
     # ---- per-stage kernel times (second pass of K steps, events per stage)
+    #      and the tracker's window pixels (its algorithmic frame reads)
+    from paper_1310_3322_b200 import api
+    api.debug_stats(reset=True)
     st.profile(True)
     for _ in range(K):
         st.step_device(ptrs[t], stream.cuda_stream)
@@ -312,6 +315,7 @@ def ours_main(args, rank, world, local_rank):
     stage_ms, prof_steps = st.profile_read()
     st.profile(False)
     stage_ms = stage_ms / max(1, prof_steps)
+    track_px = api.debug_stats(reset=True).get("meanshift_window_px", 0) / max(1, prof_steps)
 
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H timed
     e2e = None
@@ -336,18 +340,32 @@ def ours_main(args, rank, world, local_rank):
 
     value = aggregate_fps(S, world, K, ms / 1e3)
     peak, peak_kind = measured_peaks()
-    motion_ms = stage_ms[0]
-    achieved = MOTION_BYTES_PER_PX * S * PX / (motion_ms / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "motion_dram_bytes.json")
-    if os.path.exists(tp):
+
+    def dram_traffic(name):  # ncu dram bytes per launch, when captured for this stream count
+        tp = os.path.join(ROOT, "profiles", name)
         try:
             with open(tp) as f:
                 d = json.load(f)
-            if d.get("streams") == S:
-                traffic = d["dram_bytes_per_launch"]
+            return d["dram_bytes_per_launch"] if d.get("streams") == S else None
         except Exception:
-            traffic = None
+            return None
+
+    motion_ms = stage_ms[0]
+    achieved = MOTION_BYTES_PER_PX * S * PX / (motion_ms / 1e3) / 1e9
+    roofline_motion = {"bound": "hbm", "kernel": "motion_mean_kernel", "achieved": achieved, "peak": peak,
+                       "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                       "traffic": dram_traffic("motion_dram_bytes.json"),
+                       "bytes_per_launch": MOTION_BYTES_PER_PX * S * PX}
+    # the dominant kernel: track_meanshift_kernel.  SURVEY §8(d): tracking's
+    # algorithmic bytes are its frame reads, window px x iterations x channels
+    ms_ms = stage_ms[2]
+    ms_bytes = track_px * 1
+    ms_achieved = ms_bytes / (ms_ms / 1e3) / 1e9 if ms_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": "track_meanshift_kernel", "achieved": ms_achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": ms_achieved / peak,
+                "traffic": dram_traffic("meanshift_dram_bytes.json"), "bytes_per_launch": ms_bytes,
+                "note": "exact-order fp64 sums (sequential-sum reproduction) make this kernel latency/"
+                        "barrier bound, not bandwidth bound; see DESIGN.md"}
     path_gbs = PATH_BYTES_PER_PX * S * PX / (ms / K / 1e3) / 1e9
     line = {
         "metric": "frames/sec (1080p, device-timed) motion+segment+track", "value": value, "unit": "frames/s",
@@ -358,12 +376,12 @@ def ours_main(args, rank, world, local_rank):
                    "connectivity": 8, "min_area": 4, "k_clusters": 16,
                    "parallelism": f"streams sharded over {world} GPU(s), no collective",
                    "l2": f"inputs larger than L2 ({S * 4 * PX / 1e6:.0f} MB of ring traffic per step)",
-                   "stage_ms_per_step": {"motion": stage_ms[0], "ccl_stats": stage_ms[1], "tracking": stage_ms[2]},
+                   "stage_ms_per_step": {"motion": stage_ms[0], "ccl_stats": stage_ms[1],
+                                         "track_meanshift": stage_ms[2], "track_gate_spawn": stage_ms[3]},
+                   "track_window_px_per_step": track_px,
                    "stage_timing": "separate pass of K steps with CUDA events between stages",
                    "path_hbm_frac": path_gbs / peak},
-        "roofline": {"bound": "hbm", "kernel": "motion_mean_kernel", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "bytes_per_launch": MOTION_BYTES_PER_PX * S * PX},
+        "roofline": roofline, "roofline_motion": roofline_motion,
         "gpu_launches": launches, "clocks": clk,
     }
     if e2e:

@@ -184,8 +184,9 @@ int trb_streams_num_tracks(trb_streams* s, int stream, int* n);
 /* Kernel launches issued by the last step (for the bench's gpu_launches). */
 int trb_streams_last_step_launches(const trb_streams* s, int* n);
 /* Per-stage device time (CUDA events on the launch stream around the
- * motion, CCL+statistics and tracking stages), summed over the profiled
- * steps: ms_out[3].  Profiling synchronises after every step. */
+ * motion, CCL+statistics, tracker schedule+mean-shift and tracker
+ * gate+spawn stages), summed over the profiled steps: ms_out[4].
+ * Profiling synchronises after every step. */
 int trb_streams_profile(trb_streams* s, int enable);
 int trb_streams_profile_read(const trb_streams* s, double* ms_out, int* steps);
 /* Device pointers of the per-stream output planes (for device consumers). */

@@ -425,8 +425,8 @@ class Streams:
         _check(lib().trb_streams_profile(self._h, int(enable)))
 
     def profile_read(self):
-        """-> (ms per stage [motion, ccl, tracking] summed, steps)"""
-        ms = np.zeros(3)
+        """-> (ms per stage [motion, ccl, meanshift, gate+spawn] summed, steps)"""
+        ms = np.zeros(4)
         n = C.c_int(0)
         _check(lib().trb_streams_profile_read(self._h, _ptr(ms), C.byref(n)))
         return ms, n.value
@@ -453,7 +453,7 @@ def synth_raster(out_device_ptr: int, width: int, height: int, channels: int, ba
 
 STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints", "osum_elements",
               "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced",
-              "uniform_chunks_L1", "uniform_chunks_L3", "chunks_L1", "chunks_L3", "", "",
+              "", "meanshift_window_px", "", "", "", "",
               "bad_scan_merge", "bad_phaseB_merge", "bad_bp_overflow", "bad_cross_cta", "bad_fold_carry",
               "bad_fold_merge", "bad_verify_start", "bad_verify_end", "bad_final_start", "bad_final_end",
               "many_bp_centroid", "many_bp_total", "many_bp_bin", "max_bp")

@@ -236,10 +236,13 @@ void Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st) {
   if (emitted) ccl_->run(mask_.as<uint8_t>(), st, &launches);
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[2], st));
   if (emitted && tracker_)
-    tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches);
-  if (profiling_) {
+    tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches,
+                      profiling_ ? prof_ev_[3] : nullptr);
+  else if (profiling_)
     TRB_CUDA(cudaEventRecord(prof_ev_[3], st));
-    TRB_CUDA(cudaEventSynchronize(prof_ev_[3]));
+  if (profiling_) {
+    TRB_CUDA(cudaEventRecord(prof_ev_[4], st));
+    TRB_CUDA(cudaEventSynchronize(prof_ev_[4]));
     for (int i = 0; i < kStages; ++i) {
       float ms = 0.f;
       TRB_CUDA(cudaEventElapsedTime(&ms, prof_ev_[i], prof_ev_[i + 1]));

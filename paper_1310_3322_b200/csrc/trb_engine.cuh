@@ -128,7 +128,7 @@ class Streams {
   CclState& ccl() { return *ccl_; }
   TrackerState* tracker() { return tracker_.get(); }
   // per-stage device time (motion, ccl, tracking) accumulated over steps
-  static constexpr int kStages = 3;
+  static constexpr int kStages = 4;  // motion, ccl+stats, track schedule+meanshift, gate+spawn
   void set_profiling(bool on);
   const double* profile_ms() const { return prof_ms_; }
   int profile_steps() const { return prof_steps_; }

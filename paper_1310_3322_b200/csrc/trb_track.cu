@@ -85,7 +85,8 @@ namespace trb {
 
 // Device-side diagnostics: [0..4] ordered_sums stats (see trb_osum.cuh),
 // [5] mean-shift iterations, [6] spawns, [7] Lloyd iterations, [8] farthest
-// point passes, [9] tracks advanced.
+// point passes, [9] tracks advanced, [11] window pixels of the mean-shift
+// iterations (the tracker's algorithmic frame reads, one byte per pixel).
 // [16..25] ordered_sums failure reasons (bit index of the `bad` mask).
 __device__ unsigned long long g_trb_stats[32];
 // Optional per-iteration timing log: {window pixels, cycles} pairs.
@@ -542,7 +543,14 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
   if (status != TRB_TRACK_ACTIVE) return;
   if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
   for (int it = 0; it < max_iters; ++it) {
-    if (threadIdx.x == 0) atomicAdd(&g_trb_stats[5], 1ull), sm.iscal[10] = it + 1;
+    if (threadIdx.x == 0) {
+      sm.iscal[10] = it + 1;
+      if (sm.grp.rank_ == 0) {
+        const Win rw = clip_window(fw, fh, cx, cy, w, h);
+        atomicAdd(&g_trb_stats[5], 1ull);
+        atomicAdd(&g_trb_stats[11], static_cast<unsigned long long>(rw.empty() ? 0 : (rw.x1 - rw.x0) * (rw.y1 - rw.y0)));
+      }
+    }
     TRB_PROGRESS(blockIdx.x, 1, -1, it, 1);
     const long long t_it0 = clock64();
     const bool ok = window_histogram(frame, fw, fh, ch, cx, cy, w, h, K, 1, use_lut, sm, scr, sm.p);
@@ -1543,7 +1551,7 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
 TrackerState::~TrackerState() = default;
 
 void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int ch, const trb_blob* blobs,
-                           int64_t blob_stride, const int32_t* nblobs, cudaStream_t st, int* launches) {
+                           int64_t blob_stride, const int32_t* nblobs, cudaStream_t st, int* launches, cudaEvent_t after_meanshift) {
   if (matched_cap_ < blob_stride) {
     matched_.alloc(static_cast<size_t>(blob_stride) * S_);
     matched_cap_ = blob_stride;
@@ -1578,6 +1586,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   track_schedule_kernel<<<1, 1024, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_schedule_kernel");
   launch_cluster(track_meanshift_kernel, grid_, G, smem, st, d_);
+  if (after_meanshift) TRB_CUDA(cudaEventRecord(after_meanshift, st));
   track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
   launch_cluster(track_spawn_kernel, grid_, G, smem, st, d_);

@@ -75,7 +75,8 @@ for k in range(args.steps):
     ms, steps = st.profile_read()
     st.profile(True)
     d = api.debug_stats(reset=True)
-    print(f"step {k}: motion {ms[0]:.3f} ms  ccl {ms[1]:.3f} ms  track {ms[2]:.3f} ms  {d}", flush=True)
+    print(f"step {k}: motion {ms[0]:.3f} ms  ccl {ms[1]:.3f} ms  meanshift {ms[2]:.3f} ms  gate+spawn {ms[3]:.3f} ms  {d}",
+          flush=True)
 st.profile(False)
 for s in range(min(S, 4)):
     b = st.blobs(s)
