@@ -51,6 +51,7 @@
 #define TRB_OSUM_WALK_END()
 #define TRB_OSUM_COUNT(v)
 #define TRB_OSUM_WALK_FIRST(cond, dep)
+#define TRB_OSUM_ELEM_TRACE(k, dep)
 #endif
 #ifndef TRB_OSUM_MARK
 #define TRB_OSUM_MARK(stage) ((void)0)
@@ -217,6 +218,46 @@ __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
   r.e = __shfl_up_sync(0xffffffffu, p.e, o);
   r.tie = __shfl_up_sync(0xffffffffu, p.tie, o);
   return r;
+}
+
+// Exact serial fallback (one thread): the sums in element order with real
+// IEEE adds.  Out of line — it is cold, and keeping it out of the hot
+// function keeps the per-iteration instruction footprint small.
+template <int L, bool SEG, class Src>
+__device__ __noinline__ void osum_serial(int N, int nseg, int C, int GT, const Src& src, OsumShared& s) {
+  double S[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) S[l] = 0.0;
+  int cs = -1;
+  for (int g = 0; g * C < N; ++g) {  // chunk by chunk, in order
+    const int a0 = g * C, a1 = min(N, a0 + C);
+    auto cur = src.begin(a0, g, C, GT);
+    for (int jb = a0; jb < a1; jb += Src::kUnroll)
+#pragma unroll
+      for (int k = 0; k < Src::kUnroll; ++k) {
+        if (jb + k >= a1) break;
+        bool start, has;
+        int seg;
+        double v[L];
+        cur.next(k, start, seg, has, v);
+        if (SEG && start) {
+          if (cs >= 0) s.result[cs] = S[0];
+          cs = seg;
+          S[0] = 0.0;
+        }
+        if (!has) continue;
+#pragma unroll
+        for (int l = 0; l < L; ++l) S[l] = xadd(S[l], v[l]);
+      }
+  }
+  if (SEG) {
+    for (int k = 0; k < nseg; ++k)
+      if (s.segpos[k] < 0) s.result[k] = 0.0;
+    if (cs >= 0) s.result[cs] = S[0];
+  } else {
+#pragma unroll
+    for (int l = 0; l < L; ++l) s.result[l] = S[l];
+  }
 }
 
 // One run of the engine.
@@ -410,6 +451,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       double v[L];
       cur.next(k, start, seg, has, v);
       TRB_OSUM_WALK_FIRST(j == j0, v[0]);
+      TRB_OSUM_ELEM_TRACE(j - j0, v[0]);
       if (SEG && start)
 #pragma unroll
         for (int l = 0; l < L; ++l) P[l] = 0.0;
@@ -672,41 +714,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
     }
     // exact serial fallback (all lanes / segments) if anything failed
     if (s.bad[1]) {
-      if (t == 0) {
-        double S[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) S[l] = 0.0;
-        int cs = -1;
-        for (int g = 0; g * C < N; ++g) {  // chunk by chunk, in order
-          const int a0 = g * C, a1 = min(N, a0 + C);
-          auto cur = src.begin(a0, g, C, GT);
-          for (int jb = a0; jb < a1; jb += Src::kUnroll)
-#pragma unroll
-            for (int k = 0; k < Src::kUnroll; ++k) {
-              if (jb + k >= a1) break;
-              bool start, has;
-              int seg;
-              double v[L];
-              cur.next(k, start, seg, has, v);
-              if (SEG && start) {
-                if (cs >= 0) s.result[cs] = S[0];
-                cs = seg;
-                S[0] = 0.0;
-              }
-              if (!has) continue;
-#pragma unroll
-              for (int l = 0; l < L; ++l) S[l] = xadd(S[l], v[l]);
-            }
-        }
-        if (SEG) {
-          for (int k = 0; k < nseg; ++k)
-            if (s.segpos[k] < 0) s.result[k] = 0.0;
-          if (cs >= 0) s.result[cs] = S[0];
-        } else {
-#pragma unroll
-          for (int l = 0; l < L; ++l) s.result[l] = S[l];
-        }
-      }
+      if (t == 0) osum_serial<L, SEG>(N, nseg, C, GT, src, s);
       __syncthreads();
     }
   }

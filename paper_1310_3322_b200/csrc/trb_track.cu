@@ -43,6 +43,10 @@ __shared__ int s_ph_bucket;
   const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0; \
   long long walk_t1_ = walk_t0_;                                 \
   unsigned long long nslow_ = 0, nbp_ = 0
+// per-element timestamps of global thread 0's walks (L == 3 only): g_phase[192 + k]
+#define TRB_OSUM_ELEM_TRACE(k, dep) \
+  if (::trb::g_phase_on && L == 3 && rank == 0 && threadIdx.x == 0 && (k) < 32) \
+    ::trb::g_phase[192 + (k)] = clock64() - walk_t0_ + ((dep) != (dep) ? 1 : 0)
 // time to the first element's data (cursor start-up); `dep` forces the wait
 #define TRB_OSUM_WALK_FIRST(cond, dep) \
   if ((cond) && ::trb::g_phase_on) walk_t1_ = clock64() + ((dep) != (dep) ? 1 : 0)
@@ -76,6 +80,7 @@ __shared__ int s_ph_bucket;
 #define TRB_OSUM_WALK_END() ((void)0)
 #define TRB_OSUM_COUNT(v) ((void)0)
 #define TRB_OSUM_WALK_FIRST(cond, dep) ((void)0)
+#define TRB_OSUM_ELEM_TRACE(k, dep) ((void)0)
 #define TRB_OSUM_MARK(stage) ((void)0)
 #endif
 
@@ -1094,42 +1099,44 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
   const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
   const int G = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int n_work = *d.work_n;
+  // One work loop (one inlined copy of the mean-shift code): cluster mode
+  // until the first split-class track, then split mode — this CTA alone,
+  // with its 1/G share of the cluster scratch.
   bool split = false;
-  for (;;) {  // cluster mode
-    if (rank == 0 && threadIdx.x == 0) {
-      const int q = atomicAdd(d.work_head, 1);
-      sm.iscal[8] = q < n_work ? q : -1;
+  TrackScratch cur_scr = scr;
+  for (;;) {
+    if (!split) {
+      if (rank == 0 && threadIdx.x == 0) {
+        const int q = atomicAdd(d.work_head, 1);
+        sm.iscal[8] = q < n_work ? q : -1;
+      }
+      cl.sync();
+      sm.iscal[11] = *cl.map_shared_rank(&sm.iscal[8], 0);
+      cl.sync();  // the leader may overwrite iscal[8] only after everyone read it
+    } else {
+      if (threadIdx.x == 0) {
+        const int q = atomicAdd(d.work_head, 1);
+        sm.iscal[11] = q < n_work ? q : -1;
+      }
+      __syncthreads();
     }
-    cl.sync();
-    const int q = *cl.map_shared_rank(&sm.iscal[8], 0);
-    cl.sync();  // the leader may overwrite iscal[8] only after everyone read it
+    const int q = sm.iscal[11];
+    __syncthreads();
     if (q < 0) break;
-    const int item = d.work[q];
-    const int s = item / d.T, i = item - s * d.T;
-    const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
-    const bool to_split = split_class(d, g);  // read before the leader updates iters
-    meanshift_item(d, q, sm, scr, rank == 0 && threadIdx.x == 0);
+    bool to_split = false;
+    if (!split) {
+      const int item = d.work[q];
+      const int s = item / d.T, i = item - s * d.T;
+      const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
+      to_split = split_class(d, g);  // read before the leader updates iters
+    }
+    meanshift_item(d, q, sm, cur_scr, (split || rank == 0) && threadIdx.x == 0);
     if (to_split) {  // every later item is split-class too
       split = true;
-      break;
+      sm.grp = Grp::single();
+      cur_scr.vals = scr.vals + static_cast<int64_t>(rank) * (((2 * d.maxN + kValsSlack) / G) & ~31LL);
+      cur_scr.bins = scr.bins + static_cast<int64_t>(rank) * (((d.maxN + kBinsSlack) / G) & ~15LL);
     }
-  }
-  if (!split) return;
-  // split mode: this CTA alone, with its 1/G share of the cluster scratch
-  sm.grp = Grp::single();
-  TrackScratch mine = scr;
-  mine.vals = scr.vals + static_cast<int64_t>(rank) * (((2 * d.maxN + kValsSlack) / G) & ~31LL);  // 256-byte aligned
-  mine.bins = scr.bins + static_cast<int64_t>(rank) * (((d.maxN + kBinsSlack) / G) & ~15LL);  // 16-byte aligned
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const int q = atomicAdd(d.work_head, 1);
-      sm.iscal[8] = q < n_work ? q : -1;
-    }
-    __syncthreads();
-    const int q = sm.iscal[8];
-    __syncthreads();
-    if (q < 0) break;
-    meanshift_item(d, q, sm, mine, threadIdx.x == 0);
   }
 }
 
