@@ -134,6 +134,16 @@ int trb_motion_frames_seen(const trb_motion* m, int* n);
 int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* cfg, int device, int32_t* labels_out,
               trb_blob* blobs_out, int blob_cap, int* n_blobs, int64_t* pixels_out, int64_t pixels_cap);
 
+/* ---- extract_blob_features (segmentation.hpp:266-291) ----
+ * Per blob: mean intensity (luma for RGB frames) and bbox aspect
+ * (width / height), as the reference fills Blob::mean_intensity / aspect.
+ * Host buffers; labels is the w*h label image, blobs its n_blobs records.
+ * TRB_INVALID_ARGUMENT "label image dimensions do not match frame" when the
+ * sizes differ (:270-271). */
+int trb_extract_blob_features(const int32_t* labels, int width, int height, const uint8_t* frame, int frame_width,
+                              int frame_height, int channels, const trb_blob* blobs, int n_blobs, int device,
+                              double* mean_intensity, double* aspect);
+
 /* ---- Tracker (tracking.hpp:170-241) ---- */
 typedef struct trb_tracker trb_tracker;
 int trb_tracker_create(const trb_tracker_config* cfg, int device, trb_tracker** out);
@@ -189,6 +199,11 @@ int trb_streams_last_step_launches(const trb_streams* s, int* n);
  * Profiling synchronises after every step. */
 int trb_streams_profile(trb_streams* s, int enable);
 int trb_streams_profile_read(const trb_streams* s, double* ms_out, int* steps);
+/* extract_blob_features for stream `stream`'s last step, from its labels and
+ * blob table in HBM and `frame_dev` (device pointer to that step's frame):
+ * *n = blob count; mean_intensity / aspect (host, cap entries). */
+int trb_streams_blob_features(trb_streams* s, int stream, const uint8_t* frame_dev, double* mean_intensity,
+                              double* aspect, int cap, int* n);
 /* Device pointers of the per-stream output planes (for device consumers). */
 int trb_streams_device_planes(trb_streams* s, int stream, uint8_t** mask, int32_t** labels);
 

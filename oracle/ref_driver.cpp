@@ -157,6 +157,31 @@ int ref_label(const uint8_t* mask, int w, int h, const trb_seg_config* c, int se
   }
 }
 
+// ---- extract_blob_features (segmentation.hpp:268-291) ----
+// The labelling is rebuilt from the label image + blob records (the
+// function reads only labels, width/height and the blob table).
+int ref_blob_features(const int32_t* labels, int w, int h, const uint8_t* frame, int fw, int fh, int ch,
+                      const trb_blob* blobs, int n, double* mean, double* aspect) {
+  try {
+    Labeling lab;
+    lab.width = w;
+    lab.height = h;
+    lab.labels.assign(labels, labels + static_cast<std::size_t>(w) * h);
+    lab.blobs.resize(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      Blob& b = lab.blobs[static_cast<std::size_t>(i)];
+      b.label = blobs[i].label, b.area = blobs[i].area;
+      b.x_min = blobs[i].x_min, b.y_min = blobs[i].y_min, b.x_max = blobs[i].x_max, b.y_max = blobs[i].y_max;
+      b.cx = blobs[i].cx, b.cy = blobs[i].cy;
+    }
+    const auto out = extract_blob_features(lab, make_frame(frame, fw, fh, ch));
+    for (int i = 0; i < n; ++i) mean[i] = out[i].mean_intensity, aspect[i] = out[i].aspect;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ---- quantizer / histogram / meanshift ----
 int ref_quantize_colors(const double* px, int64_t n, int k, int iters, uint64_t seed, double* centers) {
   try {

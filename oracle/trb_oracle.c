@@ -184,6 +184,33 @@ void orc_grayscale(const uint8_t* rgb, int64_t n_px, uint8_t* out) {
     out[i] = (uint8_t)((77 * rgb[3 * i] + 150 * rgb[3 * i + 1] + 29 * rgb[3 * i + 2] + 128) >> 8);
 }
 
+/* extract_blob_features, segmentation.hpp:268-291: raster-order double
+ * sums of the pixel values per label (luma for RGB, frame.hpp:91-93), then
+ * sum / area and (x_max - x_min + 1) / (y_max - y_min + 1). */
+int orc_blob_features(const int32_t* labels, int w, int h, const uint8_t* frame, int fw, int fh, int ch,
+                      const trb_blob* blobs, int n, double* mean, double* aspect) {
+  if (w != fw || h != fh) return -1;
+  double* sum = (double*)calloc(n > 0 ? (size_t)n : 1, sizeof(double));
+  for (int64_t p = 0; p < (int64_t)w * h; ++p) {
+    const int l = labels[p];
+    if (l == 0) continue;
+    double v;
+    if (ch == 1) {
+      v = frame[p];
+    } else {
+      const uint8_t* q = frame + 3 * p;
+      v = (double)(uint8_t)((77 * q[0] + 150 * q[1] + 29 * q[2] + 128) >> 8);
+    }
+    sum[l - 1] += v;
+  }
+  for (int i = 0; i < n; ++i) {
+    mean[i] = sum[i] / blobs[i].area;
+    aspect[i] = (double)(blobs[i].x_max - blobs[i].x_min + 1) / (double)(blobs[i].y_max - blobs[i].y_min + 1);
+  }
+  free(sum);
+  return 0;
+}
+
 /* 3x3 morphology — new stage, no reference. */
 static void morph_pass(const uint8_t* in, int w, int h, int dilate, uint8_t* out) {
   for (int y = 0; y < h; ++y)

@@ -52,6 +52,14 @@ void orc_morph(const uint8_t* in, int width, int height, int op, uint8_t* out);
 int orc_label(const uint8_t* mask, int width, int height, int connectivity, int min_area, int32_t* labels,
               trb_blob* blobs, int cap, int64_t* pixels);
 
+/* extract_blob_features (segmentation.hpp:266-291): per blob the mean
+ * intensity (luma for RGB frames; the double sum of byte values is exact)
+ * and the bbox aspect (width / height).  Returns -1 when the label image
+ * and the frame sizes differ (InvalidArgument). */
+int orc_blob_features(const int32_t* labels, int width, int height, const uint8_t* frame, int frame_width,
+                      int frame_height, int channels, const trb_blob* blobs, int n_blobs, double* mean_intensity,
+                      double* aspect);
+
 /* ---- quantizer / tracker (quantize.hpp, tracking.hpp) ---- */
 void orc_quantize_colors(const double* pixels /* n*3 */, int64_t n, int k, int iters, uint64_t seed,
                          double* centers /* k*3 out */);

@@ -6,12 +6,14 @@ C ABI (include/trb.h, libtrb.so), mirrored here with the reference's names.
 """
 from .api import (ACTIVE, EIGHT, FOUR, LOST, MEAN, MODE, CapacityError, ConfigError, CudaError, InvalidArgument,
                   IoError, Labeling, MotionConfig, MotionDetector, SegmentationConfig, Streams, TeamrecError, Tracker,
-                  TrackerConfig, build, device_count, histogram, label_blocked, label_sequential, lib,
+                  TrackerConfig, build, device_count, extract_blob_features, histogram, label_blocked,
+                  label_sequential, lib,
                   meanshift_step, quantize_colors, synth_raster)
 
 __all__ = [
     "ACTIVE", "EIGHT", "FOUR", "LOST", "MEAN", "MODE", "CapacityError", "ConfigError", "CudaError",
     "InvalidArgument", "IoError", "Labeling", "MotionConfig", "MotionDetector", "SegmentationConfig", "Streams",
-    "TeamrecError", "Tracker", "TrackerConfig", "build", "device_count", "histogram", "label_blocked",
+    "TeamrecError", "Tracker", "TrackerConfig", "build", "device_count", "extract_blob_features", "histogram",
+    "label_blocked",
     "label_sequential", "lib", "meanshift_step", "quantize_colors", "synth_raster",
 ]

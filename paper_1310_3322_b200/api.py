@@ -120,6 +120,8 @@ def _declare(L):
         "trb_streams_step_device": [vp, vp, vp],
         "trb_streams_step_host": [vp, vp, vp, vp],
         "trb_streams_step_host_async": [vp, vp, vp, vp],
+        "trb_extract_blob_features": [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp],
+        "trb_streams_blob_features": [vp, i32, vp, vp, vp, i32, C.POINTER(C.c_int)],
         "trb_streams_synchronize": [vp],
         "trb_streams_frames_seen": [vp, C.POINTER(C.c_int)],
         "trb_streams_has_output": [vp, C.POINTER(C.c_int)],
@@ -321,6 +323,20 @@ def meanshift_step(frame: np.ndarray, width: int, height: int, channels: int, cx
     return x.value, y.value, st.value
 
 
+def extract_blob_features(labels: np.ndarray, width: int, height: int, frame: np.ndarray, frame_width: int,
+                          frame_height: int, channels: int, blobs, device: int = 0):
+    """extract_blob_features (segmentation.hpp:268-291) -> (mean_intensity,
+    aspect) arrays, one entry per blob record."""
+    lab = np.ascontiguousarray(labels, dtype=np.int32).reshape(-1)
+    f = np.ascontiguousarray(frame, dtype=np.uint8).reshape(-1)
+    b = np.ascontiguousarray(blobs)
+    n = len(b)
+    mean, aspect = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    _check(lib().trb_extract_blob_features(_ptr(lab), width, height, _ptr(f), frame_width, frame_height, channels,
+                                           _ptr(b) if n else None, n, device, _ptr(mean), _ptr(aspect)))
+    return mean[:n], aspect[:n]
+
+
 def histogram(frame: np.ndarray, width: int, height: int, channels: int, cx: float, cy: float, w: int, h: int,
               centers: np.ndarray, epanechnikov: bool = True, device: int = 0) -> np.ndarray:
     """histogram (tracking.hpp:106-112)."""
@@ -430,6 +446,16 @@ class Streams:
         n = C.c_int(0)
         _check(lib().trb_streams_profile_read(self._h, _ptr(ms), C.byref(n)))
         return ms, n.value
+
+    def blob_features(self, s: int, frame_device_ptr: int):
+        """extract_blob_features of stream s's last step (frame_device_ptr:
+        that step's frame in HBM) -> (mean_intensity, aspect)."""
+        cap = self.width * self.height // 2 + 2
+        mean, aspect = np.zeros(cap), np.zeros(cap)
+        n = C.c_int(0)
+        _check(lib().trb_streams_blob_features(self._h, s, C.c_void_p(frame_device_ptr), _ptr(mean), _ptr(aspect),
+                                               cap, C.byref(n)))
+        return mean[:n.value], aspect[:n.value]
 
     def device_planes(self, s: int):
         m, l_ = C.c_void_p(), C.c_void_p()

@@ -307,6 +307,93 @@ int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* 
   });
 }
 
+// ------------------------------------------------- blob appearance features
+namespace {
+// extract_blob_features (segmentation.hpp:268-291).  The reference's double
+// sums of byte values are exact (< 2^53), so per-label integer sums with
+// atomics give the same doubles.  One thread = 16 consecutive pixels; runs
+// of one label are flushed with one atomic.
+__global__ void blob_feature_sum_kernel(const int32_t* labels, int64_t px, const uint8_t* frame, int ch, int n_blobs,
+                                        unsigned long long* sums) {
+  const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
+  if (p0 >= px) return;
+  const int64_t p1 = min(px, p0 + 16);
+  int cur = 0;
+  unsigned long long acc = 0;
+  for (int64_t p = p0; p < p1; ++p) {
+    const int l = labels[p];
+    if (l != cur) {
+      if (cur > 0 && cur <= n_blobs) atomicAdd(&sums[cur - 1], acc);
+      cur = l, acc = 0;
+    }
+    if (l == 0) continue;
+    unsigned v;
+    if (ch == 1) {
+      v = frame[p];
+    } else {
+      const uint8_t* q = frame + 3 * p;
+      v = (77u * q[0] + 150u * q[1] + 29u * q[2] + 128u) >> 8;  // luma, frame.hpp:91-93
+    }
+    acc += v;
+  }
+  if (cur > 0 && cur <= n_blobs) atomicAdd(&sums[cur - 1], acc);
+}
+
+__global__ void blob_feature_final_kernel(const trb_blob* blobs, int n, const unsigned long long* sums, double* mean,
+                                          double* aspect) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const trb_blob b = blobs[i];
+  mean[i] = __ddiv_rn(static_cast<double>(sums[i]), static_cast<double>(b.area));
+  aspect[i] = __ddiv_rn(static_cast<double>(b.x_max - b.x_min + 1), static_cast<double>(b.y_max - b.y_min + 1));
+}
+
+// device pointers in, device pointers out
+void device_blob_features(const int32_t* labels, int64_t px, const uint8_t* frame, int ch, const trb_blob* blobs,
+                          int n, double* mean, double* aspect, cudaStream_t st) {
+  if (n <= 0) return;
+  trb::DevBuf sums;
+  sums.alloc(sizeof(unsigned long long) * n);  // zeroed
+  blob_feature_sum_kernel<<<static_cast<unsigned>(trb::ceil_div64(trb::ceil_div64(px, 16), 256)), 256, 0, st>>>(
+      labels, px, frame, ch, n, sums.as<unsigned long long>());
+  TRB_LAUNCH_CHECK("blob_feature_sum_kernel");
+  blob_feature_final_kernel<<<static_cast<unsigned>(trb::ceil_div64(n, 256)), 256, 0, st>>>(
+      blobs, n, sums.as<unsigned long long>(), mean, aspect);
+  TRB_LAUNCH_CHECK("blob_feature_final_kernel");
+  TRB_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+int trb_extract_blob_features(const int32_t* labels, int width, int height, const uint8_t* frame, int frame_width,
+                              int frame_height, int channels, const trb_blob* blobs, int n_blobs, int device,
+                              double* mean_intensity, double* aspect) {
+  return guard([&] {
+    need(labels && frame && (blobs || n_blobs == 0) && (mean_intensity || n_blobs == 0) &&
+             (aspect || n_blobs == 0),
+         "null argument");
+    if (width != frame_width || height != frame_height)
+      throw Error(TRB_INVALID_ARGUMENT, "label image dimensions do not match frame");
+    need(channels == 1 || channels == 3, "frame channels must be 1 or 3");
+    need(width >= 1 && height >= 1 && n_blobs >= 0, "dimensions must be >= 1");
+    use_device(device);
+    if (n_blobs == 0) return;
+    const int64_t px = static_cast<int64_t>(width) * height;
+    trb::DevBuf dl, df, db, dm, da;
+    dl.alloc(sizeof(int32_t) * px, false);
+    df.alloc(static_cast<size_t>(px) * channels, false);
+    db.alloc(sizeof(trb_blob) * n_blobs, false);
+    dm.alloc(sizeof(double) * n_blobs, false);
+    da.alloc(sizeof(double) * n_blobs, false);
+    TRB_CUDA(cudaMemcpy(dl.p, labels, sizeof(int32_t) * px, cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaMemcpy(df.p, frame, static_cast<size_t>(px) * channels, cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaMemcpy(db.p, blobs, sizeof(trb_blob) * n_blobs, cudaMemcpyHostToDevice));
+    device_blob_features(dl.as<int32_t>(), px, df.as<uint8_t>(), channels, db.as<trb_blob>(), n_blobs,
+                         dm.as<double>(), da.as<double>(), 0);
+    TRB_CUDA(cudaMemcpy(mean_intensity, dm.p, sizeof(double) * n_blobs, cudaMemcpyDeviceToHost));
+    TRB_CUDA(cudaMemcpy(aspect, da.p, sizeof(double) * n_blobs, cudaMemcpyDeviceToHost));
+  });
+}
+
 // ------------------------------------------------------------- tracker
 int trb_tracker_create(const trb_tracker_config* cfg, int device, trb_tracker** out) {
   return guard([&] {
@@ -580,6 +667,32 @@ int trb_streams_profile_read(const trb_streams* s, double* ms_out, int* steps) {
     need(s && ms_out && steps, "null argument");
     for (int i = 0; i < trb::Streams::kStages; ++i) ms_out[i] = s->s->profile_ms()[i];
     *steps = s->s->profile_steps();
+  });
+}
+
+int trb_streams_blob_features(trb_streams* s, int stream, const uint8_t* frame_dev, double* mean_intensity,
+                              double* aspect, int cap, int* n) {
+  return guard([&] {
+    need(s && frame_dev && n, "null argument");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    TRB_CUDA(cudaSetDevice(s->device));
+    trb::Streams& st = *s->s;
+    TRB_CUDA(cudaStreamSynchronize(st.stream()));
+    int32_t nb = 0;
+    if (st.has_output())
+      TRB_CUDA(cudaMemcpy(&nb, st.ccl().nblobs() + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    *n = nb;
+    if (nb == 0) return;
+    if (nb > cap) throw Error(TRB_CAPACITY, "feature buffer too small");
+    need(mean_intensity && aspect, "null argument");
+    trb::DevBuf dm, da;
+    dm.alloc(sizeof(double) * nb, false);
+    da.alloc(sizeof(double) * nb, false);
+    device_blob_features(st.ccl().labels() + st.px() * stream, st.px(), frame_dev, st.ch(),
+                         st.ccl().blobs() + st.ccl().blob_cap() * stream, nb, dm.as<double>(), da.as<double>(),
+                         st.stream());
+    TRB_CUDA(cudaMemcpy(mean_intensity, dm.p, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    TRB_CUDA(cudaMemcpy(aspect, da.p, sizeof(double) * nb, cudaMemcpyDeviceToHost));
   });
 }
 

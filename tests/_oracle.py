@@ -88,6 +88,8 @@ def orc_lib():
                                        C.c_uint64]
         L.orc_synth_destroy.argtypes = [vp]
         L.orc_synth_next.argtypes = [vp, C.c_void_p, C.c_void_p]
+        L.orc_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_libm_hypot.restype = C.c_double
         L.orc_libm_hypot.argtypes = [C.c_double, C.c_double]
         _orc = L
@@ -113,6 +115,8 @@ def ref_lib():
         L.ref_label.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(SEG_CFG), C.c_int, C.c_int, C.c_void_p,
                                 C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_void_p]
         L.ref_quantize_colors.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+        L.ref_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_histogram.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                     C.c_void_p, C.c_int, C.c_int, C.c_void_p]
         L.ref_meanshift_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
@@ -198,6 +202,23 @@ def cpu_label(mask: np.ndarray, w: int, h: int, conn: int = 1, min_area: int = 4
             raise RuntimeError(ref_lib().ref_last_error().decode())
         n = nn.value
     return labels, blobs_to_array(blobs, n), (pixels[:int(np.count_nonzero(labels))] if want_pixels else None)
+
+
+def cpu_blob_features(labels, w, h, frame, fw, fh, ch, blobs, impl="orc"):
+    """extract_blob_features -> (mean_intensity[n], aspect[n]); raises
+    ValueError on the reference's InvalidArgument (size mismatch)."""
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    b = np.ascontiguousarray(blobs)
+    n = len(b)
+    mean, aspect = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    L = orc_lib() if impl == "orc" else ref_lib()
+    fn = L.orc_blob_features if impl == "orc" else L.ref_blob_features
+    rc = fn(lab.ctypes.data, w, h, f.ctypes.data, fw, fh, ch, b.ctypes.data if n else None, n, mean.ctypes.data,
+            aspect.ctypes.data)
+    if rc:
+        raise ValueError(L.ref_last_error().decode() if impl != "orc" else "label image dimensions do not match frame")
+    return mean[:n], aspect[:n]
 
 
 class CpuTracker:

@@ -85,10 +85,44 @@ def tracker_case(clip: Clip, tcfg: TRACKER_CFG, min_area=4):
     return dict(log=trk.log(), frames_sha=np.array([sha(f) for f in frames]))
 
 
+def blob_features_case(trials: int = 40):
+    """extract_blob_features (segmentation.hpp:268-291) on random masks and
+    frames through the reference: ragged sizes, 4/8-connectivity, gray and
+    RGB.  Inputs and outputs flattened with offsets."""
+    rng = np.random.default_rng(11)
+    d = {k: [] for k in ("dims", "masks", "frames", "labels", "blobs", "mean", "aspect")}
+    for trial in range(trials):
+        w, h = int(rng.integers(1, 49)), int(rng.integers(1, 49))
+        ch = 1 if trial % 3 else 3
+        conn = int(trial % 2)
+        min_area = int(rng.integers(1, 5))
+        m = (rng.random(w * h) < rng.uniform(0.1, 0.8)).astype(np.uint8)
+        f = rng.integers(0, 256, size=w * h * ch, dtype=np.uint8)
+        lab, blobs, _ = O.cpu_label(m, w, h, conn, min_area, "ref", n_blocks=1)
+        mean, aspect = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "ref")
+        d["dims"].append((w, h, ch, conn, min_area, len(blobs)))
+        d["masks"].append(m)
+        d["frames"].append(f)
+        d["labels"].append(lab)
+        d["blobs"].append(np.frombuffer(blobs.tobytes(), np.uint8))
+        d["mean"].append(mean)
+        d["aspect"].append(aspect)
+    out = {"dims": np.array(d["dims"], np.int32)}
+    for k in ("masks", "frames", "labels", "blobs", "mean", "aspect"):
+        out[k] = np.concatenate(d[k]) if d[k] else np.zeros(0)
+    return out
+
+
 def main():
     if not O.ref_available():
         sys.exit("oracle/_ref/libteamrec_ref.so missing: run `make -C oracle` where /root/reference exists")
     out = {}
+    if "blob_features" in sys.argv[1:]:  # only the extract_blob_features fixture
+        out["blob_features"] = blob_features_case()
+        for name, d in out.items():
+            np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+            print(name, {k: getattr(v, "shape", None) for k, v in d.items()})
+        return
     out["c1_pipeline"] = pipeline_case(recipe("C1"), 160, MOTION_CFG())
     out["c2_pipeline"] = pipeline_case(recipe("C2"), 140, MOTION_CFG())
     out["harness_vision"] = pipeline_case(harness_vision_clip(), 29, MOTION_CFG(window=9))
@@ -110,6 +144,7 @@ def main():
         conns.append(conn)
     out["random_ccl"] = dict(masks=np.array(masks), label_sha=np.array(labels_sha), nblobs=np.array(nb),
                              conn=np.array(conns))
+    out["blob_features"] = blob_features_case()
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
         print(name, {k: getattr(v, "shape", None) for k, v in d.items()})

@@ -191,3 +191,52 @@ def test_ccl_full_size_recipe_masks(gpu, name):
         noise = rng.random(m.size) < 0.001
         m = (m ^ noise).astype(np.uint8)
         check_label(gpu, m, clip.width, clip.height, 1, 4)
+
+
+# ---------------------------------------------- extract_blob_features (§8(f) 2)
+def test_blob_features_golden(gpu):
+    """Device labels -> device extract_blob_features vs the reference's
+    values (tests/golden/blob_features.npz): ragged sizes, 4/8-conn, gray/RGB."""
+    g = np.load(os.path.join(GOLD, "blob_features.npz"))
+    om = oa = ol = 0
+    for w, h, ch, conn, min_area, nb in g["dims"]:
+        m, f = g["masks"][om:om + w * h], g["frames"][oa:oa + w * h * ch]
+        lab = gpu.label_blocked(m, w, h, SEG_CFG(1, conn, min_area))
+        assert lab.labels.tobytes() == g["labels"][om:om + w * h].tobytes()
+        mean, aspect = gpu.extract_blob_features(lab.labels, w, h, f, w, h, ch, lab.blobs)
+        assert mean.tobytes() == g["mean"][ol:ol + nb].tobytes()
+        assert aspect.tobytes() == g["aspect"][ol:ol + nb].tobytes()
+        om, oa, ol = om + w * h, oa + w * h * ch, ol + nb
+
+
+def test_blob_features_known_answers_and_errors(gpu):
+    from paper_1310_3322_b200.api import InvalidArgument
+    m = np.zeros(16, np.uint8)
+    f = np.zeros(48, np.uint8)
+    m[5] = 1
+    f[15] = 255  # pure red at (1, 1)
+    lab = gpu.label_blocked(m, 4, 4, SEG_CFG(1, 1, 1))
+    mean, aspect = gpu.extract_blob_features(lab.labels, 4, 4, f, 4, 4, 3, lab.blobs)
+    assert mean[0] == float((77 * 255 + 128) // 256) and aspect[0] == 1.0
+    empty = gpu.label_blocked(np.zeros(16, np.uint8), 4, 4, SEG_CFG(1, 1, 1))
+    assert len(gpu.extract_blob_features(empty.labels, 4, 4, np.zeros(16, np.uint8), 4, 4, 1, empty.blobs)[0]) == 0
+    with pytest.raises(InvalidArgument, match="label image dimensions do not match frame"):
+        gpu.extract_blob_features(lab.labels, 4, 4, np.zeros(20, np.uint8), 5, 4, 1, lab.blobs)
+
+
+def test_blob_features_full_frame_vs_oracle(gpu):
+    """A 1080p C3 mask with its frame: large blobs (long label runs, one
+    atomic per run) vs the oracle."""
+    clip = recipe("C3")
+    frames, _ = O.orc_frames(clip, 100)
+    mot = O.CpuMotion(MOTION_CFG(), clip.width, clip.height, "orc")
+    m = None
+    for t in range(92):
+        m = mot.push(frames[t])
+    lab = gpu.label_blocked(m, clip.width, clip.height, SEG_CFG())
+    mean, aspect = gpu.extract_blob_features(lab.labels, clip.width, clip.height, frames[91], clip.width,
+                                             clip.height, 1, lab.blobs)
+    om, oa = O.cpu_blob_features(lab.labels, clip.width, clip.height, frames[91], clip.width, clip.height, 1,
+                                 lab.blobs, "orc")
+    assert len(mean) > 5
+    assert mean.tobytes() == om.tobytes() and aspect.tobytes() == oa.tobytes()

@@ -98,3 +98,24 @@ def test_streams_pipelined_host_steps_match_golden(gpu, pinned):
         assert (emitted[:, s] == g["nblobs"]).all()
         assert st.log(s).tobytes() == g["log"].tobytes()
     assert (res[:window - 1] == 0).all()
+
+
+def test_streams_blob_features_vs_oracle(gpu):
+    """extract_blob_features on a stream's device labels / blobs and its
+    frame in HBM (trb_streams_blob_features) vs the oracle on the same step."""
+    import torch
+    clips = [recipe("C1"), recipe("C1")]
+    n = 100
+    frames = [O.orc_frames(c, n)[0] for c in clips]
+    dev = [torch.from_numpy(f).cuda() for f in frames]
+    c0 = clips[0]
+    st = gpu.Streams(2, c0.width, c0.height, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+    for t in range(n):
+        st.step_device([dev[s][t].data_ptr() for s in range(2)])
+    st.synchronize()
+    for s in range(2):
+        mean, aspect = st.blob_features(s, dev[s][n - 1].data_ptr())
+        labels, blobs = st.labels(s), st.blobs(s)
+        om, oa = O.cpu_blob_features(labels, c0.width, c0.height, frames[s][n - 1], c0.width, c0.height, 1, blobs)
+        assert len(mean) == len(blobs) > 0
+        assert mean.tobytes() == om.tobytes() and aspect.tobytes() == oa.tobytes()

@@ -208,3 +208,68 @@ def test_c1_live_vs_reference():
     b = pipeline_case(clip, 130, MOTION_CFG(), impl="ref")
     for k in a:
         assert np.array_equal(a[k], b[k]) if a[k].dtype != object else (a[k] == b[k]).all()
+
+
+# ---------------------------------------------- extract_blob_features (§8(f) 2)
+def _features_kat(impl):
+    # segmentation_test.cpp:129-148: a 3x3 square of value 120
+    m = np.zeros(16, np.uint8)
+    f = np.zeros(16, np.uint8)
+    for y in range(3):
+        for x in range(3):
+            m[y * 4 + x] = 1
+            f[y * 4 + x] = 120
+    lab, blobs, _ = O.cpu_label(m, 4, 4, 1, 4, "orc")
+    mean, aspect = O.cpu_blob_features(lab, 4, 4, f, 4, 4, 1, blobs, impl)
+    assert len(blobs) == 1 and blobs["area"][0] == 9 and mean[0] == 120.0 and aspect[0] == 1.0
+    # :150-160: a 4x1 run -> aspect 4
+    m = np.zeros(64, np.uint8)
+    m[3 * 8 + 2:3 * 8 + 6] = 1
+    lab, blobs, _ = O.cpu_label(m, 8, 8, 0, 1, "orc")
+    mean, aspect = O.cpu_blob_features(lab, 8, 8, np.full(64, 9, np.uint8), 8, 8, 1, blobs, impl)
+    assert aspect[0] == 4.0 and mean[0] == 9.0
+    # :162-171: colour frames contribute luma
+    m = np.zeros(16, np.uint8)
+    m[5] = 1
+    f = np.zeros(48, np.uint8)
+    f[15] = 255
+    lab, blobs, _ = O.cpu_label(m, 4, 4, 1, 1, "orc")
+    mean, _ = O.cpu_blob_features(lab, 4, 4, f, 4, 4, 3, blobs, impl)
+    assert mean[0] == float((77 * 255 + 128) // 256)
+    # :173-181: empty labelling, size mismatch
+    lab, blobs, _ = O.cpu_label(np.zeros(16, np.uint8), 4, 4, 1, 1, "orc")
+    assert len(O.cpu_blob_features(lab, 4, 4, np.zeros(16, np.uint8), 4, 4, 1, blobs, impl)[0]) == 0
+    with pytest.raises(ValueError):
+        O.cpu_blob_features(lab, 4, 4, np.zeros(20, np.uint8), 5, 4, 1, blobs, impl)
+
+
+def test_blob_features_known_answers():
+    _features_kat("orc")
+
+
+def test_blob_features_golden():
+    g = gold("blob_features")
+    om = oa = ol = ob = 0
+    for w, h, ch, conn, min_area, nb in g["dims"]:
+        m, f = g["masks"][om:om + w * h], g["frames"][oa:oa + w * h * ch]
+        lab, blobs, _ = O.cpu_label(m, w, h, conn, min_area, "orc")
+        assert lab.tobytes() == g["labels"][om:om + w * h].tobytes()
+        assert blobs.tobytes() == g["blobs"][ob:ob + 40 * nb].tobytes()
+        mean, aspect = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "orc")
+        assert mean.tobytes() == g["mean"][ol:ol + nb].tobytes()
+        assert aspect.tobytes() == g["aspect"][ol:ol + nb].tobytes()
+        om, oa, ol, ob = om + w * h, oa + w * h * ch, ol + nb, ob + 40 * nb
+
+
+@needs_ref
+def test_blob_features_vs_reference():
+    _features_kat("ref")
+    rng = np.random.default_rng(12)
+    for trial in range(30):
+        w, h, ch = int(rng.integers(1, 64)), int(rng.integers(1, 64)), 1 if trial % 2 else 3
+        m = (rng.random(w * h) < 0.5).astype(np.uint8)
+        f = rng.integers(0, 256, size=w * h * ch, dtype=np.uint8)
+        lab, blobs, _ = O.cpu_label(m, w, h, trial % 2, 1, "ref")
+        a = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "orc")
+        b = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "ref")
+        assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
