@@ -48,13 +48,15 @@ enum { TRB_TRACK_ACTIVE = 0, TRB_TRACK_LOST = 1 }; /* TrackStatus, tracking.hpp:
 /* 3x3 morphology is NOT in the reference; default OFF keeps parity. */
 enum { TRB_MORPH_NONE = 0, TRB_MORPH_ERODE = 1, TRB_MORPH_DILATE = 2, TRB_MORPH_OPEN = 3, TRB_MORPH_CLOSE = 4 };
 
-/* MotionConfig (motion.hpp:44-56).  warp must be 0 (identity). */
+/* MotionConfig (motion.hpp:44-56).  warp: 0 identity, 1 per-frame
+ * homography (stream_detect, motion.hpp:260-282): the batched handle then
+ * takes frames through trb_streams_step_device_warp. */
 typedef struct trb_motion_config {
   int32_t method;    /* TRB_BG_MEAN | TRB_BG_MODE, default mean */
   int32_t window;    /* default 91 */
   int32_t threshold; /* default 25 */
   int32_t bins;      /* default 32 */
-  int32_t warp;      /* 0 = identity */
+  int32_t warp;      /* 0 = identity, 1 = per-frame homography */
   int32_t morph;     /* extension: TRB_MORPH_*, default none */
 } trb_motion_config;
 
@@ -134,6 +136,12 @@ int trb_motion_frames_seen(const trb_motion* m, int* n);
 int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* cfg, int device, int32_t* labels_out,
               trb_blob* blobs_out, int blob_cap, int* n_blobs, int64_t* pixels_out, int64_t pixels_cap);
 
+/* ---- warp_frame (motion.hpp:81-119) ----
+ * Inverse-mapped bilinear resampling of one frame (host buffers) by the
+ * homography h (row-major 3x3); samples off the source plane read 0. */
+int trb_warp_frame(const uint8_t* frame, int width, int height, int channels, const double* homography, int device,
+                   uint8_t* out);
+
 /* ---- extract_blob_features (segmentation.hpp:266-291) ----
  * Per blob: mean intensity (luma for RGB frames) and bbox aspect
  * (width / height), as the reference fills Blob::mean_intensity / aspect.
@@ -170,6 +178,14 @@ int trb_streams_destroy(trb_streams* s);
 /* frames: host array of n_streams DEVICE pointers (w*h*channels bytes each).
  * cuda_stream: cudaStream_t to launch on (NULL = the handle's own). */
 int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* cuda_stream);
+/* step_device for MotionConfig::warp = homography: every frame is warped
+ * into the reference plane (warp_frame, motion.hpp:81-119) by its
+ * homography (homographies: host, n_streams * 9 doubles, row-major) before
+ * it enters the window (stream_detect, motion.hpp:279).  Errors are the
+ * reference's ("homography has a non-finite entry", "... not normalizable
+ * (h[2][2] = 0)", "... not invertible"). */
+int trb_streams_step_device_warp(trb_streams* s, const uint8_t* const* frames, const double* homographies,
+                                 void* cuda_stream);
 /* frames: host array of n_streams HOST pointers (pinned for best speed);
  * the H2D copy is part of the call.  If result_host is not NULL it
  * receives n_streams int32 blob counts (the D2H read of the step). */

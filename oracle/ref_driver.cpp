@@ -44,6 +44,7 @@ MotionConfig to_motion(const trb_motion_config* c) {
   m.window = c->window;
   m.threshold = c->threshold;
   m.bins = c->bins;
+  m.warp = c->warp == 1 ? WarpMode::PerFrameHomography : WarpMode::Identity;
   return m;
 }
 
@@ -151,6 +152,42 @@ int ref_label(const uint8_t* mask, int w, int h, const trb_seg_config* c, int se
       if (pixels_out)
         for (auto p : lab.blobs[i].pixels) pixels_out[off++] = p;
     }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// ---- warp_frame / stream_detect (motion.hpp:81-119, :260-282) ----
+static Homography to_hom(const double* h9) {
+  Homography hm;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) hm.h[r][c] = h9[3 * r + c];
+  return hm;
+}
+int ref_warp_frame(const uint8_t* in, int w, int h, int ch, const double* h9, uint8_t* out) {
+  try {
+    const Frame o = warp_frame(make_frame(in, w, h, ch), to_hom(h9));
+    std::memcpy(out, o.data.data(), o.data.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+// frames: n * w*h*ch bytes; h9s: n * 9 (NULL = no warp); masks_out: (n - W + 1) * w*h
+int ref_stream_detect(const uint8_t* frames, int n, int w, int h, int ch, const double* h9s,
+                      const trb_motion_config* c, uint8_t* masks_out, int* n_masks) {
+  try {
+    std::vector<Frame> fr;
+    const std::size_t fb = static_cast<std::size_t>(w) * h * ch;
+    for (int i = 0; i < n; ++i) fr.push_back(make_frame(frames + fb * i, w, h, ch, i));
+    std::vector<Homography> hs;
+    if (h9s)
+      for (int i = 0; i < n; ++i) hs.push_back(to_hom(h9s + 9 * i));
+    const auto masks = stream_detect(fr, h9s ? &hs : nullptr, to_motion(c));
+    *n_masks = static_cast<int>(masks.size());
+    for (std::size_t i = 0; i < masks.size(); ++i)
+      std::memcpy(masks_out + static_cast<std::size_t>(w) * h * i, masks[i].bits.data(), masks[i].bits.size());
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

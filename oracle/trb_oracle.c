@@ -184,6 +184,52 @@ void orc_grayscale(const uint8_t* rgb, int64_t n_px, uint8_t* out) {
     out[i] = (uint8_t)((77 * rgb[3 * i] + 150 * rgb[3 * i + 1] + 29 * rgb[3 * i + 2] + 128) >> 8);
 }
 
+/* warp_frame, motion.hpp:81-119.  Same expression trees as the reference
+ * (left-to-right, no contraction): the inverse by cofactors / det, per pixel
+ * w = inv20*x + inv21*y + inv22 (skipped when |w| < 1e-12), source
+ * (sx, sy), floor, bilinear weights, clamp to [0, 255], lround. */
+static double warp_tap(const uint8_t* f, int w, int h, int ch, int x, int y, int c) {
+  if (x < 0 || y < 0 || x >= w || y >= h) return 0.0;
+  return f[((size_t)y * w + x) * ch + c];
+}
+int orc_warp_frame(const uint8_t* f, int w, int hgt, int ch, const double* hm, uint8_t* out) {
+  for (int i = 0; i < 9; ++i)
+    if (!isfinite(hm[i])) return 1;
+  if (hm[8] == 0.0) return 2;
+#define H(r, c) hm[3 * (r) + (c)]
+  const double det = H(0, 0) * (H(1, 1) * H(2, 2) - H(1, 2) * H(2, 1)) - H(0, 1) * (H(1, 0) * H(2, 2) - H(1, 2) * H(2, 0)) +
+                     H(0, 2) * (H(1, 0) * H(2, 1) - H(1, 1) * H(2, 0));
+  if (fabs(det) < 1e-12) return 3;
+  const double inv[3][3] = {
+      {(H(1, 1) * H(2, 2) - H(1, 2) * H(2, 1)) / det, (H(0, 2) * H(2, 1) - H(0, 1) * H(2, 2)) / det,
+       (H(0, 1) * H(1, 2) - H(0, 2) * H(1, 1)) / det},
+      {(H(1, 2) * H(2, 0) - H(1, 0) * H(2, 2)) / det, (H(0, 0) * H(2, 2) - H(0, 2) * H(2, 0)) / det,
+       (H(0, 2) * H(1, 0) - H(0, 0) * H(1, 2)) / det},
+      {(H(1, 0) * H(2, 1) - H(1, 1) * H(2, 0)) / det, (H(0, 1) * H(2, 0) - H(0, 0) * H(2, 1)) / det,
+       (H(0, 0) * H(1, 1) - H(0, 1) * H(1, 0)) / det}};
+#undef H
+  memset(out, 0, (size_t)w * hgt * ch);
+  for (int y = 0; y < hgt; ++y)
+    for (int x = 0; x < w; ++x) {
+      const double ww = inv[2][0] * x + inv[2][1] * y + inv[2][2];
+      if (fabs(ww) < 1e-12) continue;
+      const double sx = (inv[0][0] * x + inv[0][1] * y + inv[0][2]) / ww;
+      const double sy = (inv[1][0] * x + inv[1][1] * y + inv[1][2]) / ww;
+      const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+      const double dx = sx - x0, dy = sy - y0;
+      for (int c = 0; c < ch; ++c) {
+        const double v = (1 - dx) * (1 - dy) * warp_tap(f, w, hgt, ch, x0, y0, c) +
+                         dx * (1 - dy) * warp_tap(f, w, hgt, ch, x0 + 1, y0, c) +
+                         (1 - dx) * dy * warp_tap(f, w, hgt, ch, x0, y0 + 1, c) +
+                         dx * dy * warp_tap(f, w, hgt, ch, x0 + 1, y0 + 1, c);
+        const double lo = (0.0 < v) ? v : 0.0;        /* std::max(0.0, v) */
+        const double cl = (lo < 255.0) ? lo : 255.0;  /* std::min(255.0, .) */
+        out[((size_t)y * w + x) * ch + c] = (uint8_t)lround(cl);
+      }
+    }
+  return 0;
+}
+
 /* extract_blob_features, segmentation.hpp:268-291: raster-order double
  * sums of the pixel values per label (luma for RGB, frame.hpp:91-93), then
  * sum / area and (x_max - x_min + 1) / (y_max - y_min + 1). */

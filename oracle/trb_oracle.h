@@ -52,6 +52,12 @@ void orc_morph(const uint8_t* in, int width, int height, int op, uint8_t* out);
 int orc_label(const uint8_t* mask, int width, int height, int connectivity, int min_area, int32_t* labels,
               trb_blob* blobs, int cap, int64_t* pixels);
 
+/* warp_frame (motion.hpp:81-119): inverse-mapped bilinear resampling under
+ * the homography h9 (row-major 3x3), samples off the source read 0.
+ * Returns 0, or 1 non-finite entry, 2 h[2][2] == 0, 3 not invertible
+ * (the reference's InvalidArgument cases). */
+int orc_warp_frame(const uint8_t* in, int width, int height, int channels, const double* h9, uint8_t* out);
+
 /* extract_blob_features (segmentation.hpp:266-291): per blob the mean
  * intensity (luma for RGB frames; the double sum of byte values is exact)
  * and the bbox aspect (width / height).  Returns -1 when the label image

@@ -8,12 +8,12 @@ from .api import (ACTIVE, EIGHT, FOUR, LOST, MEAN, MODE, CapacityError, ConfigEr
                   IoError, Labeling, MotionConfig, MotionDetector, SegmentationConfig, Streams, TeamrecError, Tracker,
                   TrackerConfig, build, device_count, extract_blob_features, histogram, label_blocked,
                   label_sequential, lib,
-                  meanshift_step, quantize_colors, synth_raster)
+                  meanshift_step, quantize_colors, synth_raster, warp_frame)
 
 __all__ = [
     "ACTIVE", "EIGHT", "FOUR", "LOST", "MEAN", "MODE", "CapacityError", "ConfigError", "CudaError",
     "InvalidArgument", "IoError", "Labeling", "MotionConfig", "MotionDetector", "SegmentationConfig", "Streams",
     "TeamrecError", "Tracker", "TrackerConfig", "build", "device_count", "extract_blob_features", "histogram",
     "label_blocked",
-    "label_sequential", "lib", "meanshift_step", "quantize_colors", "synth_raster",
+    "label_sequential", "lib", "meanshift_step", "quantize_colors", "synth_raster", "warp_frame",
 ]

@@ -120,6 +120,8 @@ def _declare(L):
         "trb_streams_step_device": [vp, vp, vp],
         "trb_streams_step_host": [vp, vp, vp, vp],
         "trb_streams_step_host_async": [vp, vp, vp, vp],
+        "trb_warp_frame": [vp, i32, i32, i32, vp, i32, vp],
+        "trb_streams_step_device_warp": [vp, vp, vp, vp],
         "trb_extract_blob_features": [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp],
         "trb_streams_blob_features": [vp, i32, vp, vp, vp, i32, C.POINTER(C.c_int)],
         "trb_streams_synchronize": [vp],
@@ -323,6 +325,16 @@ def meanshift_step(frame: np.ndarray, width: int, height: int, channels: int, cx
     return x.value, y.value, st.value
 
 
+def warp_frame(frame: np.ndarray, width: int, height: int, channels: int, homography, device: int = 0) -> np.ndarray:
+    """warp_frame (motion.hpp:81-119): inverse-mapped bilinear resampling by
+    the 3x3 homography (samples off the source plane read 0)."""
+    f = np.ascontiguousarray(frame, dtype=np.uint8).reshape(-1)
+    hm = np.ascontiguousarray(homography, dtype=np.float64).reshape(9)
+    out = np.empty(width * height * channels, np.uint8)
+    _check(lib().trb_warp_frame(_ptr(f), width, height, channels, _ptr(hm), device, _ptr(out)))
+    return out
+
+
 def extract_blob_features(labels: np.ndarray, width: int, height: int, frame: np.ndarray, frame_width: int,
                           frame_height: int, channels: int, blobs, device: int = 0):
     """extract_blob_features (segmentation.hpp:268-291) -> (mean_intensity,
@@ -380,6 +392,14 @@ class Streams:
         for i, p in enumerate(frame_ptrs):
             self._ptrs[i] = p
         _check(lib().trb_streams_step_device(self._h, self._ptrs, C.c_void_p(cuda_stream)))
+
+    def step_device_warp(self, frame_ptrs: Sequence[int], homographies, cuda_stream: int = 0) -> None:
+        """MotionConfig(warp=1): warp every stream's frame by its homography
+        (n_streams x 3 x 3) before it enters the window (stream_detect)."""
+        for i, p in enumerate(frame_ptrs):
+            self._ptrs[i] = p
+        hm = np.ascontiguousarray(homographies, dtype=np.float64).reshape(-1)
+        _check(lib().trb_streams_step_device_warp(self._h, self._ptrs, _ptr(hm), C.c_void_p(cuda_stream)))
 
     def step_host(self, frames: Sequence[np.ndarray], result: Optional[np.ndarray] = None,
                   cuda_stream: int = 0) -> None:

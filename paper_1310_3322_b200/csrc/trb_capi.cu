@@ -548,6 +548,40 @@ int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t*
   });
 }
 
+int trb_streams_step_device_warp(trb_streams* s, const uint8_t* const* frames, const double* homographies,
+                                 void* cuda_stream) {
+  return guard([&] {
+    need(s && frames, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->step_device_warp(frames, homographies, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int trb_warp_frame(const uint8_t* frame, int width, int height, int channels, const double* homography, int device,
+                   uint8_t* out) {
+  return guard([&] {
+    need(frame && homography && out, "null argument");
+    need(width >= 1 && height >= 1, "frame dimensions must be >= 1");
+    need(channels == 1 || channels == 3, "frame channels must be 1 or 3");
+    double inv[9];
+    trb::homography_inverse(homography, inv);  // validation first, like warp_frame
+    use_device(device);
+    const size_t fb = static_cast<size_t>(width) * height * channels;
+    trb::DevBuf din, dout, dinv, dptr;
+    din.alloc(fb, false);
+    dout.alloc(fb, false);
+    dinv.alloc(sizeof(inv), false);
+    dptr.alloc(sizeof(void*), false);
+    const uint8_t* p = din.as<uint8_t>();
+    TRB_CUDA(cudaMemcpy(din.p, frame, fb, cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaMemcpy(dinv.p, inv, sizeof(inv), cudaMemcpyHostToDevice));
+    TRB_CUDA(cudaMemcpy(dptr.p, &p, sizeof(void*), cudaMemcpyHostToDevice));
+    trb::launch_warp_frames(dptr.as<const uint8_t*>(), dout.as<uint8_t>(), static_cast<int64_t>(fb),
+                            dinv.as<double>(), width, height, channels, 1, 0);
+    TRB_CUDA(cudaMemcpy(out, dout.p, fb, cudaMemcpyDeviceToHost));
+  });
+}
+
 int trb_streams_step_host_async(trb_streams* s, const uint8_t* const* frames, int32_t* result_host,
                                 void* cuda_stream) {
   return guard([&] {

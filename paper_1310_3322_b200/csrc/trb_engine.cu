@@ -18,6 +18,8 @@ void validate_motion(const trb_motion_config& c) {
     throw Error(TRB_INVALID_ARGUMENT, "unknown background method (expected mean|mode)");
   if (c.morph < TRB_MORPH_NONE || c.morph > TRB_MORPH_CLOSE)
     throw Error(TRB_CONFIG_ERROR, "motion morph must be none|erode|dilate|open|close");
+  if (c.warp != 0 && c.warp != 1)
+    throw Error(TRB_CONFIG_ERROR, "unknown warp mode (expected identity|homography)");
 }
 
 // block_grid (segmentation.hpp:79-84): most-square factorisation.
@@ -265,8 +267,33 @@ const uint8_t* const* Streams::upload_ptrs_(const uint8_t* const* frames, cudaSt
   return dp;
 }
 
+void Streams::step_device_warp(const uint8_t* const* frames, const double* h9s, cudaStream_t st) {
+  if (!st) st = own_;
+  if (!h9s) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
+  const size_t fb = static_cast<size_t>(px_) * ch_;
+  if (!warp_buf_.p) {
+    warp_buf_.alloc(fb * S_);
+    std::vector<const uint8_t*> wp(S_);
+    for (int s = 0; s < S_; ++s) wp[s] = warp_buf_.as<uint8_t>() + fb * s;
+    warp_ptrs_.alloc(sizeof(void*) * S_, false);
+    TRB_CUDA(cudaMemcpy(warp_ptrs_.p, wp.data(), sizeof(void*) * S_, cudaMemcpyHostToDevice));
+    invs_dev_.alloc(sizeof(double) * 9 * S_ * kPtrSlots, false);
+    invs_host_.alloc(sizeof(double) * 9 * S_ * kPtrSlots);
+  }
+  const int slot = ptr_slot_;
+  const uint8_t* const* dp = upload_ptrs_(frames, st);  // waits for the slot's previous use
+  double* ih = static_cast<double*>(invs_host_.p) + static_cast<size_t>(slot) * 9 * S_;
+  for (int s = 0; s < S_; ++s) homography_inverse(h9s + 9 * s, ih + 9 * s);
+  double* id = invs_dev_.as<double>() + static_cast<size_t>(slot) * 9 * S_;
+  TRB_CUDA(cudaMemcpyAsync(id, ih, sizeof(double) * 9 * S_, cudaMemcpyHostToDevice, st));
+  launch_warp_frames(dp, warp_buf_.as<uint8_t>(), static_cast<int64_t>(fb), id, w_, h_, ch_, S_, st);
+  run_(warp_ptrs_.as<const uint8_t*>(), st);
+  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
+}
+
 void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
   if (!st) st = own_;
+  if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(frames, st);
   run_(dp, st);
@@ -296,6 +323,7 @@ bool is_pinned(const void* p) {
 
 void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
   if (!st) st = own_;
+  if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const size_t fb = static_cast<size_t>(px_) * ch_;
   const int b = host_step_++ & 1;
   if (!staging_[b].p) staging_[b].alloc(fb * S_, false);

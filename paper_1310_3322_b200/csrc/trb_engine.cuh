@@ -108,6 +108,10 @@ class Streams {
           const trb_tracker_config& tc, bool with_tracker);
   ~Streams();
   void step_device(const uint8_t* const* frames_host_array_of_dev_ptrs, cudaStream_t st);
+  // MotionConfig::warp == per-frame homography (stream_detect, motion.hpp:
+  // 260-282): every frame is first warped into the reference plane by its
+  // homography h9s[s*9 .. s*9+8] (row-major, host memory).
+  void step_device_warp(const uint8_t* const* frames_host_array_of_dev_ptrs, const double* h9s, cudaStream_t st);
   // synchronous: result_host (S blob counts) valid on return
   void step_host(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
   // pipelined: the H2D copy of this step's frames runs on a copy stream
@@ -144,6 +148,8 @@ class Streams {
   std::unique_ptr<CclState> ccl_;
   std::unique_ptr<TrackerState> tracker_;
   DevBuf mask_, mask_tmp_, frame_ptrs_, staging_[2];
+  DevBuf warp_buf_, warp_ptrs_, invs_dev_;  // warped frames, their pointer table, inverses [slot][S][9]
+  PinnedBuf invs_host_;
   PinnedBuf result_pinned_;
   cudaStream_t copy_ = nullptr;
   cudaEvent_t copied_[2] = {}, consumed_[2] = {};

@@ -38,6 +38,11 @@ void launch_motion_mode(const ModeArgs& a, int n_streams, cudaStream_t st);
 void launch_mean_background(const void* sums, int64_t px, int W, bool wide_sums, uint8_t* out, cudaStream_t st);
 // returns the number of launches issued
 int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int op, cudaStream_t st);
+// warp_frame (motion.hpp:81-119): host inverse (throws the reference's
+// InvalidArgument messages) and the per-pixel resampling of S frames.
+void homography_inverse(const double* h9, double* inv9);
+void launch_warp_frames(const uint8_t* const* in_dev, uint8_t* out, int64_t stride, const double* invs_dev, int w,
+                        int h, int ch, int n_streams, cudaStream_t st);
 void launch_synth_raster(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects, const uint8_t* colors,
                          int n, cudaStream_t st, int n_frames = 1, int64_t frame_stride = 0);
 

@@ -13,6 +13,8 @@
 //   mask  [px]    u8 0/1
 // Algorithmic bytes per pixel per frame (Mean, gray): frame 1 + evicted
 // sample 1 + new sample 1 + sum 2+2 + mask 1 = 8.
+#include <cmath>
+
 #include "trb_kernels.cuh"
 
 namespace trb {
@@ -292,6 +294,74 @@ int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int o
   }
   TRB_CUDA(cudaMemcpyAsync(mask, tmp, static_cast<size_t>(stride) * n_streams, cudaMemcpyDeviceToDevice, st));
   return 1;
+}
+
+// ------------------------------------------------------------------- warp
+// warp_frame (motion.hpp:81-119): inverse-mapped bilinear resampling, one
+// thread per output pixel (all channels).  The inverse is computed on the
+// host with the reference's cofactor expressions; here every fp64 op is an
+// explicit round-to-nearest intrinsic in the reference's left-to-right
+// order (no contraction), floor / lround as std::floor / std::lround.
+__global__ void __launch_bounds__(256) warp_frame_kernel(const uint8_t* const* in, int64_t in_stride,
+                                                         uint8_t* out, const double* invs, int w, int h, int ch) {
+  const int s = blockIdx.y;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= static_cast<int64_t>(w) * h) return;
+  const uint8_t* f = in[s];
+  uint8_t* o = out + in_stride * s;
+  const double* inv = invs + 9 * s;
+  const int y = static_cast<int>(p / w), x = static_cast<int>(p - static_cast<int64_t>(y) * w);
+  const double xd = x, yd = y;
+  const double ww = __dadd_rn(__dadd_rn(__dmul_rn(inv[6], xd), __dmul_rn(inv[7], yd)), inv[8]);
+  if (fabs(ww) < 1e-12) {  // projects to infinity; stays 0
+    for (int c = 0; c < ch; ++c) o[p * ch + c] = 0;
+    return;
+  }
+  const double sx = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(inv[0], xd), __dmul_rn(inv[1], yd)), inv[2]), ww);
+  const double sy = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(inv[3], xd), __dmul_rn(inv[4], yd)), inv[5]), ww);
+  const int x0 = __double2int_rz(floor(sx)), y0 = __double2int_rz(floor(sy));
+  const double dx = __dsub_rn(sx, static_cast<double>(x0)), dy = __dsub_rn(sy, static_cast<double>(y0));
+  const double ex = __dsub_rn(1.0, dx), ey = __dsub_rn(1.0, dy);
+  const double w00 = __dmul_rn(ex, ey), w10 = __dmul_rn(dx, ey), w01 = __dmul_rn(ex, dy), w11 = __dmul_rn(dx, dy);
+  auto tap = [&](int tx, int ty, int c) -> double {
+    if (tx < 0 || ty < 0 || tx >= w || ty >= h) return 0.0;
+    return f[(static_cast<int64_t>(ty) * w + tx) * ch + c];
+  };
+  for (int c = 0; c < ch; ++c) {
+    double v = __dmul_rn(w00, tap(x0, y0, c));
+    v = __dadd_rn(v, __dmul_rn(w10, tap(x0 + 1, y0, c)));
+    v = __dadd_rn(v, __dmul_rn(w01, tap(x0, y0 + 1, c)));
+    v = __dadd_rn(v, __dmul_rn(w11, tap(x0 + 1, y0 + 1, c)));
+    const double lo = (0.0 < v) ? v : 0.0;        // std::max(0.0, v)
+    const double cl = (lo < 255.0) ? lo : 255.0;  // std::min(255.0, .)
+    o[p * ch + c] = static_cast<uint8_t>(llround(cl));
+  }
+}
+
+// Homography::validate + the inverse of warp_frame (motion.hpp:73-95); host.
+void homography_inverse(const double* hm, double* inv) {
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(hm[i])) throw Error(TRB_INVALID_ARGUMENT, "homography has a non-finite entry");
+  if (hm[8] == 0.0) throw Error(TRB_INVALID_ARGUMENT, "homography is not normalizable (h[2][2] = 0)");
+  auto H = [&](int r, int c) { return hm[3 * r + c]; };
+  const double det = H(0, 0) * (H(1, 1) * H(2, 2) - H(1, 2) * H(2, 1)) -
+                     H(0, 1) * (H(1, 0) * H(2, 2) - H(1, 2) * H(2, 0)) +
+                     H(0, 2) * (H(1, 0) * H(2, 1) - H(1, 1) * H(2, 0));
+  if (std::abs(det) < 1e-12) throw Error(TRB_INVALID_ARGUMENT, "homography is not invertible");
+  const double r[9] = {(H(1, 1) * H(2, 2) - H(1, 2) * H(2, 1)) / det, (H(0, 2) * H(2, 1) - H(0, 1) * H(2, 2)) / det,
+                       (H(0, 1) * H(1, 2) - H(0, 2) * H(1, 1)) / det, (H(1, 2) * H(2, 0) - H(1, 0) * H(2, 2)) / det,
+                       (H(0, 0) * H(2, 2) - H(0, 2) * H(2, 0)) / det, (H(0, 2) * H(1, 0) - H(0, 0) * H(1, 2)) / det,
+                       (H(1, 0) * H(2, 1) - H(1, 1) * H(2, 0)) / det, (H(0, 1) * H(2, 0) - H(0, 0) * H(2, 1)) / det,
+                       (H(0, 0) * H(1, 1) - H(0, 1) * H(1, 0)) / det};
+  for (int i = 0; i < 9; ++i) inv[i] = r[i];
+}
+
+void launch_warp_frames(const uint8_t* const* in_dev, uint8_t* out, int64_t stride, const double* invs_dev, int w,
+                        int h, int ch, int n_streams, cudaStream_t st) {
+  const int64_t px = static_cast<int64_t>(w) * h;
+  dim3 grid(static_cast<unsigned>(ceil_div64(px, 256)), n_streams);
+  warp_frame_kernel<<<grid, 256, 0, st>>>(in_dev, stride, out, invs_dev, w, h, ch);
+  TRB_LAUNCH_CHECK("warp_frame_kernel");
 }
 
 void launch_synth_raster(uint8_t* out, int w, int h, int ch, uint8_t bg, const int32_t* rects, const uint8_t* colors,

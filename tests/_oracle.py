@@ -88,6 +88,7 @@ def orc_lib():
                                        C.c_uint64]
         L.orc_synth_destroy.argtypes = [vp]
         L.orc_synth_next.argtypes = [vp, C.c_void_p, C.c_void_p]
+        L.orc_warp_frame.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_libm_hypot.restype = C.c_double
@@ -115,6 +116,9 @@ def ref_lib():
         L.ref_label.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(SEG_CFG), C.c_int, C.c_int, C.c_void_p,
                                 C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_void_p]
         L.ref_quantize_colors.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+        L.ref_warp_frame.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_stream_detect.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                        C.POINTER(MOTION_CFG), C.c_void_p, C.POINTER(C.c_int)]
         L.ref_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_histogram.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -202,6 +206,38 @@ def cpu_label(mask: np.ndarray, w: int, h: int, conn: int = 1, min_area: int = 4
             raise RuntimeError(ref_lib().ref_last_error().decode())
         n = nn.value
     return labels, blobs_to_array(blobs, n), (pixels[:int(np.count_nonzero(labels))] if want_pixels else None)
+
+
+WARP_ERRORS = {1: "homography has a non-finite entry", 2: "homography is not normalizable (h[2][2] = 0)",
+               3: "homography is not invertible"}
+
+
+def cpu_warp_frame(frame, w, h, ch, hom, impl="orc"):
+    """warp_frame -> uint8[w*h*ch]; ValueError(message) on InvalidArgument."""
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    hm = np.ascontiguousarray(hom, dtype=np.float64).reshape(9)
+    out = np.zeros(w * h * ch, np.uint8)
+    if impl == "orc":
+        rc = orc_lib().orc_warp_frame(f.ctypes.data, w, h, ch, hm.ctypes.data, out.ctypes.data)
+        if rc:
+            raise ValueError(WARP_ERRORS[rc])
+    else:
+        if ref_lib().ref_warp_frame(f.ctypes.data, w, h, ch, hm.ctypes.data, out.ctypes.data):
+            raise ValueError(ref_lib().ref_last_error().decode())
+    return out
+
+
+def ref_stream_detect(frames, w, h, ch, homs, cfg: MOTION_CFG):
+    """The reference's stream_detect (motion.hpp:260-282) -> masks [n-W+1, w*h]."""
+    fr = np.ascontiguousarray(frames, dtype=np.uint8)
+    n = fr.shape[0]
+    hm = None if homs is None else np.ascontiguousarray(homs, dtype=np.float64)
+    out = np.zeros((max(1, n - cfg.window + 1), w * h), np.uint8)
+    nm = C.c_int(0)
+    if ref_lib().ref_stream_detect(fr.ctypes.data, n, w, h, ch, None if hm is None else hm.ctypes.data,
+                                   C.byref(cfg), out.ctypes.data, C.byref(nm)):
+        raise ValueError(ref_lib().ref_last_error().decode())
+    return out[:nm.value]
 
 
 def cpu_blob_features(labels, w, h, frame, fw, fh, ch, blobs, impl="orc"):

@@ -113,12 +113,64 @@ def blob_features_case(trials: int = 40):
     return out
 
 
+def _random_homography(rng, kind):
+    if kind == 0:
+        return np.eye(3)
+    if kind == 1:  # fractional translation
+        h = np.eye(3)
+        h[0, 2], h[1, 2] = rng.uniform(-6, 6), rng.uniform(-6, 6)
+        return h
+    if kind == 2:  # rotation + scale + translation
+        a, sc = rng.uniform(-0.4, 0.4), rng.uniform(0.7, 1.4)
+        return np.array([[sc * np.cos(a), -sc * np.sin(a), rng.uniform(-5, 5)],
+                         [sc * np.sin(a), sc * np.cos(a), rng.uniform(-5, 5)], [0.0, 0.0, 1.0]])
+    if kind == 3:  # projective
+        h = np.eye(3) + rng.uniform(-0.05, 0.05, size=(3, 3))
+        h[2, 0], h[2, 1] = rng.uniform(-0.01, 0.01), rng.uniform(-0.01, 0.01)
+        h[2, 2] = rng.uniform(0.8, 1.2)
+        return h
+    h = np.eye(3)  # everything maps off the source plane
+    h[0, 2] = 1e4
+    return h
+
+
+def warp_case(trials: int = 40):
+    """warp_frame (motion.hpp:81-119) through the reference on random frames
+    and homographies (identity, sub-pixel translation, rotation/scale,
+    projective, off-plane), gray and RGB; plus stream_detect (:260-282) with
+    per-frame homographies on a small clip."""
+    rng = np.random.default_rng(21)
+    dims, frames, homs, outs = [], [], [], []
+    for trial in range(trials):
+        w, h, ch = int(rng.integers(1, 65)), int(rng.integers(1, 65)), 1 if trial % 3 else 3
+        f = rng.integers(0, 256, size=w * h * ch, dtype=np.uint8)
+        hm = _random_homography(rng, trial % 5)
+        dims.append((w, h, ch))
+        frames.append(f)
+        homs.append(hm.reshape(9))
+        outs.append(O.cpu_warp_frame(f, w, h, ch, hm, "ref"))
+    # stream_detect on a panning 48x36 clip, W = 9
+    clip = harness_vision_clip()
+    n = 20
+    cf, _ = O.ref_frames(clip, n)
+    sh = np.stack([np.array([[1, 0.02 * t, 0.7 * t], [-0.02 * t, 1, -0.4 * t], [0, 0, 1]], np.float64).reshape(9)
+                   for t in range(n)])
+    mcfg = MOTION_CFG(window=9)
+    mcfg.warp = 1
+    masks = O.ref_stream_detect(cf, clip.width, clip.height, clip.channels, sh, mcfg)
+    return dict(dims=np.array(dims, np.int32), frames=np.concatenate(frames), homs=np.array(homs),
+                outs=np.concatenate(outs), stream_frames=cf, stream_homs=sh, stream_masks=masks)
+
+
 def main():
     if not O.ref_available():
         sys.exit("oracle/_ref/libteamrec_ref.so missing: run `make -C oracle` where /root/reference exists")
     out = {}
     if "blob_features" in sys.argv[1:]:  # only the extract_blob_features fixture
         out["blob_features"] = blob_features_case()
+    if "warp" in sys.argv[1:]:  # only the warp_frame / stream_detect fixture
+        out["warp"] = warp_case()
+    if out:
         for name, d in out.items():
             np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
             print(name, {k: getattr(v, "shape", None) for k, v in d.items()})
@@ -145,6 +197,7 @@ def main():
     out["random_ccl"] = dict(masks=np.array(masks), label_sha=np.array(labels_sha), nblobs=np.array(nb),
                              conn=np.array(conns))
     out["blob_features"] = blob_features_case()
+    out["warp"] = warp_case()
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
         print(name, {k: getattr(v, "shape", None) for k, v in d.items()})

@@ -240,3 +240,29 @@ def test_blob_features_full_frame_vs_oracle(gpu):
                                  lab.blobs, "orc")
     assert len(mean) > 5
     assert mean.tobytes() == om.tobytes() and aspect.tobytes() == oa.tobytes()
+
+
+# ---------------------------------------------------- warp_frame (§8(f) 4)
+def test_warp_frame_golden(gpu):
+    g = np.load(os.path.join(GOLD, "warp.npz"))
+    of = 0
+    for (w, h, ch), hm in zip(g["dims"], g["homs"]):
+        n = w * h * ch
+        out = gpu.warp_frame(g["frames"][of:of + n], w, h, ch, hm)
+        assert out.tobytes() == g["outs"][of:of + n].tobytes()
+        of += n
+
+
+def test_warp_frame_errors_and_large(gpu):
+    from paper_1310_3322_b200.api import InvalidArgument
+    f = np.zeros(12, np.uint8)
+    for hm, msg in [([[1, 0, np.inf], [0, 1, 0], [0, 0, 1]], "non-finite"),
+                    ([[1, 0, 0], [0, 1, 0], [0, 0, 0.0]], "not normalizable"),
+                    ([[1, 2, 0], [2, 4, 0], [0, 0, 1.0]], "not invertible")]:
+        with pytest.raises(InvalidArgument, match=msg):
+            gpu.warp_frame(f, 4, 3, 1, np.array(hm, np.float64))
+    # a full 1080p frame under a projective homography vs the oracle
+    rng = np.random.default_rng(3)
+    fr = rng.integers(0, 256, size=1920 * 1080, dtype=np.uint8)
+    hm = np.array([[0.98, 0.05, 12.3], [-0.04, 1.01, -7.7], [1e-5, -2e-5, 1.0]])
+    assert gpu.warp_frame(fr, 1920, 1080, 1, hm).tobytes() == O.cpu_warp_frame(fr, 1920, 1080, 1, hm).tobytes()

@@ -119,3 +119,29 @@ def test_streams_blob_features_vs_oracle(gpu):
         om, oa = O.cpu_blob_features(labels, c0.width, c0.height, frames[s][n - 1], c0.width, c0.height, 1, blobs)
         assert len(mean) == len(blobs) > 0
         assert mean.tobytes() == om.tobytes() and aspect.tobytes() == oa.tobytes()
+
+
+def test_streams_warp_matches_reference_stream_detect(gpu):
+    """MotionConfig(warp=homography): frames warped into the reference plane
+    on the device before the window (stream_detect, motion.hpp:260-282); the
+    masks equal the reference's stream_detect output (golden)."""
+    import torch
+    from paper_1310_3322_b200.api import InvalidArgument
+    g = np.load(os.path.join(GOLD, "warp.npz"))
+    clip = harness_vision_clip()
+    frames, homs = g["stream_frames"], g["stream_homs"]
+    mcfg = MOTION_CFG(window=9)
+    mcfg.warp = 1
+    dev = torch.from_numpy(frames).cuda()
+    st = gpu.Streams(2, clip.width, clip.height, clip.channels, mcfg, SEG_CFG(), TRACKER_CFG())
+    with pytest.raises(InvalidArgument, match="requires per-frame homographies"):
+        st.step_device([dev[0].data_ptr()] * 2)
+    masks = []
+    for t in range(frames.shape[0]):
+        st.step_device_warp([dev[t].data_ptr()] * 2, np.stack([homs[t], homs[t]]))
+        if st.has_output:
+            masks.append((st.mask(0).copy(), st.mask(1).copy()))
+    st.synchronize()
+    assert len(masks) == len(g["stream_masks"])
+    for (m0, m1), ref in zip(masks, g["stream_masks"]):
+        assert m0.tobytes() == ref.tobytes() and m1.tobytes() == ref.tobytes()

@@ -273,3 +273,34 @@ def test_blob_features_vs_reference():
         a = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "orc")
         b = O.cpu_blob_features(lab, w, h, f, w, h, ch, blobs, "ref")
         assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+
+
+# ---------------------------------------------------- warp_frame (§8(f) 4)
+def test_warp_golden():
+    g = gold("warp")
+    of = 0
+    for (w, h, ch), hm in zip(g["dims"], g["homs"]):
+        n = w * h * ch
+        out = O.cpu_warp_frame(g["frames"][of:of + n], w, h, ch, hm, "orc")
+        assert out.tobytes() == g["outs"][of:of + n].tobytes()
+        of += n
+
+
+def test_warp_errors():
+    f = np.zeros(12, np.uint8)
+    for hm, msg in [(np.array([[1, 0, np.inf], [0, 1, 0], [0, 0, 1]]), "non-finite"),
+                    (np.array([[1, 0, 0], [0, 1, 0], [0, 0, 0.0]]), "not normalizable"),
+                    (np.array([[1, 2, 0], [2, 4, 0], [0, 0, 1.0]]), "not invertible")]:
+        with pytest.raises(ValueError, match=msg):
+            O.cpu_warp_frame(f, 4, 3, 1, hm, "orc")
+
+
+@needs_ref
+def test_warp_vs_reference():
+    rng = np.random.default_rng(22)
+    from tests.golden.make_golden import _random_homography
+    for trial in range(25):
+        w, h, ch = int(rng.integers(1, 40)), int(rng.integers(1, 40)), 1 if trial % 2 else 3
+        f = rng.integers(0, 256, size=w * h * ch, dtype=np.uint8)
+        hm = _random_homography(rng, trial % 5)
+        assert O.cpu_warp_frame(f, w, h, ch, hm, "orc").tobytes() == O.cpu_warp_frame(f, w, h, ch, hm, "ref").tobytes()
