@@ -136,6 +136,27 @@ int trb_motion_frames_seen(const trb_motion* m, int* n);
 int trb_label(const uint8_t* mask, int width, int height, const trb_seg_config* cfg, int device, int32_t* labels_out,
               trb_blob* blobs_out, int blob_cap, int* n_blobs, int64_t* pixels_out, int64_t pixels_cap);
 
+/* ---- frame / track-log I/O (host side, no device) ----
+ * decode_pnm / load_pnm (frame.hpp:152-183): binary P5 (gray) / P6 (RGB),
+ * maxval 255, '#' comments in the header.  out == NULL queries the shape.
+ * load_frame_sequence (:198-225): every .pgm/.ppm of `dir`, ordered by the
+ * trailing digits of the file stem; out receives n_frames frames back to
+ * back, indices (nullable) their indices.  Errors: TRB_IO_ERROR with the
+ * reference's IoError messages. */
+int trb_decode_pnm(const uint8_t* bytes, int64_t n, const char* source_name, int* width, int* height, int* channels,
+                   uint8_t* out, int64_t out_cap);
+int trb_load_pnm(const char* path, int* width, int* height, int* channels, uint8_t* out, int64_t out_cap);
+int trb_load_frame_sequence(const char* dir, int* n_frames, int* width, int* height, int* channels,
+                            int64_t* indices, uint8_t* out, int64_t out_cap);
+/* Track-log interchange (tracking.hpp:244-285): text lines
+ * `frame track_id x y w h status` (x, y as %.17g).  format: *len = text
+ * length (out NULL = query; cap includes the terminating NUL). */
+int trb_format_track_log(const trb_track_log_entry* log, int64_t n, char* out, int64_t cap, int64_t* len);
+int trb_parse_track_log(const char* text, int64_t len, const char* source, trb_track_log_entry* out, int64_t cap,
+                        int64_t* n);
+int trb_save_track_log(const char* path, const trb_track_log_entry* log, int64_t n);
+int trb_load_track_log(const char* path, trb_track_log_entry* out, int64_t cap, int64_t* n);
+
 /* ---- warp_frame (motion.hpp:81-119) ----
  * Inverse-mapped bilinear resampling of one frame (host buffers) by the
  * homography h (row-major 3x3); samples off the source plane read 0. */

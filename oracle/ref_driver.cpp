@@ -194,6 +194,65 @@ int ref_stream_detect(const uint8_t* frames, int n, int w, int h, int ch, const 
   }
 }
 
+// ---- PNM ingest / track-log interchange (frame.hpp:152-225, tracking.hpp:247-285) ----
+int ref_decode_pnm(const uint8_t* bytes, int64_t n, const char* src, int* w, int* h, int* ch, uint8_t* out,
+                   int64_t cap) {
+  try {
+    const Frame f = decode_pnm(std::vector<std::uint8_t>(bytes, bytes + n), src);
+    *w = f.width, *h = f.height, *ch = f.channels;
+    if (out && static_cast<int64_t>(f.data.size()) <= cap) std::memcpy(out, f.data.data(), f.data.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int ref_load_frame_sequence(const char* dir, int* n, int* w, int* h, int* ch, int64_t* idx, uint8_t* out,
+                            int64_t cap) {
+  try {
+    const auto fr = load_frame_sequence(dir);
+    *n = static_cast<int>(fr.size());
+    *w = fr.empty() ? 0 : fr[0].width, *h = fr.empty() ? 0 : fr[0].height, *ch = fr.empty() ? 0 : fr[0].channels;
+    int64_t off = 0;
+    for (std::size_t i = 0; i < fr.size(); ++i) {
+      if (idx) idx[i] = fr[i].index;
+      if (out && off + static_cast<int64_t>(fr[i].data.size()) <= cap)
+        std::memcpy(out + off, fr[i].data.data(), fr[i].data.size());
+      off += static_cast<int64_t>(fr[i].data.size());
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+static TrackLogEntry to_entry(const trb_track_log_entry& e) {
+  TrackLogEntry t;
+  t.frame = e.frame, t.track_id = e.track_id, t.x = e.x, t.y = e.y, t.w = e.w, t.h = e.h;
+  t.status = e.status == 0 ? TrackStatus::Active : TrackStatus::Lost;
+  return t;
+}
+int64_t ref_format_track_log(const trb_track_log_entry* log, int64_t n, char* out, int64_t cap) {
+  std::vector<TrackLogEntry> v;
+  for (int64_t i = 0; i < n; ++i) v.push_back(to_entry(log[i]));
+  const std::string s = format_track_log(v);
+  if (out && static_cast<int64_t>(s.size()) < cap) std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int64_t>(s.size());
+}
+int ref_parse_track_log(const char* text, int64_t len, const char* src, trb_track_log_entry* out, int64_t cap,
+                        int64_t* n) {
+  try {
+    const auto v = parse_track_log(std::string(text, static_cast<std::size_t>(len)), src);
+    *n = static_cast<int64_t>(v.size());
+    for (std::size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) {
+      out[i].frame = v[i].frame, out[i].track_id = v[i].track_id, out[i].x = v[i].x, out[i].y = v[i].y;
+      out[i].w = v[i].w, out[i].h = v[i].h, out[i].status = v[i].status == TrackStatus::Active ? 0 : 1;
+      out[i]._pad = 0;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ---- extract_blob_features (segmentation.hpp:268-291) ----
 // The labelling is rebuilt from the label image + blob records (the
 // function reads only labels, width/height and the blob table).

@@ -8,12 +8,14 @@ from .api import (ACTIVE, EIGHT, FOUR, LOST, MEAN, MODE, CapacityError, ConfigEr
                   IoError, Labeling, MotionConfig, MotionDetector, SegmentationConfig, Streams, TeamrecError, Tracker,
                   TrackerConfig, build, device_count, extract_blob_features, histogram, label_blocked,
                   label_sequential, lib,
-                  meanshift_step, quantize_colors, synth_raster, warp_frame)
+                  meanshift_step, quantize_colors, synth_raster, warp_frame, decode_pnm, load_pnm,
+                  load_frame_sequence, format_track_log, parse_track_log, save_track_log, load_track_log)
 
 __all__ = [
     "ACTIVE", "EIGHT", "FOUR", "LOST", "MEAN", "MODE", "CapacityError", "ConfigError", "CudaError",
     "InvalidArgument", "IoError", "Labeling", "MotionConfig", "MotionDetector", "SegmentationConfig", "Streams",
     "TeamrecError", "Tracker", "TrackerConfig", "build", "device_count", "extract_blob_features", "histogram",
     "label_blocked",
-    "label_sequential", "lib", "meanshift_step", "quantize_colors", "synth_raster", "warp_frame",
+    "label_sequential", "lib", "meanshift_step", "quantize_colors", "synth_raster", "warp_frame", "decode_pnm",
+    "load_pnm", "load_frame_sequence", "format_track_log", "parse_track_log", "save_track_log", "load_track_log",
 ]

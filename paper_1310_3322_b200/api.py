@@ -121,6 +121,14 @@ def _declare(L):
         "trb_streams_step_host": [vp, vp, vp, vp],
         "trb_streams_step_host_async": [vp, vp, vp, vp],
         "trb_warp_frame": [vp, i32, i32, i32, vp, i32, vp],
+        "trb_decode_pnm": [vp, i64, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), vp, i64],
+        "trb_load_pnm": [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), vp, i64],
+        "trb_load_frame_sequence": [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int), vp, vp, i64],
+        "trb_format_track_log": [vp, i64, vp, i64, C.POINTER(C.c_int64)],
+        "trb_parse_track_log": [C.c_char_p, i64, C.c_char_p, vp, i64, C.POINTER(C.c_int64)],
+        "trb_save_track_log": [C.c_char_p, vp, i64],
+        "trb_load_track_log": [C.c_char_p, vp, i64, C.POINTER(C.c_int64)],
         "trb_streams_step_device_warp": [vp, vp, vp, vp],
         "trb_extract_blob_features": [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp],
         "trb_streams_blob_features": [vp, i32, vp, vp, vp, i32, C.POINTER(C.c_int)],
@@ -323,6 +331,75 @@ def meanshift_step(frame: np.ndarray, width: int, height: int, channels: int, cx
     _check(lib().trb_meanshift_step(_ptr(f), width, height, channels, C.byref(x), C.byref(y), w, h, _ptr(c), _ptr(q),
                                     q.size, max_iters, eps, C.byref(st), device))
     return x.value, y.value, st.value
+
+
+# ------------------------------------------------------------------ I/O
+def decode_pnm(data: bytes, source_name: str = "<memory>"):
+    """decode_pnm (frame.hpp:152-175) -> (pixels uint8[w*h*ch], w, h, ch)."""
+    buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+    w, h, c = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib().trb_decode_pnm(_ptr(buf), len(data), source_name.encode(), C.byref(w), C.byref(h), C.byref(c),
+                                None, 0))
+    out = np.empty(w.value * h.value * c.value, np.uint8)
+    _check(lib().trb_decode_pnm(_ptr(buf), len(data), source_name.encode(), C.byref(w), C.byref(h), C.byref(c),
+                                _ptr(out), out.size))
+    return out, w.value, h.value, c.value
+
+
+def load_pnm(path: str):
+    """load_pnm (frame.hpp:177-182) -> (pixels, w, h, ch)."""
+    w, h, c = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib().trb_load_pnm(str(path).encode(), C.byref(w), C.byref(h), C.byref(c), None, 0))
+    out = np.empty(w.value * h.value * c.value, np.uint8)
+    _check(lib().trb_load_pnm(str(path).encode(), C.byref(w), C.byref(h), C.byref(c), _ptr(out), out.size))
+    return out, w.value, h.value, c.value
+
+
+def load_frame_sequence(directory: str):
+    """load_frame_sequence (frame.hpp:198-225) -> (frames [n, w*h*ch], indices, w, h, ch)."""
+    n, w, h, c = C.c_int(0), C.c_int(0), C.c_int(0), C.c_int(0)
+    d = str(directory).encode()
+    _check(lib().trb_load_frame_sequence(d, C.byref(n), C.byref(w), C.byref(h), C.byref(c), None, None, 0))
+    fb = w.value * h.value * c.value
+    out = np.empty((n.value, fb), np.uint8)
+    idx = np.empty(max(1, n.value), np.int64)
+    _check(lib().trb_load_frame_sequence(d, C.byref(n), C.byref(w), C.byref(h), C.byref(c), _ptr(idx), _ptr(out),
+                                         out.size))
+    return out, idx[:n.value], w.value, h.value, c.value
+
+
+def format_track_log(log) -> str:
+    """format_track_log (tracking.hpp:247-256)."""
+    a = np.ascontiguousarray(log, dtype=LOG_DTYPE)
+    n = C.c_int64(0)
+    _check(lib().trb_format_track_log(_ptr(a) if len(a) else None, len(a), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().trb_format_track_log(_ptr(a) if len(a) else None, len(a), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def parse_track_log(text: str, source: str = "<memory>") -> np.ndarray:
+    """parse_track_log (tracking.hpp:258-277) -> structured log array."""
+    t = text.encode()
+    n = C.c_int64(0)
+    _check(lib().trb_parse_track_log(t, len(t), source.encode(), None, 0, C.byref(n)))
+    out = np.zeros(n.value, LOG_DTYPE)
+    _check(lib().trb_parse_track_log(t, len(t), source.encode(), _ptr(out) if n.value else None, n.value,
+                                     C.byref(n)))
+    return out
+
+
+def save_track_log(log, path: str) -> None:
+    a = np.ascontiguousarray(log, dtype=LOG_DTYPE)
+    _check(lib().trb_save_track_log(str(path).encode(), _ptr(a) if len(a) else None, len(a)))
+
+
+def load_track_log(path: str) -> np.ndarray:
+    n = C.c_int64(0)
+    _check(lib().trb_load_track_log(str(path).encode(), None, 0, C.byref(n)))
+    out = np.zeros(n.value, LOG_DTYPE)
+    _check(lib().trb_load_track_log(str(path).encode(), _ptr(out) if n.value else None, n.value, C.byref(n)))
+    return out
 
 
 def warp_frame(frame: np.ndarray, width: int, height: int, channels: int, homography, device: int = 0) -> np.ndarray:

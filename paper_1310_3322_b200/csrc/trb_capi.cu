@@ -5,8 +5,14 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <map>
+#include <sstream>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -887,3 +893,237 @@ extern "C" int trb_debug_phases(uint64_t* out128) {
     trb::read_phases(reinterpret_cast<unsigned long long*>(out128));
   });
 }
+
+// ===================================================================== I/O
+// SURVEY §8(f) row 3, host side: PNM ingest (frame.hpp:119-225) and the
+// track-log interchange (tracking.hpp:244-285), restated in C++ with the
+// reference's parsing rules and IoError messages (same standard library, so
+// std::stoi / istream / std::sort behave identically).
+namespace {
+namespace fs = std::filesystem;
+
+std::string pnm_token(const uint8_t* b, size_t n, size_t& pos, const std::string& src) {  // frame.hpp:120-134
+  for (;;) {
+    while (pos < n && std::isspace(b[pos])) ++pos;
+    if (pos < n && b[pos] == '#') {
+      while (pos < n && b[pos] != '\n') ++pos;
+      continue;
+    }
+    break;
+  }
+  if (pos >= n) throw Error(TRB_IO_ERROR, "truncated pnm header in " + src);
+  std::string tok;
+  while (pos < n && !std::isspace(b[pos])) tok.push_back(static_cast<char>(b[pos++]));
+  return tok;
+}
+
+int pnm_int(const uint8_t* b, size_t n, size_t& pos, const std::string& src) {  // frame.hpp:136-148
+  const std::string tok = pnm_token(b, n, pos, src);
+  try {
+    size_t used = 0;
+    const int v = std::stoi(tok, &used);
+    if (used != tok.size()) throw std::invalid_argument(tok);
+    return v;
+  } catch (const std::exception&) {
+    throw Error(TRB_IO_ERROR, "bad pnm header value '" + tok + "' in " + src);
+  }
+}
+
+struct Pnm {
+  int w, h, ch;
+  size_t off;  // first pixel byte
+};
+
+Pnm decode_pnm_header(const uint8_t* b, size_t n, const std::string& src) {  // decode_pnm, frame.hpp:152-175
+  size_t pos = 0;
+  const std::string magic = pnm_token(b, n, pos, src);
+  int ch = 0;
+  if (magic == "P5") ch = 1;
+  else if (magic == "P6") ch = 3;
+  else throw Error(TRB_IO_ERROR, "unsupported pnm magic '" + magic + "' in " + src + " (want P5 or P6)");
+  const int w = pnm_int(b, n, pos, src);
+  const int h = pnm_int(b, n, pos, src);
+  const int maxval = pnm_int(b, n, pos, src);
+  if (w < 1 || h < 1) throw Error(TRB_IO_ERROR, "bad pnm dimensions in " + src);
+  if (maxval != 255) throw Error(TRB_IO_ERROR, "unsupported pnm maxval " + std::to_string(maxval) + " in " + src);
+  ++pos;  // single whitespace after maxval
+  const size_t need = static_cast<size_t>(w) * h * ch;
+  if (n < pos || n - pos < need) throw Error(TRB_IO_ERROR, "truncated pnm pixel data in " + src);
+  return Pnm{w, h, ch, pos};
+}
+
+std::vector<uint8_t> slurp_bytes(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(TRB_IO_ERROR, "cannot open " + path);
+  return std::vector<uint8_t>((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+std::string fmt_g17(double v) {  // textio.hpp:16-20
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+
+std::string format_track_log(const trb_track_log_entry* log, int64_t n) {  // tracking.hpp:247-256
+  std::string out = "# frame track_id x y w h status\n";
+  for (int64_t i = 0; i < n; ++i) {
+    const auto& e = log[i];
+    out += std::to_string(e.frame) + " " + std::to_string(e.track_id) + " " + fmt_g17(e.x) + " " + fmt_g17(e.y) +
+           " " + std::to_string(e.w) + " " + std::to_string(e.h) + " " +
+           (e.status == TRB_TRACK_ACTIVE ? "active" : "lost") + "\n";
+  }
+  return out;
+}
+
+std::vector<trb_track_log_entry> parse_track_log(const std::string& text, const std::string& source) {  // :258-277
+  std::vector<trb_track_log_entry> out;
+  std::istringstream in(text);
+  std::string line;
+  size_t lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    const auto first = line.find_first_not_of(" \t\r");
+    if (first == std::string::npos || line[first] == '#') continue;
+    std::istringstream ls(line);
+    trb_track_log_entry e{};
+    int frame = 0, id = 0, w = 0, h = 0;
+    double x = 0, y = 0;
+    std::string status;
+    if (!(ls >> frame >> id >> x >> y >> w >> h >> status))
+      throw Error(TRB_IO_ERROR, "bad track log record at " + source + ":" + std::to_string(lineno));
+    e.frame = frame, e.track_id = id, e.x = x, e.y = y, e.w = w, e.h = h;
+    if (status == "active") e.status = TRB_TRACK_ACTIVE;
+    else if (status == "lost") e.status = TRB_TRACK_LOST;
+    else throw Error(TRB_IO_ERROR, "unknown track status '" + status + "' at " + source + ":" + std::to_string(lineno));
+    out.push_back(e);
+  }
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+int trb_decode_pnm(const uint8_t* bytes, int64_t n, const char* source_name, int* width, int* height, int* channels,
+                   uint8_t* out, int64_t out_cap) {
+  return guard([&] {
+    need(bytes && width && height && channels, "null argument");
+    const Pnm p = decode_pnm_header(bytes, static_cast<size_t>(n), source_name ? source_name : "<memory>");
+    *width = p.w, *height = p.h, *channels = p.ch;
+    if (!out) return;
+    const size_t need_b = static_cast<size_t>(p.w) * p.h * p.ch;
+    if (static_cast<int64_t>(need_b) > out_cap) throw Error(TRB_CAPACITY, "pixel buffer too small");
+    std::memcpy(out, bytes + p.off, need_b);
+  });
+}
+
+int trb_load_pnm(const char* path, int* width, int* height, int* channels, uint8_t* out, int64_t out_cap) {
+  return guard([&] {
+    need(path && width && height && channels, "null argument");
+    const auto b = slurp_bytes(path);
+    const Pnm p = decode_pnm_header(b.data(), b.size(), path);
+    *width = p.w, *height = p.h, *channels = p.ch;
+    if (!out) return;
+    const size_t need_b = static_cast<size_t>(p.w) * p.h * p.ch;
+    if (static_cast<int64_t>(need_b) > out_cap) throw Error(TRB_CAPACITY, "pixel buffer too small");
+    std::memcpy(out, b.data() + p.off, need_b);
+  });
+}
+
+int trb_load_frame_sequence(const char* dir, int* n_frames, int* width, int* height, int* channels,
+                            int64_t* indices, uint8_t* out, int64_t out_cap) {
+  return guard([&] {  // load_frame_sequence, frame.hpp:198-225
+    need(dir && n_frames && width && height && channels, "null argument");
+    const fs::path d(dir);
+    if (!fs::is_directory(d)) throw Error(TRB_IO_ERROR, "not a directory: " + d.string());
+    std::vector<fs::path> files;
+    for (const auto& e : fs::directory_iterator(d)) {
+      if (!e.is_regular_file()) continue;
+      const auto ext = e.path().extension().string();
+      if (ext == ".pgm" || ext == ".ppm") files.push_back(e.path());
+    }
+    std::sort(files.begin(), files.end());
+    struct F {
+      std::vector<uint8_t> bytes;
+      Pnm p;
+      int64_t index;
+    };
+    std::vector<F> frames;
+    for (const auto& path : files) {
+      F f;
+      f.bytes = slurp_bytes(path.string());
+      f.p = decode_pnm_header(f.bytes.data(), f.bytes.size(), path.string());
+      const std::string stem = path.stem().string();
+      size_t k = stem.size();
+      while (k > 0 && std::isdigit(static_cast<unsigned char>(stem[k - 1]))) --k;
+      f.index = k < stem.size() ? std::stoll(stem.substr(k)) : static_cast<int64_t>(frames.size());
+      if (!frames.empty()) {
+        const Pnm& a = frames.front().p;
+        if (a.w != f.p.w || a.h != f.p.h || a.ch != f.p.ch)
+          throw Error(TRB_IO_ERROR, "dimension mismatch in " + path.string() + ": expected " + std::to_string(a.w) +
+                                        "x" + std::to_string(a.h) + "x" + std::to_string(a.ch) + ", got " +
+                                        std::to_string(f.p.w) + "x" + std::to_string(f.p.h) + "x" +
+                                        std::to_string(f.p.ch));
+      }
+      frames.push_back(std::move(f));
+    }
+    std::sort(frames.begin(), frames.end(), [](const F& a, const F& b) { return a.index < b.index; });
+    *n_frames = static_cast<int>(frames.size());
+    *width = frames.empty() ? 0 : frames[0].p.w;
+    *height = frames.empty() ? 0 : frames[0].p.h;
+    *channels = frames.empty() ? 0 : frames[0].p.ch;
+    if (!out) return;
+    const size_t fb = frames.empty() ? 0 : static_cast<size_t>(*width) * *height * *channels;
+    if (static_cast<int64_t>(fb * frames.size()) > out_cap) throw Error(TRB_CAPACITY, "frame buffer too small");
+    for (size_t i = 0; i < frames.size(); ++i) {
+      std::memcpy(out + fb * i, frames[i].bytes.data() + frames[i].p.off, fb);
+      if (indices) indices[i] = frames[i].index;
+    }
+  });
+}
+
+int trb_format_track_log(const trb_track_log_entry* log, int64_t n, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need((log || n == 0) && len, "null argument");
+    const std::string s = format_track_log(log, n);
+    *len = static_cast<int64_t>(s.size());
+    if (!out) return;
+    if (static_cast<int64_t>(s.size()) + 1 > cap) throw Error(TRB_CAPACITY, "text buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
+int trb_parse_track_log(const char* text, int64_t len, const char* source, trb_track_log_entry* out, int64_t cap,
+                        int64_t* n) {
+  return guard([&] {
+    need(text && n, "null argument");
+    const auto v = parse_track_log(std::string(text, static_cast<size_t>(len)), source ? source : "<memory>");
+    *n = static_cast<int64_t>(v.size());
+    if (!out) return;
+    if (static_cast<int64_t>(v.size()) > cap) throw Error(TRB_CAPACITY, "log buffer too small");
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+int trb_save_track_log(const char* path, const trb_track_log_entry* log, int64_t n) {
+  return guard([&] {  // save_track_log -> detail::spit (textio.hpp:43-48)
+    need(path && (log || n == 0), "null argument");
+    std::ofstream o(path, std::ios::binary);
+    if (!o) throw Error(TRB_IO_ERROR, std::string("cannot write ") + path);
+    o << format_track_log(log, n);
+    if (!o) throw Error(TRB_IO_ERROR, std::string("write failed for ") + path);
+  });
+}
+
+int trb_load_track_log(const char* path, trb_track_log_entry* out, int64_t cap, int64_t* n) {
+  return guard([&] {  // load_track_log -> slurp (textio.hpp:35-41) + parse
+    need(path && n, "null argument");
+    const auto b = slurp_bytes(path);
+    const auto v = parse_track_log(std::string(b.begin(), b.end()), path);
+    *n = static_cast<int64_t>(v.size());
+    if (!out) return;
+    if (static_cast<int64_t>(v.size()) > cap) throw Error(TRB_CAPACITY, "log buffer too small");
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+}  // extern "C"

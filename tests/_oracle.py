@@ -119,6 +119,14 @@ def ref_lib():
         L.ref_warp_frame.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_stream_detect.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                         C.POINTER(MOTION_CFG), C.c_void_p, C.POINTER(C.c_int)]
+        L.ref_decode_pnm.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int), C.c_void_p, C.c_int64]
+        L.ref_load_frame_sequence.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                              C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_format_track_log.restype = C.c_int64
+        L.ref_format_track_log.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64]
+        L.ref_parse_track_log.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_void_p, C.c_int64,
+                                          C.POINTER(C.c_int64)]
         L.ref_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_histogram.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,

@@ -162,6 +162,52 @@ def warp_case(trials: int = 40):
                 outs=np.concatenate(outs), stream_frames=cf, stream_homs=sh, stream_masks=masks)
 
 
+PNM_CASES = [
+    b"P5\n3 2\n255\n" + bytes(range(6)),
+    b"P6 2 2 255 " + bytes(range(12)),
+    b"P5\n# a comment\n  4 1 # trailing\n255\n" + b"abcd",
+    b"P5\t1\r1\x0b255\n\x07extra",
+    b"P2 3 2 255 " + bytes(6),
+    b"P5 3 2 65535 " + bytes(12),
+    b"P5 3x 2 255 " + bytes(6),
+    b"P5 0 2 255 ",
+    b"P5 -3 2 255 ",
+    b"P5 3 2",
+    b"P5 3 2 255 " + bytes(5),
+    b"",
+    b"# only a comment",
+    b"P6 +2 1 255 " + bytes(6),
+    b"P5 99999999999 1 255 ",
+]
+
+
+def io_case():
+    """decode_pnm (frame.hpp:152-175) and the track-log text format
+    (tracking.hpp:247-277) through the reference."""
+    L = O.ref_lib()
+    import ctypes as C
+    dims, px, errs = [], [], []
+    for b in PNM_CASES:
+        buf = np.frombuffer(b, np.uint8) if b else np.zeros(1, np.uint8)
+        w, h, c = C.c_int(0), C.c_int(0), C.c_int(0)
+        out = np.zeros(256, np.uint8)
+        rc = L.ref_decode_pnm(buf.ctypes.data, len(b), b"<memory>", C.byref(w), C.byref(h), C.byref(c),
+                              out.ctypes.data, out.size)
+        if rc:
+            dims.append((0, 0, 0))
+            errs.append(L.ref_last_error().decode())
+            px.append(np.zeros(0, np.uint8))
+        else:
+            dims.append((w.value, h.value, c.value))
+            errs.append("")
+            px.append(out[:w.value * h.value * c.value].copy())
+    log = np.load(os.path.join(HERE, "acceptance6.npz"))["log"]
+    text = C.create_string_buffer(1 << 20)
+    n = L.ref_format_track_log(log.ctypes.data, len(log), text, len(text))
+    return dict(pnm_dims=np.array(dims, np.int32), pnm_pixels=np.concatenate(px), pnm_errors=np.array(errs),
+                log=log, log_text=np.frombuffer(text.raw[:n], np.uint8))
+
+
 def main():
     if not O.ref_available():
         sys.exit("oracle/_ref/libteamrec_ref.so missing: run `make -C oracle` where /root/reference exists")
@@ -170,6 +216,8 @@ def main():
         out["blob_features"] = blob_features_case()
     if "warp" in sys.argv[1:]:  # only the warp_frame / stream_detect fixture
         out["warp"] = warp_case()
+    if "io" in sys.argv[1:]:  # only the PNM / track-log text fixture
+        out["io"] = io_case()
     if out:
         for name, d in out.items():
             np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
@@ -198,6 +246,7 @@ def main():
                              conn=np.array(conns))
     out["blob_features"] = blob_features_case()
     out["warp"] = warp_case()
+    out["io"] = io_case()
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
         print(name, {k: getattr(v, "shape", None) for k, v in d.items()})
