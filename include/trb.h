@@ -294,6 +294,9 @@ int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int64_t* n);
  * [bucket][64] by window size (<5k, <50k, <150k, larger pixels); entry 0 of
  * a bucket counts its iterations (256 entries) */
 int trb_debug_phases(uint64_t* out256);
+/* diagnostics build: per mean-shift CTA [busy ns, last item end
+ * (globaltimer ns)] while the log is on (2048 entries) */
+int trb_debug_cta_times(uint64_t* out2048, int reset);
 
 #ifdef __cplusplus
 }

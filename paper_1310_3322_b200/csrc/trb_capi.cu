@@ -886,6 +886,14 @@ extern "C" int trb_debug_itlog(int enable, int64_t* out_pairs, int64_t cap, int6
   });
 }
 
+extern "C" int trb_debug_cta_times(uint64_t* out2048, int reset) {
+  return guard([&] {
+    need(out2048 != nullptr, "null argument");
+    use_device(0);
+    trb::read_cta_times(reinterpret_cast<unsigned long long*>(out2048), reset != 0);
+  });
+}
+
 extern "C" int trb_debug_phases(uint64_t* out128) {
   return guard([&] {
     need(out128 != nullptr, "null argument");

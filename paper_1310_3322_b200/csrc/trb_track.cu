@@ -16,6 +16,9 @@ __device__ unsigned long long g_phase[256];
 __device__ int g_phase_on;
 __shared__ long long s_ph_last;
 __shared__ int s_ph_bucket;
+__shared__ unsigned long long s_item_t0;
+// per-CTA [busy ns, last item end (globaltimer)] of the mean-shift kernel
+__device__ unsigned long long g_cta_time[2 * 1024];
 }  // namespace trb
 // The device-side instrumentation below compiles only into the diagnostics
 // build (make diag -> libtrb_diag.so, -DTRB_DIAG); the product build has no
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     // ~30k px + window area); 4 buckets per octave, small index = costly.
     // Split-class tracks go after every cluster-class one.
     const unsigned cost =
-        static_cast<unsigned>(max(1, d.iters[g])) * static_cast<unsigned>(30000 + max(1, d.w[g] * d.h[g]));
+        static_cast<unsigned>(max(d.iter_floor, d.iters[g])) * static_cast<unsigned>(30000 + max(1, d.w[g] * d.h[g]));
     const int lz = __clz(cost);
     const int sub = lz <= 29 ? static_cast<int>((cost >> (29 - lz)) & 3u) : 0;
     return (split_class(d, g) ? 128 : 0) + 4 * lz + (3 - sub);
@@ -1123,6 +1126,13 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
     const int q = sm.iscal[11];
     __syncthreads();
     if (q < 0) break;
+#ifdef TRB_DIAG
+    if (g_phase_on && threadIdx.x == 0) {  // per-CTA busy time and finish time (globaltimer ns)
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      s_item_t0 = t0;
+    }
+#endif
     bool to_split = false;
     if (!split) {
       const int item = d.work[q];
@@ -1131,6 +1141,14 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
       to_split = split_class(d, g);  // read before the leader updates iters
     }
     meanshift_item(d, q, sm, cur_scr, (split || rank == 0) && threadIdx.x == 0);
+#ifdef TRB_DIAG
+    if (g_phase_on && threadIdx.x == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      atomicAdd(&g_cta_time[2 * blockIdx.x], t1 - s_item_t0);
+      atomicMax(&g_cta_time[2 * blockIdx.x + 1], t1);
+    }
+#endif
     if (to_split) {  // every later item is split-class too
       split = true;
       sm.grp = Grp::single();
@@ -1414,6 +1432,14 @@ void enable_itlog(bool on) {
   if (on) TRB_CUDA(cudaMemcpyToSymbol(g_phase, zz, sizeof(zz)));
 }
 
+void read_cta_times(unsigned long long* out2048, bool reset) {
+  TRB_CUDA(cudaMemcpyFromSymbol(out2048, g_cta_time, 2048 * sizeof(*out2048)));
+  if (reset) {
+    std::vector<unsigned long long> z(2048, 0);
+    TRB_CUDA(cudaMemcpyToSymbol(g_cta_time, z.data(), 2048 * sizeof(unsigned long long)));
+  }
+}
+
 void read_phases(unsigned long long* out128) {
   TRB_CUDA(cudaMemcpyFromSymbol(out128, g_phase, 256 * sizeof(*out128)));
 }
@@ -1581,6 +1607,8 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     // its cluster's scratch
     const char* es = getenv("TRB_SPLIT_US");
     d_.split_us = es ? atof(es) : 300.0;
+    const char* ef = getenv("TRB_ITER_FLOOR");
+    d_.iter_floor = ef ? std::max(1, atoi(ef)) : 6;  // iteration history is noisy: order mostly by area
     d_.G = G;
     if (getenv("TRB_VERBOSE"))
       fprintf(stderr, "[trb] tracker: %d clusters of %d CTAs, split below %.0f us, %zu B dynamic smem per CTA\n",

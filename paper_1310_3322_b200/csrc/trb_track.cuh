@@ -57,6 +57,7 @@ struct TrackDev {
   int32_t* work_n;
   int32_t* work_head;
   int G;               // CTAs per cluster
+  int iter_floor;      // scheduling: iterations assumed at least
   double split_us;     // tracks estimated below this (single-CTA us) run in split mode
   // per-cluster scratch (breakpoint list, partitioned weights, bin cache)
   unsigned char* scratch;
@@ -117,4 +118,5 @@ int* enable_progress(int n_ctas);
 void enable_itlog(bool on);
 int64_t read_itlog(long long* out, int64_t cap);
 void read_phases(unsigned long long* out128);
+void read_cta_times(unsigned long long* out2048, bool reset);
 }  // namespace trb
