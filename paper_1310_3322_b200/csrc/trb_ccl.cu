@@ -14,11 +14,14 @@
 // (popcount of the bits to the left).  `n_blocks` never changes the output.
 //
 // Kernels (grid.z or grid.y = stream):
-//   ccl_local    32x32 tile in shared memory: union-find (atomicMin, root =
-//                smallest local index = raster-first pixel), per tile
-//                component stats (area, bbox, sum x, sum y), one global slot
-//                per tile component; labg[p] = slot for foreground pixels
-//   ccl_merge    unions across tile seams on the slot union-find
+//   ccl_occupancy one warp per 32x32 tile: tiles holding foreground are
+//                appended to a compact list
+//   ccl_local    per listed tile (persistent CTAs): run-based union-find in
+//                shared memory (root = smallest local index = raster-first
+//                pixel), per tile component stats (area, bbox, sum x,
+//                sum y), one global slot per tile component; labg[p] = slot
+//                for foreground pixels
+//   ccl_merge    unions across the seams of listed tiles (slot union-find)
 //   ccl_resolve  slot -> set root; stats of non-root slots atomically
 //                folded into their root
 //   ccl_mark     surviving roots: bitmap bit + per-row count
@@ -117,6 +120,31 @@ __device__ __forceinline__ int run_start_at(uint32_t starts, int p) {  // start 
   return 31 - __clz(x);
 }
 
+// Tiles holding foreground: one warp per 32x32 tile (lane = row, 32 bytes
+// per lane), appended to a compact list that the local and seam kernels
+// walk — most of a frame is background (C5: ~8 % foreground).
+__global__ void __launch_bounds__(256) ccl_occupancy_kernel(CclArgs a, int vec_ok) {
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tiles) return;
+  const int s = blockIdx.y;
+  const int tile = s * n_tiles + t;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int gy = ty * kTileH + lane, gx0 = tx * kTileW;
+  bool any = false;
+  if (gy < a.h) {
+    const uint8_t* row = a.mask + static_cast<int64_t>(s) * a.px + static_cast<int64_t>(gy) * a.w + gx0;
+    if (vec_ok && gx0 + kTileW <= a.w) {
+      const uint4 q0 = reinterpret_cast<const uint4*>(row)[0], q1 = reinterpret_cast<const uint4*>(row)[1];
+      any = (q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w) != 0;
+    } else {
+      for (int c = 0; c < kTileW && gx0 + c < a.w; ++c) any |= row[c] != 0;
+    }
+  }
+  if (__any_sync(0xffffffffu, any) && lane == 0) a.tile_list[atomicAdd(a.tile_count, 1)] = static_cast<int>(tile);
+}
+
 __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   __shared__ int lab[kTilePx];
   __shared__ int cid[kTilePx];  // compact component id of each local root
@@ -125,11 +153,16 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
       st_y1[kMaxTileComps], st_sx[kMaxTileComps], st_sy[kMaxTileComps];
   __shared__ int n_comp, slot_base_id;
 
-  const int s = blockIdx.z;
+  const int n_list = *a.tile_count;
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  for (int it = blockIdx.x; it < n_list; it += gridDim.x) {
+  const int tile = a.tile_list[it];
+  const int s = tile / n_tiles, tl = tile - s * n_tiles;
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
-  const int tx0 = blockIdx.x * kTileW, ty0 = blockIdx.y * kTileH;
+  const int tx0 = (tl % a.tiles_x) * kTileW, ty0 = (tl / a.tiles_x) * kTileH;
   const int w = threadIdx.x >> 5, c = threadIdx.x & 31, gx = tx0 + c;
+  __syncthreads();  // the previous tile is done with the shared arrays
   if (threadIdx.x == 0) n_comp = 0;
 
   // 1. rows as bit masks
@@ -144,8 +177,7 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
     mine |= static_cast<uint32_t>(fg) << rr;
     any |= fg;
   }
-  // most tiles are pure background: leave at once
-  if (!__syncthreads_or(any)) return;
+  if (!__syncthreads_or(any)) continue;  // (listed tiles hold foreground)
 
   // 2. run starts are the union-find nodes
 #pragma unroll
@@ -245,16 +277,12 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
     t.sy[slot] = static_cast<unsigned long long>(st_sy[id]);
     t.minpix[slot] = (ty0 + r) * a.w + gx;
   }
+  }  // tile loop
 }
 
 // ------------------------------------------------------------------ merge
 // One thread per tile-seam pixel: 32 top-seam + 32 left-seam per tile.
-__global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
-  const int s = blockIdx.y;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t n_tiles = static_cast<int64_t>(a.tiles_x) * a.tiles_y;
-  if (gid >= n_tiles * 64) return;
-  const int tile = static_cast<int>(gid >> 6), j = static_cast<int>(gid & 63);
+__device__ __forceinline__ void ccl_merge_one(const CclArgs& a, int s, int tile, int j) {
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   const int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
@@ -283,6 +311,19 @@ __global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
       if (y > 0 && fgat(x - 1, y - 1)) gunion(parent, me, sl(x - 1, y - 1));
       if (y + 1 < h && fgat(x - 1, y + 1)) gunion(parent, me, sl(x - 1, y + 1));
     }
+  }
+}
+
+// Only listed (foreground) tiles can own a seam union: the pixel below /
+// right of the seam must be foreground.  Grid-stride over list x 64.
+__global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
+  const int64_t total = static_cast<int64_t>(*a.tile_count) * 64;
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  for (int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gid < total;
+       gid += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int lt = a.tile_list[gid >> 6];
+    const int s = lt / n_tiles, tile = lt - s * n_tiles;
+    ccl_merge_one(a, s, tile, static_cast<int>(gid & 63));
   }
 }
 
@@ -432,9 +473,15 @@ int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   TRB_CUDA(cudaMemsetAsync(a.nslots, 0, sizeof(int32_t) * S, st));
   TRB_CUDA(cudaMemsetAsync(a.rowcount, 0, sizeof(int32_t) * static_cast<size_t>(a.h) * S, st));
   TRB_CUDA(cudaMemsetAsync(a.bitmap, 0, sizeof(uint32_t) * static_cast<size_t>(a.h) * a.wpr * S, st));
-  ccl_local_kernel<<<dim3(a.tiles_x, a.tiles_y, S), 256, 0, st>>>(a);
+  TRB_CUDA(cudaMemsetAsync(a.tile_count, 0, sizeof(int32_t), st));
+  const int vec_occ = (a.w % 16 == 0);
+  ccl_occupancy_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 32, 256)), S), 256, 0, st>>>(a, vec_occ);
+  TRB_LAUNCH_CHECK("ccl_occupancy_kernel");
+  // persistent CTAs over the foreground-tile list (count known on the device)
+  const unsigned list_ctas = static_cast<unsigned>(std::min<int64_t>(n_tiles * S, 148 * 8));
+  ccl_local_kernel<<<list_ctas, 256, 0, st>>>(a);
   TRB_LAUNCH_CHECK("ccl_local_kernel");
-  ccl_merge_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 64, 256)), S), 256, 0, st>>>(a);
+  ccl_merge_kernel<<<list_ctas, 256, 0, st>>>(a);
   TRB_LAUNCH_CHECK("ccl_merge_kernel");
   // slot kernels: enough CTAs to cover a typical frame, grid-stride beyond
   const unsigned slot_blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div64(a.slot_cap, 256), 64));
@@ -449,7 +496,7 @@ int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   const int vec_ok = (a.px % 16 == 0);
   ccl_final_kernel<<<dim3(static_cast<unsigned>(ceil_div64(ceil_div64(a.px, 16), 256)), S), 256, 0, st>>>(a, vec_ok);
   TRB_LAUNCH_CHECK("ccl_final_kernel");
-  return 7;
+  return 8;
 }
 
 }  // namespace trb

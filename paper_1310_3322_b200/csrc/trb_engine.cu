@@ -142,6 +142,7 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   bitmap_.alloc(sizeof(uint32_t) * static_cast<size_t>(h) * wpr * S);
   blobs_.alloc(sizeof(trb_blob) * blob_cap_ * S, false);
   nblobs_.alloc(sizeof(int32_t) * S);
+  tiles_.alloc(sizeof(int32_t) * (static_cast<size_t>(tx) * ty * S + 1), false);
 
   CclArgs& a = args_;
   a.labg = labg_.as<int32_t>();
@@ -176,6 +177,8 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   a.blobs = blobs_.as<trb_blob>();
   a.blob_cap = blob_cap_;
   a.nblobs = nblobs_.as<int32_t>();
+  a.tile_count = tiles_.as<int32_t>();
+  a.tile_list = a.tile_count + 1;
 }
 
 void CclState::run(const uint8_t* mask, cudaStream_t st, int* launches) {

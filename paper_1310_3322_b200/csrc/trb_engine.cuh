@@ -96,7 +96,7 @@ class CclState {
   CclArgs args_{};
   int S_, w_, h_;
   int64_t px_, slot_cap_, blob_cap_;
-  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_, nblobs_;
+  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_, nblobs_, tiles_;
 };
 
 class TrackerState;  // trb_track.cu

@@ -81,6 +81,8 @@ struct CclArgs {
   trb_blob* blobs;      // [S][blob_cap]
   int64_t blob_cap;
   int32_t* nblobs;      // [S]
+  int32_t* tile_list;   // [S * tiles] tiles holding foreground (s * tiles + ty * tiles_x + tx)
+  int32_t* tile_count;  // [1]
 };
 
 // Launches the full CCL + blob-statistics chain; returns launches issued.
