@@ -34,11 +34,16 @@ namespace trb {
 
 namespace {
 
-__device__ __forceinline__ int sfind(const int* lab, int i) {
+// find with path halving: every visited node is re-pointed at its
+// grandparent (values only move towards the root, so racing writers are
+// harmless and later finds walk shorter chains)
+__device__ __forceinline__ int sfind(int* lab, int i) {
   int p = lab[i];
   while (p != i) {
+    const int gp = lab[p];
+    if (gp != p) lab[i] = gp;
     i = p;
-    p = lab[i];
+    p = gp;
   }
   return i;
 }
