@@ -297,6 +297,7 @@ def ours_main(args, rank, world, local_rank):
         st.step_device(ptrs[t], stream.cuda_stream)
         launches += st.last_launches
         t += 1
+    st.join(stream.cuda_stream)  # the last step's tracking (internal stream) is inside the timed region
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

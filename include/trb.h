@@ -197,8 +197,16 @@ int trb_streams_create(int n_streams, int width, int height, int channels, const
                        const trb_seg_config* sc, const trb_tracker_config* tc, int device, trb_streams** out);
 int trb_streams_destroy(trb_streams* s);
 /* frames: host array of n_streams DEVICE pointers (w*h*channels bytes each).
- * cuda_stream: cudaStream_t to launch on (NULL = the handle's own). */
+ * cuda_stream: cudaStream_t to launch on (NULL = the handle's own).
+ * Step overlap: motion + CCL of a step run on cuda_stream; its tracking runs
+ * on the handle's internal stream and overlaps the NEXT step's motion + CCL.
+ * cuda_stream covers all work up to the previous step's tracking;
+ * trb_streams_join makes a stream wait for everything issued so far
+ * (trb_streams_synchronize and the download calls wait for everything).
+ * The frames must stay valid until the step's tracking has run. */
 int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* cuda_stream);
+/* cuda_stream waits (on the device) for every step issued so far. */
+int trb_streams_join(trb_streams* s, void* cuda_stream);
 /* step_device for MotionConfig::warp = homography: every frame is warped
  * into the reference plane (warp_frame, motion.hpp:81-119) by its
  * homography (homographies: host, n_streams * 9 doubles, row-major) before
@@ -212,7 +220,7 @@ int trb_streams_step_device_warp(trb_streams* s, const uint8_t* const* frames, c
  * receives n_streams int32 blob counts (the D2H read of the step). */
 int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t* result_host, void* cuda_stream);
 /* Pipelined step_host: returns once the work is queued.  The frames' H2D
- * copy runs on the handle's copy stream into one of two staging buffers and
+ * copy runs on the handle's copy stream into one of three staging buffers and
  * overlaps the previous step's kernels; result_host (if not NULL) is written
  * when cuda_stream reaches this step.  frames and result_host must stay
  * valid until trb_streams_synchronize (or a later synchronous call). */

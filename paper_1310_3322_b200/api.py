@@ -133,6 +133,7 @@ def _declare(L):
         "trb_extract_blob_features": [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp],
         "trb_streams_blob_features": [vp, i32, vp, vp, vp, i32, C.POINTER(C.c_int)],
         "trb_streams_synchronize": [vp],
+        "trb_streams_join": [vp, vp],
         "trb_streams_frames_seen": [vp, C.POINTER(C.c_int)],
         "trb_streams_has_output": [vp, C.POINTER(C.c_int)],
         "trb_streams_download_mask": [vp, i32, vp],
@@ -498,6 +499,12 @@ class Streams:
     def synchronize(self) -> None:
         _check(lib().trb_streams_synchronize(self._h))
 
+    def join(self, cuda_stream: int = 0) -> None:
+        """Make cuda_stream wait (on the device) for every step issued so far
+        (a step's tracking overlaps the next step's motion + CCL on an
+        internal stream; trb_streams_join)."""
+        _check(lib().trb_streams_join(self._h, C.c_void_p(cuda_stream)))
+
     @property
     def has_output(self) -> bool:
         v = C.c_int(0)
@@ -576,7 +583,7 @@ def synth_raster(out_device_ptr: int, width: int, height: int, channels: int, ba
 
 STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints", "osum_elements",
               "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced",
-              "", "meanshift_window_px", "", "", "", "",
+              "", "meanshift_window_px", "fast_warps", "", "general_warps", "",
               "bad_scan_merge", "bad_phaseB_merge", "bad_bp_overflow", "bad_cross_cta", "bad_fold_carry",
               "bad_fold_merge", "bad_verify_start", "bad_verify_end", "bad_final_start", "bad_final_end",
               "many_bp_centroid", "many_bp_total", "many_bp_bin", "max_bp")

@@ -546,6 +546,14 @@ int trb_streams_step_device(trb_streams* s, const uint8_t* const* frames, void* 
   });
 }
 
+int trb_streams_join(trb_streams* s, void* cuda_stream) {
+  return guard([&] {
+    need(s != nullptr, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->join(static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
 int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t* result_host, void* cuda_stream) {
   return guard([&] {
     need(s && frames, "null argument");
@@ -717,7 +725,7 @@ int trb_streams_blob_features(trb_streams* s, int stream, const uint8_t* frame_d
     need(stream >= 0 && stream < s->s->S(), "stream index out of range");
     TRB_CUDA(cudaSetDevice(s->device));
     trb::Streams& st = *s->s;
-    TRB_CUDA(cudaStreamSynchronize(st.stream()));
+    TRB_CUDA(cudaDeviceSynchronize());
     int32_t nb = 0;
     if (st.has_output())
       TRB_CUDA(cudaMemcpy(&nb, st.ccl().nblobs() + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));

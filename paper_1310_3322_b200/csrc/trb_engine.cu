@@ -140,8 +140,10 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   nslots_.alloc(sizeof(int32_t) * S);
   rowcount_.alloc(sizeof(int32_t) * h * S);
   bitmap_.alloc(sizeof(uint32_t) * static_cast<size_t>(h) * wpr * S);
-  blobs_.alloc(sizeof(trb_blob) * blob_cap_ * S, false);
-  nblobs_.alloc(sizeof(int32_t) * S);
+  for (int b = 0; b < 2; ++b) {
+    blobs_[b].alloc(sizeof(trb_blob) * blob_cap_ * S, false);
+    nblobs_[b].alloc(sizeof(int32_t) * S);
+  }
   tiles_.alloc(sizeof(int32_t) * (static_cast<size_t>(tx) * ty * S + 1), false);
 
   CclArgs& a = args_;
@@ -174,16 +176,18 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   a.rowcount = rowcount_.as<int32_t>();
   a.bitmap = bitmap_.as<uint32_t>();
   a.wpr = wpr;
-  a.blobs = blobs_.as<trb_blob>();
   a.blob_cap = blob_cap_;
-  a.nblobs = nblobs_.as<int32_t>();
   a.tile_count = tiles_.as<int32_t>();
   a.tile_list = a.tile_count + 1;
 }
 
 void CclState::run(const uint8_t* mask, cudaStream_t st, int* launches) {
+  const int b = cur_ ^ 1;
   args_.mask = mask;
+  args_.blobs = blobs_[b].as<trb_blob>();
+  args_.nblobs = nblobs_[b].as<int32_t>();
   *launches += launch_ccl(args_, S_, st);
+  cur_ = b;
 }
 
 // ----------------------------------------------------------------- streams
@@ -208,9 +212,15 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   for (int i = 0; i < kStages + 1; ++i) TRB_CUDA(cudaEventCreate(&prof_ev_[i]));
   TRB_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
   TRB_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
+  TRB_CUDA(cudaStreamCreateWithFlags(&trk_, cudaStreamNonBlocking));
+  if (const char* e = getenv("TRB_OVERLAP")) overlap_ = atoi(e) != 0;
+  for (int i = 0; i < kStaging; ++i) {
     TRB_CUDA(cudaEventCreateWithFlags(&copied_[i], cudaEventDisableTiming));
     TRB_CUDA(cudaEventCreateWithFlags(&consumed_[i], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < 2; ++i) {
+    TRB_CUDA(cudaEventCreateWithFlags(&ccl_ev_[i], cudaEventDisableTiming));
+    TRB_CUDA(cudaEventCreateWithFlags(&trk_ev_[i], cudaEventDisableTiming));
   }
 }
 
@@ -219,10 +229,15 @@ Streams::~Streams() {
     if (e) cudaEventDestroy(e);
   for (auto& e : prof_ev_)
     if (e) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kStaging; ++i) {
     if (copied_[i]) cudaEventDestroy(copied_[i]);
     if (consumed_[i]) cudaEventDestroy(consumed_[i]);
   }
+  for (int i = 0; i < 2; ++i) {
+    if (ccl_ev_[i]) cudaEventDestroy(ccl_ev_[i]);
+    if (trk_ev_[i]) cudaEventDestroy(trk_ev_[i]);
+  }
+  if (trk_) cudaStreamDestroy(trk_);
   if (copy_) cudaStreamDestroy(copy_);
   if (own_) cudaStreamDestroy(own_);
 }
@@ -233,18 +248,47 @@ void Streams::set_profiling(bool on) {
   prof_steps_ = 0;
 }
 
-void Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st) {
+// Step overlap.  Motion and CCL of step t+1 do not depend on the tracker of
+// step t (only step t+1's tracker does), so with `overlap` the tracker runs
+// on the internal stream trk_ behind an event of this step's CCL, and the
+// caller's stream goes on to the next step's motion + CCL while it runs.
+// Hazards: CCL(t+1) writes the other blob table (double-buffered) and waits
+// for the tracker that last read it (step t-1); at the end of step t the
+// caller's stream also waits for the tracker of step t-1 (a lag-one join,
+// which costs no overlap: that tracker ended before step t's began), so the
+// caller's stream trails the issued work by at most one tracker — join()
+// closes it.  `done` (frames released) is recorded after the tracker.
+cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bool overlap, cudaEvent_t done) {
   int launches = 0;
+  overlap = overlap && tracker_ && !profiling_;
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[0], st));
   const bool emitted = motion_->push(frames_dev, mask_.as<uint8_t>(), mask_tmp_.as<uint8_t>(), st, &launches);
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[1], st));
-  if (emitted) ccl_->run(mask_.as<uint8_t>(), st, &launches);
+  const int b = ccl_->next_buffer();
+  if (emitted) {
+    if (trk_pending_[b]) TRB_CUDA(cudaStreamWaitEvent(st, trk_ev_[b], 0));  // its last reader
+    ccl_->run(mask_.as<uint8_t>(), st, &launches);
+  }
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[2], st));
-  if (emitted && tracker_)
-    tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches,
-                      profiling_ ? prof_ev_[3] : nullptr);
-  else if (profiling_)
-    TRB_CUDA(cudaEventRecord(prof_ev_[3], st));
+  if (emitted && tracker_ && overlap) {
+    TRB_CUDA(cudaEventRecord(ccl_ev_[b], st));
+    TRB_CUDA(cudaStreamWaitEvent(trk_, ccl_ev_[b], 0));
+    tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), trk_, &launches,
+                      nullptr);
+    TRB_CUDA(cudaEventRecord(trk_ev_[b], trk_));
+    trk_pending_[b] = true;
+    last_trk_ = b;
+    if (trk_pending_[b ^ 1]) TRB_CUDA(cudaStreamWaitEvent(st, trk_ev_[b ^ 1], 0));  // lag-one join
+    if (done) TRB_CUDA(cudaEventRecord(done, trk_));
+  } else {
+    if (last_trk_ >= 0) join(st), last_trk_ = -1;  // back to in-stream tracking (profiling, warp mode)
+    if (emitted && tracker_)
+      tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches,
+                        profiling_ ? prof_ev_[3] : nullptr);
+    else if (profiling_)
+      TRB_CUDA(cudaEventRecord(prof_ev_[3], st));
+    if (done) TRB_CUDA(cudaEventRecord(done, st));
+  }
   if (profiling_) {
     TRB_CUDA(cudaEventRecord(prof_ev_[4], st));
     TRB_CUDA(cudaEventSynchronize(prof_ev_[4]));
@@ -257,6 +301,12 @@ void Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st) {
   }
   has_output_ = emitted;
   last_launches_ = launches;
+  return (overlap && emitted) ? trk_ : st;
+}
+
+void Streams::join(cudaStream_t st) {
+  if (!st) st = own_;
+  if (last_trk_ >= 0) TRB_CUDA(cudaStreamWaitEvent(st, trk_ev_[last_trk_], 0));
 }
 
 const uint8_t* const* Streams::upload_ptrs_(const uint8_t* const* frames, cudaStream_t st) {
@@ -289,9 +339,9 @@ void Streams::step_device_warp(const uint8_t* const* frames, const double* h9s, 
   for (int s = 0; s < S_; ++s) homography_inverse(h9s + 9 * s, ih + 9 * s);
   double* id = invs_dev_.as<double>() + static_cast<size_t>(slot) * 9 * S_;
   TRB_CUDA(cudaMemcpyAsync(id, ih, sizeof(double) * 9 * S_, cudaMemcpyHostToDevice, st));
+  // no overlap: the next step's warp rewrites the plane this tracker reads
   launch_warp_frames(dp, warp_buf_.as<uint8_t>(), static_cast<int64_t>(fb), id, w_, h_, ch_, S_, st);
-  run_(warp_ptrs_.as<const uint8_t*>(), st);
-  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
+  run_(warp_ptrs_.as<const uint8_t*>(), st, false, slot_ev_[slot]);
 }
 
 void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
@@ -299,8 +349,7 @@ void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
   if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(frames, st);
-  run_(dp, st);
-  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
+  run_(dp, st, overlap_, slot_ev_[slot]);
 }
 
 namespace {
@@ -328,10 +377,10 @@ void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host
   if (!st) st = own_;
   if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const size_t fb = static_cast<size_t>(px_) * ch_;
-  const int b = host_step_++ & 1;
+  const int b = host_step_++ % kStaging;
   if (!staging_[b].p) staging_[b].alloc(fb * S_, false);
   uint8_t* stage = staging_[b].as<uint8_t>();
-  // the copy may start once the step two back (same buffer) is done with it
+  // the copy may start once the step kStaging back (same buffer) is done with it
   TRB_CUDA(cudaStreamWaitEvent(copy_, consumed_[b], 0));
   for (int s = 0; s < S_; ++s)
     TRB_CUDA(cudaMemcpyAsync(stage + fb * s, frames[s], fb, cudaMemcpyHostToDevice, copy_));
@@ -341,9 +390,8 @@ void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(dev.data(), st);
   TRB_CUDA(cudaStreamWaitEvent(st, copied_[b], 0));
-  run_(dp, st);
-  TRB_CUDA(cudaEventRecord(slot_ev_[slot], st));
-  TRB_CUDA(cudaEventRecord(consumed_[b], st));  // tracking read the frames too
+  const cudaStream_t last_reader = run_(dp, st, overlap_, slot_ev_[slot]);
+  TRB_CUDA(cudaEventRecord(consumed_[b], last_reader));  // tracking read the frames too
   if (result_host) {
     const size_t rb = sizeof(int32_t) * S_;
     if (!has_output_) {

@@ -85,10 +85,14 @@ class CclState {
  public:
   CclState(int S, int w, int h, const trb_seg_config& cfg);
   // mask: device [S][px].  Labels, blobs and counts stay on the device.
+  // The blob table is double-buffered: run() writes the buffer the previous
+  // run did not, so a tracker may still read the last table while the next
+  // frame is labelled.  blobs()/nblobs() = the table of the latest run.
   void run(const uint8_t* mask, cudaStream_t st, int* launches);
   int32_t* labels() const { return labels_.as<int32_t>(); }
-  trb_blob* blobs() const { return blobs_.as<trb_blob>(); }
-  int32_t* nblobs() const { return nblobs_.as<int32_t>(); }
+  trb_blob* blobs() const { return blobs_[cur_].as<trb_blob>(); }
+  int32_t* nblobs() const { return nblobs_[cur_].as<int32_t>(); }
+  int next_buffer() const { return cur_ ^ 1; }
   int64_t blob_cap() const { return blob_cap_; }
   int64_t px() const { return px_; }
 
@@ -96,7 +100,8 @@ class CclState {
   CclArgs args_{};
   int S_, w_, h_;
   int64_t px_, slot_cap_, blob_cap_;
-  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_, nblobs_, tiles_;
+  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_[2], nblobs_[2], tiles_;
+  int cur_ = 0;
 };
 
 class TrackerState;  // trb_track.cu
@@ -119,6 +124,10 @@ class Streams {
   // buffers; result_host is written when `st` reaches this step (valid after
   // synchronize()); frames_host must stay untouched until then.
   void step_host_async(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
+  // Make `st` wait for every step issued so far (the tracker of the last
+  // step runs on an internal stream; see run_).
+  void join(cudaStream_t st);
+  void set_overlap(bool on) { overlap_ = on; }
   cudaStream_t stream() const { return own_; }
   int S() const { return S_; }
   int w() const { return w_; }
@@ -139,7 +148,11 @@ class Streams {
 
  private:
   static constexpr int kPtrSlots = 16;
-  void run_(const uint8_t* const* frames_dev, cudaStream_t st);
+  static constexpr int kStaging = 3;  // host-path staging ring (step t's tracker reads its frames during t+1)
+  // frames_dev stays valid until `done` (an event recorded after the last
+  // read of the frames: the tracker's stream when it overlaps)
+  // returns the stream of the frames' last reader
+  cudaStream_t run_(const uint8_t* const* frames_dev, cudaStream_t st, bool overlap, cudaEvent_t done);
   const uint8_t* const* upload_ptrs_(const uint8_t* const* frames, cudaStream_t st);
   int S_, w_, h_, ch_;
   int64_t px_;
@@ -147,12 +160,19 @@ class Streams {
   std::unique_ptr<MotionState> motion_;
   std::unique_ptr<CclState> ccl_;
   std::unique_ptr<TrackerState> tracker_;
-  DevBuf mask_, mask_tmp_, frame_ptrs_, staging_[2];
+  DevBuf mask_, mask_tmp_, frame_ptrs_, staging_[kStaging];
+  // step overlap: the tracker of step t runs on trk_ while motion + CCL of
+  // step t+1 run on the caller's stream (blob tables double-buffered)
+  cudaStream_t trk_ = nullptr;
+  cudaEvent_t ccl_ev_[2] = {}, trk_ev_[2] = {};
+  bool trk_pending_[2] = {false, false};
+  int last_trk_ = -1;
+  bool overlap_ = true;  // TRB_OVERLAP=0 disables (A/B)
   DevBuf warp_buf_, warp_ptrs_, invs_dev_;  // warped frames, their pointer table, inverses [slot][S][9]
   PinnedBuf invs_host_;
   PinnedBuf result_pinned_;
   cudaStream_t copy_ = nullptr;
-  cudaEvent_t copied_[2] = {}, consumed_[2] = {};
+  cudaEvent_t copied_[kStaging] = {}, consumed_[kStaging] = {};
   int host_step_ = 0;
   PinnedBuf ptrs_host_;
   cudaStream_t own_ = nullptr;

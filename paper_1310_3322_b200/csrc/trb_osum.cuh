@@ -61,7 +61,10 @@ namespace trb {
 
 namespace cg = cooperative_groups;
 
-constexpr int kOsumThreads = 256;
+#ifndef TRB_NT
+#define TRB_NT 256
+#endif
+constexpr int kOsumThreads = TRB_NT;
 constexpr int kOsumBpRecs = 240;  // breakpoint records per CTA (all lanes)
 constexpr int kMaxCluster = 16;
 constexpr int kMaxSegs = 256;     // segments (histogram bins) per run
@@ -435,7 +438,89 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
 #pragma unroll
   for (int l = 0; l < L; ++l)
     pc[l] = piece_identity(), hadbp[l] = 0, firstbp[l] = -1, hi[l] = -1.0, M[l] = 1.0, ea[l] = 0;
+  // Segment heads.  The state at a segment start (element 0 of a plain run)
+  // is exactly +0, so the thread owning that element sums from there to the
+  // next start / its chunk end with real IEEE adds — the exact sequential
+  // prefix — and records it as ONE breakpoint (value = that sum, piece =
+  // its steps before the start).  The replay's S = +0 + sum reproduces the
+  // state; no step of a head is classified (a young sum crosses a binade
+  // every few elements, which made the owning thread the cluster's slowest).
+  bool inhead = false;
+  int hj = 0, hseg = 0;
+  double Sh[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) Sh[l] = 0.0;
+  auto emit_head = [&]() {
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const int idx = atomicAdd(&s.nbp[l], 1);
+      if (idx < cap_lane) {
+        OsumBp& b = s.bp[l * cap_lane + idx];
+        b.p = pc[l];
+        b.v = Sh[l];
+        b.j = hj;
+        b.t = static_cast<short>(t);
+        b.first = static_cast<char>(!hadbp[l]);
+        b.start = static_cast<char>(SEG);
+        b.seg = hseg;
+        if (!hadbp[l]) firstbp[l] = idx;
+      } else {
+        tover = 1;
+      }
+      hadbp[l] = 1;
+      pc[l] = piece_identity();
+      hi[l] = -1.0;
+    }
+  };
+  // Chunk-armed fast walk.  When the chunk holds no segment start and, for
+  // every lane, the approximate prefixes before its first step (xP) and
+  // after its last (xP + aP, same error budget) lie inside one binade with
+  // the 2*delta margins, every step of the chunk is safe in that binade (the
+  // true sums are monotone in between): no per-step prefix or compare, the
+  // piece is the composition of the add / tie steps (osum_step_safe).  The
+  // decision is per warp (all lanes fast or none).
+  bool done = false;
+#ifndef TRB_FASTWALK
+#define TRB_FASTWALK 1
+#endif
   {
+    bool fast = TRB_FASTWALK && af == 0 && j0 < j1 && !(j0 == 0 && !SEG);
+    double Mf[L];
+    int ef[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const double Pe = xadd(xP[l], aP[l]);
+      const long long bp_ = __double_as_longlong(xP[l]), bn_ = __double_as_longlong(Pe);
+      const int eb = static_cast<int>(bp_ >> 52);
+      fast = fast && xP[l] > 0.0 && eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 &&
+             (bp_ & kMant) >= lowm && (bn_ & kMant) <= highm;
+      Mf[l] = osum_pow2(eb - 1023);
+      ef[l] = eb - 1023;
+    }
+    // warp-uniform: a warp whose lanes split between the two walks would
+    // execute both loops one after the other
+    fast = __all_sync(0xffffffffu, fast);
+    if (stats && (t & 31) == 0) atomicAdd(&stats[fast ? 12 : 14], 1ull);
+    if (fast) {
+      // every step is safe in binade ef: ties compose into the piece
+      auto cur = src.begin(j0, gt, C, GT);
+      for (int jb = j0; jb < j1; jb += Src::kUnroll)
+#pragma unroll
+        for (int k = 0; k < Src::kUnroll; ++k) {
+          const int j = jb + k;
+          if (j >= j1) break;
+          bool start, has;
+          int seg;
+          double v[L];
+          cur.next(k, start, seg, has, v);
+          if (!has) continue;
+#pragma unroll
+          for (int l = 0; l < L; ++l) osum_step_safe(pc[l], v[l], Mf[l], ef[l], tbad);
+        }
+      done = true;
+    }
+  }
+  if (!done) {
     double P[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) P[l] = xP[l];
@@ -452,6 +537,18 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       cur.next(k, start, seg, has, v);
       TRB_OSUM_WALK_FIRST(j == j0, v[0]);
       TRB_OSUM_ELEM_TRACE(j - j0, v[0]);
+      if (SEG ? start : j == 0) {  // a segment head begins (S = +0 exactly)
+        if (inhead) emit_head();
+        inhead = true, hj = j, hseg = seg;
+#pragma unroll
+        for (int l = 0; l < L; ++l) Sh[l] = 0.0;
+      }
+      if (inhead) {
+        if (has)
+#pragma unroll
+          for (int l = 0; l < L; ++l) Sh[l] = xadd(Sh[l], v[l]);
+        continue;
+      }
       if (SEG && start)
 #pragma unroll
         for (int l = 0; l < L; ++l) P[l] = 0.0;
@@ -509,6 +606,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         }
       }
     }
+    if (inhead) emit_head();
   }
   TRB_OSUM_WALK_END();
   TRB_OSUM_MARK(4);

@@ -145,3 +145,33 @@ def test_streams_warp_matches_reference_stream_detect(gpu):
     assert len(masks) == len(g["stream_masks"])
     for (m0, m1), ref in zip(masks, g["stream_masks"]):
         assert m0.tobytes() == ref.tobytes() and m1.tobytes() == ref.tobytes()
+
+
+def test_streams_overlapped_steps_without_sync(gpu):
+    """The bench's issue pattern: device-resident C5 steps enqueued back to
+    back on a user stream with no host sync (each step's tracking overlaps
+    the next step's motion + CCL on the internal stream; blob tables
+    double-buffered), then join(): track logs equal the oracle's and the
+    in-stream (TRB_OVERLAP=0) run's."""
+    import torch
+    clips = [recipe("C5", s) for s in (5, 6)]
+    n = 100
+    frames = [O.orc_frames(c, n)[0] for c in clips]
+    dev = [torch.from_numpy(f).cuda() for f in frames]
+    logs = {}
+    for ov in ("1", "0"):
+        os.environ["TRB_OVERLAP"] = ov
+        try:
+            st = gpu.Streams(2, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+        finally:
+            os.environ.pop("TRB_OVERLAP")
+        stream = torch.cuda.Stream()
+        for t in range(n):
+            st.step_device([dev[s][t].data_ptr() for s in range(2)], stream.cuda_stream)
+        st.join(stream.cuda_stream)
+        stream.synchronize()  # the join alone must cover the last step's tracking
+        logs[ov] = [st.log(s).tobytes() for s in range(2)]
+        st.synchronize()
+    assert logs["1"] == logs["0"]
+    out, log, _ = O.run_pipeline_cpu(clips[0], frames[0], MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), "orc")
+    assert logs["1"][0] == log.tobytes()
