@@ -305,6 +305,10 @@ int trb_debug_phases(uint64_t* out256);
 /* diagnostics build: per mean-shift CTA [busy ns, last item end
  * (globaltimer ns)] while the log is on (2048 entries) */
 int trb_debug_cta_times(uint64_t* out2048, int reset);
+/* diagnostics build: per (cluster rank 0..7, warp 0..7, [histogram,
+ * centroid]) the sum over 8-CTA engine runs of the warp's phase-B walk
+ * cycles (slowest lane) while the log is on (128 entries) */
+int trb_debug_warp_walks(uint64_t* out128, int reset);
 
 #ifdef __cplusplus
 }

@@ -902,6 +902,14 @@ extern "C" int trb_debug_cta_times(uint64_t* out2048, int reset) {
   });
 }
 
+extern "C" int trb_debug_warp_walks(uint64_t* out128, int reset) {
+  return guard([&] {
+    need(out128 != nullptr, "null argument");
+    use_device(0);
+    trb::read_warpwalk(reinterpret_cast<unsigned long long*>(out128), reset != 0);
+  });
+}
+
 extern "C" int trb_debug_phases(uint64_t* out128) {
   return guard([&] {
     need(out128 != nullptr, "null argument");

@@ -19,6 +19,8 @@ __shared__ int s_ph_bucket;
 __shared__ unsigned long long s_item_t0;
 // per-CTA [busy ns, last item end (globaltimer)] of the mean-shift kernel
 __device__ unsigned long long g_cta_time[2 * 1024];
+// per (cluster rank, warp, hist/cent): sum over runs of the warp's phase-B walk cycles (8-CTA runs)
+__device__ unsigned long long g_warpwalk[8 * 8 * 2];
 }  // namespace trb
 // The device-side instrumentation below compiles only into the diagnostics
 // build (make diag -> libtrb_diag.so, -DTRB_DIAG); the product build has no
@@ -43,20 +45,26 @@ __device__ unsigned long long g_cta_time[2 * 1024];
   } while (0)
 // per-thread phase-B walk cycles of rank-0 CTAs: [40 + 2*(L==3)] max, [41 + 2*(L==3)] sum
 #define TRB_OSUM_WALK_BEGIN() \
-  const long long walk_t0_ = ::trb::g_phase_on ? clock64() : 0; \
+  const bool walk_on_ = ::trb::g_phase_on != 0;             \
+  const long long walk_t0_ = walk_on_ ? clock64() : 0;       \
   long long walk_t1_ = walk_t0_;                                 \
   unsigned long long nslow_ = 0, nbp_ = 0
 // per-element timestamps of global thread 0's walks (L == 3 only): g_phase[192 + k]
 #define TRB_OSUM_ELEM_TRACE(k, dep) \
-  if (::trb::g_phase_on && L == 3 && rank == 0 && threadIdx.x == 0 && (k) < 32) \
+  if (walk_on_ && L == 3 && rank == 0 && threadIdx.x == 0 && (k) < 32) \
     ::trb::g_phase[192 + (k)] = clock64() - walk_t0_ + ((dep) != (dep) ? 1 : 0)
 // time to the first element's data (cursor start-up); `dep` forces the wait
 #define TRB_OSUM_WALK_FIRST(cond, dep) \
-  if ((cond) && ::trb::g_phase_on) walk_t1_ = clock64() + ((dep) != (dep) ? 1 : 0)
+  if ((cond) && walk_on_) walk_t1_ = clock64() + ((dep) != (dep) ? 1 : 0)
 #define TRB_OSUM_COUNT(v) ++(v)
 #define TRB_OSUM_WALK_END()                                                                        \
   do {                                                                                             \
-    if (::trb::g_phase_on && rank == 0 && j0 < j1) {                                               \
+    if (walk_on_ && G == 8) { /* per (rank, warp): the warp's slowest lane, summed over runs */   \
+      const unsigned wm_ = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(clock64() - walk_t0_)); \
+      if ((threadIdx.x & 31) == 0)                                                                 \
+        atomicAdd(&::trb::g_warpwalk[((rank * 8 + (threadIdx.x >> 5)) * 2) + (L == 3)], wm_);      \
+    }                                                                                              \
+    if (walk_on_ && rank == 0 && j0 < j1) {                                                        \
       const unsigned long long d_ = clock64() - walk_t0_;                                          \
       unsigned long long* ph_ = ::trb::g_phase + 64 * ::trb::s_ph_bucket;                         \
       atomicMax(&ph_[40 + 2 * (L == 3)], d_);                                                      \
@@ -318,32 +326,40 @@ __device__ __forceinline__ unsigned u4_byte(const uint4& u, int k) {
 }
 
 // mean-shift centroid: every window pixel, weight sqrt(q/p) of its bin;
-// bins are 16-pixel units (uint4), chunk-interleaved, streamed through two
-// cp.async slots per thread.  The loop stays rolled (kUnroll 1).
+// bins are 4-pixel words, chunk-interleaved (word i of thread gt at
+// i*GT + gt, so a warp's loads are coalesced), streamed through a ring of
+// kRing 4-byte cp.async slots per thread.  Chunks are multiples of 4 pixels
+// (not 16), so small and medium windows spread over all the cluster's
+// threads.  The loop stays rolled (kUnroll 1).
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 struct CentroidSrc {
   static constexpr int kUnroll = 1;
+  static constexpr int kRing = 8;
   const uint8_t* bins;
   const double* wsq;  // < 0 when p[b] <= 0
   int x0, y0, ww;
-  uint4* stage;       // [2][blockDim.x]
-  static __device__ __forceinline__ int chunk(int N, int GT) { return ((N + GT - 1) / GT + 15) & ~15; }
+  uint32_t* stage;    // [kRing][blockDim.x] 4-byte slots
+  static __device__ __forceinline__ int chunk(int N, int GT) { return ((N + GT - 1) / GT + 3) & ~3; }
   struct Cursor {
     const CentroidSrc* s;
-    const uint4* p;  // next unit to request
-    int i, xx, GT;   // i = element index inside the chunk
-    double xd, yd;   // pixel coordinates as doubles (exact integers)
-    uint4 cur;
+    const uint32_t* p;  // next word to request
+    int i, xx, GT;      // i = element index inside the chunk
+    double xd, yd;      // pixel coordinates as doubles (exact integers)
+    uint32_t cur;
     __device__ __forceinline__ void next(int /*k*/, bool& start, int& seg, bool& has, double* v) {
-      const int k = i & 15;
+      const int k = i & 3;
       if (k == 0) {
-        cp_async_wait<1>();  // this unit has landed (the next may still fly)
-        uint4* slot = s->stage + ((i >> 4) & 1) * blockDim.x + threadIdx.x;
-        cur = *slot;
-        cp_async16(slot, p);  // the unit after next
+        const int w = i >> 2;
+        cp_async_wait<kRing - 2>();  // word w has landed
+        cur = s->stage[(w & (kRing - 1)) * blockDim.x + threadIdx.x];
+        cp_async4(s->stage + ((w + kRing - 1) & (kRing - 1)) * blockDim.x + threadIdx.x, p);
         cp_async_commit();
         p += GT;
       }
-      const double w = s->wsq[u4_byte(cur, k)];
+      const double w = s->wsq[(cur >> (8 * k)) & 0xffu];
       start = false, seg = 0, has = w >= 0.0;
       v[0] = w;
       v[1] = xmul(w, xd);
@@ -353,23 +369,25 @@ struct CentroidSrc {
       if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0);
     }
   };
-  // j0 = gt * C with C a multiple of 16
+  // j0 = gt * C with C a multiple of 4
   __device__ Cursor begin(int j0, int gt, int /*C*/, int GT) const {
     const int xx = j0 % ww, yy = j0 / ww;
-    const uint4* p = reinterpret_cast<const uint4*>(bins) + gt;
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(bins) + gt;
     Cursor c;
     c.s = this, c.i = 0, c.xx = xx, c.GT = GT;
     c.xd = static_cast<double>(x0 + xx), c.yd = static_cast<double>(y0 + yy);
-    c.cur = make_uint4(0, 0, 0, 0);
+    c.cur = 0;
     cp_async_wait<0>();
-    cp_async16(stage + threadIdx.x, p);
-    cp_async_commit();
-    cp_async16(stage + blockDim.x + threadIdx.x, p + GT);
-    cp_async_commit();
-    c.p = p + 2 * GT;
+#pragma unroll
+    for (int r = 0; r < kRing - 1; ++r, p += GT) {
+      cp_async4(stage + r * blockDim.x + threadIdx.x, p);
+      cp_async_commit();
+    }
+    c.p = p;
     return c;
   }
 };
+static_assert(CentroidSrc::kRing * 4 * NT <= kOsumStageBytes, "centroid staging ring exceeds the gather list");
 
 __device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int x, int y, const TrackSmem& sm, int K,
                                       bool use_lut) {
@@ -406,17 +424,12 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   {
     int xx = j0 % ww, yy = j0 / ww, npos = 0;
     unsigned wacc = 0;
-    uint4 uacc = make_uint4(0, 0, 0, 0);
-    uint4* bw = reinterpret_cast<uint4*>(scr.bins) + gt;
-    // word (j >> 2) & 3 of the unit is complete: place it, store full units
-    auto put_word = [&](int j, bool last) {
-      const int q = (j >> 2) & 3;
-      if (q == 0) uacc.x = wacc;
-      else if (q == 1) uacc.y = wacc;
-      else if (q == 2) uacc.z = wacc;
-      else uacc.w = wacc;
+    uint32_t* bw = reinterpret_cast<uint32_t*>(scr.bins) + gt;
+    // a 4-pixel word of bins is complete: store it (word-interleaved)
+    auto put_word = [&](int /*j*/, bool /*last*/) {
+      *bw = wacc;
+      bw += GT;
       wacc = 0;
-      if (q == 3 || last) *bw = uacc, bw += GT, uacc = make_uint4(0, 0, 0, 0);
     };
     if (ch == 1 && use_lut) {
       // gray + LUT (the tracker's case): pixels are loaded one step ahead
@@ -494,16 +507,16 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] += static_cast<int>(sm.red[b]);
   {
     int xx = j0 % ww, yy = j0 / ww;
-    const uint4* bw = reinterpret_cast<const uint4*>(scr.bins) + gt;
-    uint4 unit = bw[0], unext = bw[GT];  // (slack past N)
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(scr.bins) + gt;
+    uint32_t word = bw[0], wnext = bw[GT];  // (slack past N)
     bw += 2 * GT;
     // vals in BinsSrc's interleaved layout for its chunk size
     const int nseq = sm.binoff[NB], Cv = BinsSrc::chunk(nseq, GT);
     const UDiv32 divC = UDiv32::make(static_cast<uint32_t>(max(1, Cv)));
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
-      const int b = u4_byte(unit, j & 15);
-      if ((j & 15) == 15) unit = unext, unext = *bw, bw += GT;
+      const int b = (word >> (8 * (j & 3))) & 0xffu;
+      if ((j & 3) == 3) word = wnext, wnext = *bw, bw += GT;
       if (w > 0.0) {
         TRB_CHECK(b < K && sm.cnt[b * NT_ + t] < 2 * N && sm.cnt[K * NT_ + t] < 2 * N, "partition scatter", b,
                   sm.cnt[K * NT_ + t]);
@@ -587,7 +600,7 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
     }
     // the window is the same (same cx, cy); its bins are cached in scr.bins
     const Win r = clip_window(fw, fh, cx, cy, w, h);
-    CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0, osum_stage(*sm.os)};
+    CentroidSrc cs{scr.bins, sm.wsq, r.x0, r.y0, r.x1 - r.x0, reinterpret_cast<uint32_t*>(osum_stage(*sm.os))};
     osum_run<3, false>(sm.grp, (r.x1 - r.x0) * (r.y1 - r.y0), 0, cs, *sm.os, g_trb_stats);
     const double sw = sm.os->result[0], sx = sm.os->result[1], sy = sm.os->result[2];
     __syncthreads();
@@ -1442,6 +1455,14 @@ void read_cta_times(unsigned long long* out2048, bool reset) {
 
 void read_phases(unsigned long long* out128) {
   TRB_CUDA(cudaMemcpyFromSymbol(out128, g_phase, 256 * sizeof(*out128)));
+}
+
+void read_warpwalk(unsigned long long* out128, bool reset) {
+  TRB_CUDA(cudaMemcpyFromSymbol(out128, g_warpwalk, 128 * sizeof(*out128)));
+  if (reset) {
+    unsigned long long z[128] = {};
+    TRB_CUDA(cudaMemcpyToSymbol(g_warpwalk, z, sizeof(z)));
+  }
 }
 
 int64_t read_itlog(long long* out, int64_t cap) {

@@ -119,4 +119,5 @@ void enable_itlog(bool on);
 int64_t read_itlog(long long* out, int64_t cap);
 void read_phases(unsigned long long* out128);
 void read_cta_times(unsigned long long* out2048, bool reset);
+void read_warpwalk(unsigned long long* out128, bool reset);
 }  // namespace trb

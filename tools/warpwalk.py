@@ -1,0 +1,45 @@
+"""Per (cluster rank, warp) phase-B walk time of the mean-shift engine runs
+over a few steady C5 steps (diagnostics build): where the slowest warps of a
+cluster sit.  Diagnostics only."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+_DIAG = os.path.join(ROOT, "paper_1310_3322_b200", "libtrb_diag.so")
+if os.path.exists(_DIAG):
+    os.environ.setdefault("TRB_LIB", _DIAG)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1310_3322_b200 as trb  # noqa: E402
+from paper_1310_3322_b200 import api  # noqa: E402
+from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
+from paper_1310_3322_b200.synth import recipe  # noqa: E402
+
+S, steps = 64, 3
+stream = torch.cuda.Stream()
+clips = [recipe("C5", s) for s in range(S)]
+n = 93 + steps
+frames = bench.make_frames(trb, clips, n, stream)
+st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+for t in range(93):
+    st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
+torch.cuda.synchronize()
+L = api.lib()
+L.trb_debug_warp_walks.argtypes = [C.c_void_p, C.c_int]
+buf = np.zeros(128, np.uint64)
+L.trb_debug_warp_walks(buf.ctypes.data, 1)
+api.debug_itlog(True)
+for t in range(93, n):
+    st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
+torch.cuda.synchronize()
+api.debug_itlog(False)
+L.trb_debug_warp_walks(buf.ctypes.data, 1)
+w = buf.reshape(8, 8, 2).astype(np.float64) / 1.965e3 / steps  # us per step
+for k, nm in enumerate(("histogram", "centroid")):
+    print(f"{nm}: walk us per step summed over runs, [rank][warp]")
+    for r in range(8):
+        print(f"  rank {r}: " + " ".join(f"{v:8.0f}" for v in w[r, :, k]))
