@@ -472,72 +472,56 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       hi[l] = -1.0;
     }
   };
-  // Chunk-armed fast walk.  When the chunk holds no segment start and, for
-  // every lane, the approximate prefixes before its first step (xP) and
-  // after its last (xP + aP, same error budget) lie inside one binade with
-  // the 2*delta margins, every step of the chunk is safe in that binade (the
-  // true sums are monotone in between): no per-step prefix or compare, the
-  // piece is the composition of the add / tie steps (osum_step_safe).  The
-  // decision is per warp (all lanes fast or none).
-  bool done = false;
-#ifndef TRB_FASTWALK
-#define TRB_FASTWALK 1
-#endif
   {
-    bool fast = TRB_FASTWALK && af == 0 && j0 < j1 && !(j0 == 0 && !SEG);
-    double Mf[L];
-    int ef[L];
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      const double Pe = xadd(xP[l], aP[l]);
-      const long long bp_ = __double_as_longlong(xP[l]), bn_ = __double_as_longlong(Pe);
-      const int eb = static_cast<int>(bp_ >> 52);
-      fast = fast && xP[l] > 0.0 && eb == static_cast<int>(bn_ >> 52) && eb > 64 && eb < 1982 &&
-             (bp_ & kMant) >= lowm && (bn_ & kMant) <= highm;
-      Mf[l] = osum_pow2(eb - 1023);
-      ef[l] = eb - 1023;
-    }
-    // warp-uniform: a warp whose lanes split between the two walks would
-    // execute both loops one after the other
-    fast = __all_sync(0xffffffffu, fast);
-    if (stats && (t & 31) == 0) atomicAdd(&stats[fast ? 12 : 14], 1ull);
-    if (fast) {
-      // every step is safe in binade ef: ties compose into the piece
-      auto cur = src.begin(j0, gt, C, GT);
-      for (int jb = j0; jb < j1; jb += Src::kUnroll)
-#pragma unroll
-        for (int k = 0; k < Src::kUnroll; ++k) {
-          const int j = jb + k;
-          if (j >= j1) break;
-          bool start, has;
-          int seg;
-          double v[L];
-          cur.next(k, start, seg, has, v);
-          if (!has) continue;
-#pragma unroll
-          for (int l = 0; l < L; ++l) osum_step_safe(pc[l], v[l], Mf[l], ef[l], tbad);
-        }
-      done = true;
-    }
-  }
-  if (!done) {
     double P[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) P[l] = xP[l];
+    for (int l = 0; l < L; ++l) {
+      P[l] = xP[l];
+      // pre-armed from the prefix before the first step (lower margin met):
+      // the first step is then safe iff P_next <= hi, as for any armed step
+      const long long bp_ = __double_as_longlong(xP[l]);
+      const int eb = static_cast<int>(bp_ >> 52);
+      if (xP[l] > 0.0 && eb > 64 && eb < 1982 && (bp_ & kMant) >= lowm) {
+        hi[l] = __longlong_as_double((static_cast<long long>(eb) << 52) | highm);
+        M[l] = osum_pow2(eb - 1023);
+        ea[l] = eb - 1023;
+      }
+    }
     auto cur = src.begin(j0, gt, C, GT);
-    // unrolled so the cursor's read-ahead slots are static registers
-    for (int jb = j0; jb < j1; jb += Src::kUnroll)
-#pragma unroll
-    for (int k = 0; k < Src::kUnroll; ++k) {
-      const int j = jb + k;
-      if (j >= j1) break;
+    static_assert(Src::kUnroll == 1, "phase B walks one element per iteration");
+    for (int j = j0; j < j1; ++j) {
       bool start, has;
       int seg;
       double v[L];
-      cur.next(k, start, seg, has, v);
+      cur.next(0, start, seg, has, v);
       TRB_OSUM_WALK_FIRST(j == j0, v[0]);
       TRB_OSUM_ELEM_TRACE(j - j0, v[0]);
-      if (SEG ? start : j == 0) {  // a segment head begins (S = +0 exactly)
+      const bool hs = SEG ? start : j == 0;
+      if (!hs && !inhead) {
+        // the common step, kept lean (no branch per lane, no state merges):
+        // every lane armed with P_next <= hi and no tie -> X += RN(a/u).
+        // Anything else (arming, binade crossing, tie, head) falls through
+        // to the general code below for this element.
+        if (!has) continue;
+        bool ok = true;
+        double Pn[L];
+        long long r[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          Pn[l] = xadd(P[l], v[l]);
+          const double y = xadd(M[l], v[l]);
+          const double d = xsub(v[l], xsub(y, M[l]));
+          const double hu = __longlong_as_double(__double_as_longlong(M[l]) - (53LL << 52));  // u/2
+          ok = ok & (Pn[l] <= hi[l]) & (fabs(d) != hu);
+          r[l] = __double_as_longlong(y) - __double_as_longlong(M[l]);
+        }
+        if (ok) {
+#pragma unroll
+          for (int l = 0; l < L; ++l) pc[l].B += r[l], pc[l].e = ea[l], P[l] = Pn[l];
+          continue;
+        }
+      }
+      if (hs) {  // a segment head begins (S = +0 exactly)
         if (inhead) emit_head();
         inhead = true, hj = j, hseg = seg;
 #pragma unroll

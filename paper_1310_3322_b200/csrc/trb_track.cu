@@ -59,10 +59,16 @@ __device__ unsigned long long g_warpwalk[8 * 8 * 2];
 #define TRB_OSUM_COUNT(v) ++(v)
 #define TRB_OSUM_WALK_END()                                                                        \
   do {                                                                                             \
-    if (walk_on_ && G == 8) { /* per (rank, warp): the warp's slowest lane, summed over runs */   \
+    if (walk_on_ && G == 8) { /* by warp class: the warp's slowest lane, summed, and counted */    \
       const unsigned wm_ = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(clock64() - walk_t0_)); \
-      if ((threadIdx.x & 31) == 0)                                                                 \
-        atomicAdd(&::trb::g_warpwalk[((rank * 8 + (threadIdx.x >> 5)) * 2) + (L == 3)], wm_);      \
+      const bool work_ = __any_sync(0xffffffffu, j0 < j1);                                         \
+      const int cls_ = !work_ ? 2 : 1;                                                \
+      const unsigned ns_ = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nslow_));          \
+      if ((threadIdx.x & 31) == 0) {                                                               \
+        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + cls_ * 2], wm_);                               \
+        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + cls_ * 2 + 1], 1ull);                          \
+        if (cls_ == 1) atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + 8], ns_);                       \
+      }                                                                                            \
     }                                                                                              \
     if (walk_on_ && rank == 0 && j0 < j1) {                                                        \
       const unsigned long long d_ = clock64() - walk_t0_;                                          \
@@ -263,7 +269,7 @@ __device__ __forceinline__ double epan_weight(const TrackSmem& sm, int xx, int y
 // 2-element blocks: block b of thread gt is the double2 at b*GT + gt.  The
 // cursor streams blocks through a ring of kRing cp.async slots per thread.
 struct BinsSrc {
-  static constexpr int kUnroll = 2;
+  static constexpr int kUnroll = 1;
   static constexpr int kRing = 5;
   const double* vals;
   const int* off;  // [K+1]
@@ -274,8 +280,9 @@ struct BinsSrc {
     const BinsSrc* s;
     const double2* p;  // next block to request
     int j, b, sb, nb, GT, blk;  // current segment b = [sb, nb); blk = block being consumed
+    int k;                      // element of the current 2-element block
     double c0, c1;
-    __device__ __forceinline__ void next(int k, bool& start, int& seg, bool& has, double* v) {
+    __device__ __forceinline__ void next(int /*k*/, bool& start, int& seg, bool& has, double* v) {
       if (k == 0) {
         cp_async_wait<kRing - 2>();  // block blk has landed
         const uint4* slot = s->stage + (blk % kRing) * blockDim.x + threadIdx.x;
@@ -293,13 +300,14 @@ struct BinsSrc {
       TRB_CHECK(b < s->K, "BinsSrc segment", b, j);
       start = (j == sb), seg = b, has = true, v[0] = k == 0 ? c0 : c1;
       ++j;
+      k ^= 1;
     }
   };
   __device__ Cursor begin(int j0, int gt, int /*C*/, int GT) const {
     int b = 0;
     while (b < K - 1 && off[b + 1] <= j0) ++b;
     Cursor c;
-    c.s = this, c.j = j0, c.b = b, c.sb = off[b], c.nb = off[b + 1], c.GT = GT, c.blk = 0;
+    c.s = this, c.j = j0, c.b = b, c.sb = off[b], c.nb = off[b + 1], c.GT = GT, c.blk = 0, c.k = 0;
     c.c0 = c.c1 = 0.0;
     cp_async_wait<0>();  // nothing of an earlier walk is still landing
     const double2* p = reinterpret_cast<const double2*>(vals) + gt;

@@ -38,8 +38,10 @@ for t in range(93, n):
 torch.cuda.synchronize()
 api.debug_itlog(False)
 L.trb_debug_warp_walks(buf.ctypes.data, 1)
-w = buf.reshape(8, 8, 2).astype(np.float64) / 1.965e3 / steps  # us per step
+w = buf.astype(np.float64)
 for k, nm in enumerate(("histogram", "centroid")):
-    print(f"{nm}: walk us per step summed over runs, [rank][warp]")
-    for r in range(8):
-        print(f"  rank {r}: " + " ".join(f"{v:8.0f}" for v in w[r, :, k]))
+    b = w[16 * k:16 * k + 16]
+    for c, cn in enumerate(("fast", "general", "idle")):
+        n = max(b[2 * c + 1], 1)
+        print(f"{nm:10s} {cn:8s} warps/step {b[2 * c + 1] / steps:9.0f}  mean walk {b[2 * c] / n / 1.965e3:7.2f} us")
+    print(f"{nm:10s} general warps: mean max-lane slow events {b[8] / max(b[3], 1):.1f}")
