@@ -43,6 +43,7 @@ WIDTH, HEIGHT = 1920, 1080
 PX = WIDTH * HEIGHT
 MOTION_BYTES_PER_PX = 8   # frame 1 + evict 1 + insert 1 + u16 sum 2+2 + mask 1
 PATH_BYTES_PER_PX = 12    # + int32 labels
+MORPH_BYTES_PER_PX = 2    # fused 3x3 open: mask in 1 + mask out 1 (halo re-reads are not algorithmic)
 
 
 def parse():
@@ -318,6 +319,23 @@ def ours_main(args, rank, world, local_rank):
     stage_ms = stage_ms / max(1, prof_steps)
     track_px = api.debug_stats(reset=True).get("meanshift_window_px", 0) / max(1, prof_steps)
 
+    # ---- the fused 3x3 morphology kernel (north-star kernel (2); OFF in the
+    #      reference-parity workload): open (erode -> dilate, one fused pass)
+    #      on this step's 64 x 1080p masks, CUDA events around K launches
+    mask0, _ = st.device_planes(0)
+    morph_out = torch.empty((S, PX), dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            api.morph_device(mask0, morph_out.data_ptr(), WIDTH, HEIGHT, S, 3, stream.cuda_stream)
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for _ in range(K):
+            api.morph_device(mask0, morph_out.data_ptr(), WIDTH, HEIGHT, S, 3, stream.cuda_stream)
+        m1.record(stream)
+    torch.cuda.synchronize()
+    morph_ms = m0.elapsed_time(m1) / K
+    del morph_out
+
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H timed
     e2e = None
     if e2e_steps:
@@ -357,6 +375,13 @@ def ours_main(args, rank, world, local_rank):
                        "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                        "traffic": dram_traffic("motion_dram_bytes.json"),
                        "bytes_per_launch": MOTION_BYTES_PER_PX * S * PX}
+    morph_achieved = MORPH_BYTES_PER_PX * S * PX / (morph_ms / 1e3) / 1e9
+    roofline_morph = {"bound": "hbm", "kernel": "morph_strip_kernel<open> (erode+dilate fused)",
+                      "achieved": morph_achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                      "frac": morph_achieved / peak, "traffic": None, "bytes_per_launch": MORPH_BYTES_PER_PX * S * PX,
+                      "ms_per_launch": morph_ms,
+                      "note": "not on the parity path (the reference has no morphology); one launch per step when "
+                              "MotionConfig.morph is set; back-to-back launches on the same 133 MB of masks"}
     # the dominant kernel: track_meanshift_kernel.  SURVEY §8(d): tracking's
     # algorithmic bytes are its frame reads, window px x iterations x channels
     ms_ms = stage_ms[2]
@@ -382,7 +407,7 @@ def ours_main(args, rank, world, local_rank):
                    "track_window_px_per_step": track_px,
                    "stage_timing": "separate pass of K steps with CUDA events between stages",
                    "path_hbm_frac": path_gbs / peak},
-        "roofline": roofline, "roofline_motion": roofline_motion,
+        "roofline": roofline, "roofline_motion": roofline_motion, "roofline_morph": roofline_morph,
         "gpu_launches": launches, "clocks": clk,
     }
     if e2e:

@@ -157,6 +157,14 @@ int trb_parse_track_log(const char* text, int64_t len, const char* source, trb_t
 int trb_save_track_log(const char* path, const trb_track_log_entry* log, int64_t n);
 int trb_load_track_log(const char* path, trb_track_log_entry* out, int64_t cap, int64_t* n);
 
+/* ---- 3x3 morphology on device masks (extension, not in the reference) ----
+ * n_planes masks of width x height bytes (0/1), back to back in device memory;
+ * out-of-image neighbours are ignored.  op: TRB_MORPH_*.  Widths that are a
+ * multiple of 16 take the fused row-strip kernel (open/close in one pass);
+ * `in` and `out` must not overlap.  cuda_stream: NULL = legacy stream. */
+int trb_morph_device(const uint8_t* in, uint8_t* out, int width, int height, int n_planes, int op,
+                     void* cuda_stream);
+
 /* ---- warp_frame (motion.hpp:81-119) ----
  * Inverse-mapped bilinear resampling of one frame (host buffers) by the
  * homography h (row-major 3x3); samples off the source plane read 0. */

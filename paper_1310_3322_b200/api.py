@@ -132,6 +132,7 @@ def _declare(L):
         "trb_streams_step_device_warp": [vp, vp, vp, vp],
         "trb_extract_blob_features": [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp],
         "trb_streams_blob_features": [vp, i32, vp, vp, vp, i32, C.POINTER(C.c_int)],
+        "trb_morph_device": [vp, vp, i32, i32, i32, i32, vp],
         "trb_streams_synchronize": [vp],
         "trb_streams_join": [vp, vp],
         "trb_streams_frames_seen": [vp, C.POINTER(C.c_int)],
@@ -634,3 +635,10 @@ def selftest_hypot(x: np.ndarray, y: np.ndarray, on_device: bool) -> np.ndarray:
     out = np.empty_like(x)
     _check(lib().trb_selftest_hypot(_ptr(x), _ptr(y), x.size, _ptr(out), int(on_device)))
     return out
+
+
+def morph_device(in_ptr: int, out_ptr: int, width: int, height: int, n_planes: int, op: int,
+                 cuda_stream: int = 0) -> None:
+    """3x3 morphology on device masks (trb_morph_device); op = TRB_MORPH_*."""
+    _check(lib().trb_morph_device(C.c_void_p(in_ptr), C.c_void_p(out_ptr), width, height, n_planes, op,
+                                  C.c_void_p(cuda_stream)))

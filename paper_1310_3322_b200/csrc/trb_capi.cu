@@ -139,7 +139,7 @@ int trb_motion_create(const trb_motion_config* cfg, int width, int height, int d
     const size_t px = static_cast<size_t>(width) * height;
     m->frame.alloc(px, false);
     m->mask.alloc(px);
-    if (cfg->morph != TRB_MORPH_NONE) m->tmp.alloc(px);
+    if (cfg->morph != TRB_MORPH_NONE) m->tmp.alloc(2 * px);  // raw mask + 2-pass scratch
     m->ptrs.alloc(sizeof(void*), false);
     const void* fp = m->frame.p;
     TRB_CUDA(cudaMemcpy(m->ptrs.p, &fp, sizeof(void*), cudaMemcpyHostToDevice));
@@ -568,6 +568,20 @@ int trb_streams_step_device_warp(trb_streams* s, const uint8_t* const* frames, c
     need(s && frames, "null argument");
     TRB_CUDA(cudaSetDevice(s->device));
     s->s->step_device_warp(frames, homographies, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int trb_morph_device(const uint8_t* in, uint8_t* out, int width, int height, int n_planes, int op,
+                     void* cuda_stream) {
+  return guard([&] {
+    need(in && out, "null argument");
+    need(width >= 1 && height >= 1 && n_planes >= 1, "morphology needs positive dimensions");
+    need(op >= TRB_MORPH_ERODE && op <= TRB_MORPH_CLOSE, "unknown morphology op");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    thread_local trb::DevBuf scratch;  // two-pass path only (width not a multiple of 16)
+    if (width % 16 != 0 && (op == TRB_MORPH_OPEN || op == TRB_MORPH_CLOSE))
+      scratch.alloc(static_cast<size_t>(width) * height * n_planes, false);
+    trb::launch_morph(in, out, scratch.as<uint8_t>(), width, height, n_planes, op, st);
   });
 }
 

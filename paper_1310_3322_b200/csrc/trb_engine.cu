@@ -72,7 +72,11 @@ bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t*
   a.ring = ring_.as<uint8_t>();
   a.ring_stride = px_ * W;
   a.sums = sums_.p;
-  a.mask = mask;
+  // with morphology, motion writes its raw mask into tmp and the (fused)
+  // morphology stage writes the final mask
+  const bool morph = cfg_.morph != TRB_MORPH_NONE;
+  uint8_t* raw = morph ? tmp : mask;
+  a.mask = raw;
   a.px = px_;
   a.slot = frames_seen_ % W;
   a.full_before = frames_seen_ >= W;
@@ -96,14 +100,14 @@ bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t*
       m.bins = cfg_.bins;
       m.threshold = cfg_.threshold;
       m.newest = a.slot;
-      m.mask = mask;
+      m.mask = raw;
       launch_motion_mode(m, S_, st);
       ++*launches;
     }
   }
   ++frames_seen_;
   if (!a.emit) return false;
-  if (cfg_.morph != TRB_MORPH_NONE) *launches += launch_morph(mask, tmp, w_, h_, S_, cfg_.morph, st);
+  if (morph) *launches += launch_morph(raw, mask, tmp + static_cast<size_t>(px_) * S_, w_, h_, S_, cfg_.morph, st);
   return true;
 }
 
@@ -203,7 +207,7 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   ccl_ = std::make_unique<CclState>(S, w, h, sc);
   if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S);
   mask_.alloc(static_cast<size_t>(px_) * S);
-  if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S);
+  if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S * 2);  // raw mask + 2-pass scratch
   // ring of per-step frame-pointer tables: a table is rewritten only after
   // the event of its previous use completed, so steps never block the host
   frame_ptrs_.alloc(sizeof(void*) * S * kPtrSlots);

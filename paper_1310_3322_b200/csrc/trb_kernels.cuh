@@ -37,7 +37,8 @@ void launch_ring_update(const MotionArgs& a, int channels, bool wide_sums, int n
 void launch_motion_mode(const ModeArgs& a, int n_streams, cudaStream_t st);
 void launch_mean_background(const void* sums, int64_t px, int W, bool wide_sums, uint8_t* out, cudaStream_t st);
 // returns the number of launches issued
-int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int op, cudaStream_t st);
+int launch_morph(const uint8_t* in, uint8_t* out, uint8_t* scratch, int w, int h, int n_streams, int op,
+                 cudaStream_t st);
 // warp_frame (motion.hpp:81-119): host inverse (throws the reference's
 // InvalidArgument messages) and the per-pixel resampling of S frames.
 void homography_inverse(const double* h9, double* inv9);

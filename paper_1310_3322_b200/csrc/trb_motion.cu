@@ -206,6 +206,114 @@ __global__ void __launch_bounds__(256) morph3x3_kernel(const uint8_t* __restrict
   out[static_cast<int64_t>(gy) * w + gx] = static_cast<uint8_t>(acc);
 }
 
+// Row-strip 3x3 morphology for widths that are a multiple of 16 (the HBM
+// path): a lane owns a 16-pixel column block (one 16-byte vector per row)
+// and walks a strip of kStripRows rows with a sliding window, so each mask
+// byte is read ~(R+4)/R times and written once.  The horizontal 3-tap runs
+// on two u64 words with byte shifts; the neighbours' edge bytes come from
+// the adjacent lanes (__shfl), so a warp covers 32 blocks but stores only
+// its 30 inner ones (lanes 0 and 31 are halo).  OP: 0 erode, 1 dilate,
+// 2 open (erode then dilate), 3 close (dilate then erode) — the two-stage
+// ops run fused (the eroded rows never leave registers).  Out-of-image
+// neighbours are ignored (neutral element), as morph3x3_kernel.
+#ifndef TRB_MORPH_ROWS
+#define TRB_MORPH_ROWS 8
+#endif
+constexpr int kStripRows = TRB_MORPH_ROWS;
+constexpr uint64_t kOnes = 0x0101010101010101ull;
+
+template <bool AND>
+__device__ __forceinline__ uint64_t bop(uint64_t a, uint64_t b) {
+  return AND ? (a & b) : (a | b);
+}
+
+// horizontal 3-tap over this lane's 16 bytes (all 32 lanes must call it)
+template <bool AND>
+__device__ __forceinline__ void horiz3(uint64_t& lo, uint64_t& hi, int lane) {
+  const uint64_t nb = AND ? 1ull : 0ull;
+  uint64_t lb = __shfl_up_sync(0xffffffffu, hi >> 56, 1);
+  uint64_t rb = __shfl_down_sync(0xffffffffu, lo & 0xffull, 1);
+  if (lane == 0) lb = nb;
+  if (lane == 31) rb = nb;
+  const uint64_t l_lo = (lo << 8) | lb, l_hi = (hi << 8) | (lo >> 56);
+  const uint64_t r_lo = (lo >> 8) | (hi << 56), r_hi = (hi >> 8) | (rb << 56);
+  lo = bop<AND>(bop<AND>(lo, l_lo), r_lo);
+  hi = bop<AND>(bop<AND>(hi, l_hi), r_hi);
+}
+
+#ifndef TRB_MORPH_LD
+#define TRB_MORPH_LD __ldg  // halo rows are re-read by the neighbouring strip: keep them in L2
+#define TRB_MORPH_ST __stcs
+#endif
+
+template <int OP>
+__global__ void __launch_bounds__(128) morph_strip_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                          int w, int h, int64_t stride) {
+  constexpr bool A1 = (OP == 0 || OP == 2);  // stage 1 erodes (AND) or dilates (OR)
+  constexpr bool TWO = OP >= 2;
+  constexpr bool A2 = (OP == 3);             // stage 2 of open dilates, of close erodes
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t s = blockIdx.z;
+  in += s * stride;
+  out += s * stride;
+  const int bx = (blockIdx.x * 4 + warp) * 30 + lane - 1;  // this lane's 16-pixel block
+  const bool colok = bx >= 0 && bx * 16 < w;
+  const bool store = colok && lane >= 1 && lane <= 30;
+  const int y0 = blockIdx.y * kStripRows, y1 = min(h, y0 + kStripRows);
+  const uint64_t n1 = A1 ? kOnes : 0ull, n2 = A2 ? kOnes : 0ull;
+  // horizontal stage-1 tap of raw row y (neutral outside the image)
+  auto h1 = [&](int y, uint64_t& lo, uint64_t& hi) {
+    lo = hi = n1;
+    if (colok && y >= 0 && y < h) {
+      const uint4 q = TRB_MORPH_LD(reinterpret_cast<const uint4*>(in + static_cast<int64_t>(y) * w) + bx);
+      lo = (static_cast<uint64_t>(q.y) << 32) | q.x;
+      hi = (static_cast<uint64_t>(q.w) << 32) | q.z;
+    }
+    horiz3<A1>(lo, hi, lane);
+  };
+  auto put = [&](int y, uint64_t lo, uint64_t hi) {
+    if (store) {
+      uint4 q;
+      q.x = static_cast<uint32_t>(lo), q.y = static_cast<uint32_t>(lo >> 32);
+      q.z = static_cast<uint32_t>(hi), q.w = static_cast<uint32_t>(hi >> 32);
+      TRB_MORPH_ST(reinterpret_cast<uint4*>(out + static_cast<int64_t>(y) * w) + bx, q);
+    }
+  };
+  uint64_t al, ah, bl, bh, cl, ch;  // stage-1 taps of rows e-1, e, e+1
+  if (!TWO) {
+    h1(y0 - 1, al, ah);
+    h1(y0, bl, bh);
+    for (int y = y0; y < y1; ++y) {
+      h1(y + 1, cl, ch);
+      put(y, bop<A1>(bop<A1>(al, bl), cl), bop<A1>(bop<A1>(ah, bh), ch));
+      al = bl, ah = bh, bl = cl, bh = ch;
+    }
+  } else {
+    // stage-1 rows e = y0-1 .. y1 (neutral for stage 2 outside the image),
+    // each through the stage-2 horizontal tap
+    auto e_row = [&](int e, uint64_t& lo, uint64_t& hi) {
+      lo = bop<A1>(bop<A1>(al, bl), cl), hi = bop<A1>(bop<A1>(ah, bh), ch);
+      if (!(colok && e >= 0 && e < h)) lo = hi = n2;
+      horiz3<A2>(lo, hi, lane);
+    };
+    uint64_t pl, ph, ql, qh, rl, rh;  // stage-2 taps of stage-1 rows y-1, y, y+1
+    h1(y0 - 2, al, ah);
+    h1(y0 - 1, bl, bh);
+    h1(y0, cl, ch);
+    e_row(y0 - 1, pl, ph);
+    al = bl, ah = bh, bl = cl, bh = ch;
+    h1(y0 + 1, cl, ch);
+    e_row(y0, ql, qh);
+    for (int y = y0; y < y1; ++y) {
+      al = bl, ah = bh, bl = cl, bh = ch;
+      h1(y + 2, cl, ch);
+      e_row(y + 1, rl, rh);
+      put(y, bop<A2>(bop<A2>(pl, ql), rl), bop<A2>(bop<A2>(ph, qh), rh));
+      pl = ql, ph = qh, ql = rl, qh = rh;
+    }
+  }
+}
+
 // Synthetic frame raster (synth.hpp:295-328): background fill, then every
 // shape's rectangle in order (later shapes overwrite earlier ones).
 // grid.y = frame: frame f uses rects + f*n*4 and writes out + f*frame_stride.
@@ -266,34 +374,34 @@ void launch_mean_background(const void* sums, int64_t px, int W, bool wide_sums,
   TRB_LAUNCH_CHECK("mean_background_kernel");
 }
 
-int launch_morph(uint8_t* mask, uint8_t* tmp, int w, int h, int n_streams, int op, cudaStream_t st) {
-  if (op == TRB_MORPH_NONE) return 0;
+// in -> out (distinct buffers).  Returns the number of launches.
+int launch_morph(const uint8_t* in, uint8_t* out, uint8_t* scratch, int w, int h, int n_streams, int op,
+                 cudaStream_t st) {
+  if (op < TRB_MORPH_ERODE || op > TRB_MORPH_CLOSE) throw Error(TRB_CONFIG_ERROR, "unknown morphology op");
   const int64_t stride = static_cast<int64_t>(w) * h;
+  if (w % 16 == 0) {  // HBM path: one fused launch for every op
+    const int warps_per_row = ceil_div(w / 16, 30);
+    dim3 grid(ceil_div(warps_per_row, 4), ceil_div(h, kStripRows), n_streams);
+    switch (op) {
+      case TRB_MORPH_ERODE: morph_strip_kernel<0><<<grid, 128, 0, st>>>(in, out, w, h, stride); break;
+      case TRB_MORPH_DILATE: morph_strip_kernel<1><<<grid, 128, 0, st>>>(in, out, w, h, stride); break;
+      case TRB_MORPH_OPEN: morph_strip_kernel<2><<<grid, 128, 0, st>>>(in, out, w, h, stride); break;
+      default: morph_strip_kernel<3><<<grid, 128, 0, st>>>(in, out, w, h, stride); break;
+    }
+    TRB_LAUNCH_CHECK("morph_strip_kernel");
+    return 1;
+  }
   dim3 grid(ceil_div(w, 32), ceil_div(h, 8), n_streams);
-  auto pass = [&](const uint8_t* in, uint8_t* out, int dilate) {
-    morph3x3_kernel<<<grid, 256, 0, st>>>(in, out, w, h, stride, dilate);
+  auto pass = [&](const uint8_t* src, uint8_t* dst, int dilate) {
+    morph3x3_kernel<<<grid, 256, 0, st>>>(src, dst, w, h, stride, dilate);
     TRB_LAUNCH_CHECK("morph3x3_kernel");
   };
   switch (op) {
-    case TRB_MORPH_ERODE:
-      pass(mask, tmp, 0);
-      break;
-    case TRB_MORPH_DILATE:
-      pass(mask, tmp, 1);
-      break;
-    case TRB_MORPH_OPEN:
-      pass(mask, tmp, 0);
-      pass(tmp, mask, 1);
-      return 2;  // result back in mask
-    case TRB_MORPH_CLOSE:
-      pass(mask, tmp, 1);
-      pass(tmp, mask, 0);
-      return 2;
-    default:
-      throw Error(TRB_CONFIG_ERROR, "unknown morphology op");
+    case TRB_MORPH_ERODE: pass(in, out, 0); return 1;
+    case TRB_MORPH_DILATE: pass(in, out, 1); return 1;
+    case TRB_MORPH_OPEN: pass(in, scratch, 0); pass(scratch, out, 1); return 2;
+    default: pass(in, scratch, 1); pass(scratch, out, 0); return 2;
   }
-  TRB_CUDA(cudaMemcpyAsync(mask, tmp, static_cast<size_t>(stride) * n_streams, cudaMemcpyDeviceToDevice, st));
-  return 1;
 }
 
 // ------------------------------------------------------------------- warp
