@@ -1072,6 +1072,8 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     for (int b = 0; b < 256; ++b) off[b] = o, o += cnt[b];
     *d.work_n = o;
     *d.work_head = 0;
+    *d.spawn_n = 0;  // this frame's spawn list (track_gate_kernel appends)
+    *d.spawn_head = 0;
   }
   __syncthreads();
   for (int item = t; item < n; item += blockDim.x) {
@@ -1269,6 +1271,7 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
           const int64_t g = slot_index(d, s, slot);
           d.used[g] = 1;
           d.pending[g] = 1;
+          d.spawn_list[atomicAdd(d.spawn_n, 1)] = static_cast<int32_t>(g);
           d.id[g] = id;
           d.cx[g] = b.cx;
           d.cy[g] = b.cy;
@@ -1346,14 +1349,22 @@ __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
   const int K = d.K;
   const TrackScratch scr = cluster_scratch(d.scratch, d.scratch_stride, d.maxN);
   const int G = static_cast<int>(cl.num_blocks());
-  const int cid = blockIdx.x / G, ncl = gridDim.x / G;
   const int rank = static_cast<int>(cl.block_rank());
   const bool gray = d.CH == 1;
-  for (int item = cid; item < d.S * d.T; item += ncl) {
-    const int s = item / d.T, slot = item - s * d.T;
-    TRB_PROGRESS(blockIdx.x, 2, item, -1, 0);
-    const int64_t g = slot_index(d, s, slot);
-    if (!d.pending[g]) continue;
+  // clusters claim this frame's spawns from the gate kernel's list (no scan
+  // of every slot: with few or no spawns the kernel is a few microseconds)
+  for (;;) {
+    if (rank == 0 && threadIdx.x == 0) {
+      const int q = atomicAdd(d.spawn_head, 1);
+      sm.iscal[8] = q < *d.spawn_n ? d.spawn_list[q] : -1;
+    }
+    cl.sync();
+    const int claimed = *cl.map_shared_rank(&sm.iscal[8], 0);
+    cl.sync();  // the leader may overwrite iscal[8] only after everyone read it
+    if (claimed < 0) break;
+    const int64_t g = claimed;
+    const int s = static_cast<int>(g / d.T);
+    TRB_PROGRESS(blockIdx.x, 2, claimed, -1, 0);
     const double cx = d.cx[g], cy = d.cy[g];
     const int w = d.w[g], h = d.h[g];
     if (rank == 0) {
@@ -1601,10 +1612,13 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   d_.log = log_.as<trb_track_log_entry>();
   d_.log_cap = log_cap_;
   d_.n_log = nlog_.as<int64_t>();
-  work_.alloc(sizeof(int32_t) * (n + 2));
+  work_.alloc(sizeof(int32_t) * (2 * n + 4));
   d_.work = work_.as<int32_t>();
   d_.work_n = d_.work + n;
   d_.work_head = d_.work + n + 1;
+  d_.spawn_list = d_.work + n + 2;
+  d_.spawn_n = d_.spawn_list + n;
+  d_.spawn_head = d_.spawn_n + 1;
   // next_id starts at 1 (tracking.hpp:239)
   std::vector<int32_t> ones(S, 1);
   TRB_CUDA(cudaMemcpy(d_.next_id, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));

@@ -56,6 +56,10 @@ struct TrackDev {
   int32_t* work;       // [S*T]
   int32_t* work_n;
   int32_t* work_head;
+  // tracks spawned this frame (gate kernel appends, spawn kernel claims)
+  int32_t* spawn_list;  // [S*T] slot indices
+  int32_t* spawn_n;
+  int32_t* spawn_head;
   int G;               // CTAs per cluster
   int iter_floor;      // scheduling: iterations assumed at least
   double split_us;     // tracks estimated below this (single-CTA us) run in split mode
