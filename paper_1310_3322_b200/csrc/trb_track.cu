@@ -1047,7 +1047,6 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
   const int t = threadIdx.x;
   if (t < 256) cnt[t] = 0;
   __syncthreads();
-  const int n = d.S * d.T;
   auto bucket = [&](int item) -> int {
     const int s = item / d.T, i = item - s * d.T;
     if (i >= d.n_list[s]) return -1;
@@ -1062,23 +1061,43 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     const int sub = lz <= 29 ? static_cast<int>((cost >> (29 - lz)) & 3u) : 0;
     return (split_class(d, g) ? 128 : 0) + 4 * lz + (3 - sub);
   };
-  for (int item = t; item < n; item += blockDim.x) {
-    const int b = bucket(item);
-    if (b >= 0) atomicAdd(&cnt[b], 1);
+  // only the listed tracks: one warp per stream, lanes over its list
+  const int lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  for (int s = wid; s < d.S; s += nw) {
+    const int nl = d.n_list[s];
+    for (int i = lane; i < nl; i += 32) {
+      const int b = bucket(s * d.T + i);
+      if (b >= 0) atomicAdd(&cnt[b], 1);
+    }
   }
   __syncthreads();
-  if (t == 0) {
-    int o = 0;
-    for (int b = 0; b < 256; ++b) off[b] = o, o += cnt[b];
-    *d.work_n = o;
-    *d.work_head = 0;
-    *d.spawn_n = 0;  // this frame's spawn list (track_gate_kernel appends)
-    *d.spawn_head = 0;
+  if (wid == 0) {  // exclusive scan of the 256 bucket counts (8 per lane)
+    int v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = cnt[lane * 8 + k], sum += v[k];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int o = incl - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) off[lane * 8 + k] = o, o += v[k];
+    if (lane == 31) {
+      *d.work_n = incl;
+      *d.work_head = 0;
+      *d.spawn_n = 0;  // this frame's spawn list (track_gate_kernel appends)
+      *d.spawn_head = 0;
+    }
   }
   __syncthreads();
-  for (int item = t; item < n; item += blockDim.x) {
-    const int b = bucket(item);
-    if (b >= 0) d.work[atomicAdd(&off[b], 1)] = item;
+  for (int s = wid; s < d.S; s += nw) {
+    const int nl = d.n_list[s];
+    for (int i = lane; i < nl; i += 32) {
+      const int b = bucket(s * d.T + i);
+      if (b >= 0) d.work[atomicAdd(&off[b], 1)] = s * d.T + i;
+    }
   }
 }
 
