@@ -587,6 +587,16 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
           hadbp[l] = 1;
           pc[l] = piece_identity();
           hi[l] = -1.0;
+          // re-arm at once from the prefix after this (replayed) step when it
+          // clears the lower margin of its binade (as the pre-arming from xP):
+          // a crossing then costs one slow step, not two or three
+          const long long bn_ = __double_as_longlong(Pn);
+          const int en = static_cast<int>(bn_ >> 52);
+          if (!(SEG && start) && Pn > 0.0 && en > 64 && en < 1982 && (bn_ & kMant) >= lowm) {
+            hi[l] = __longlong_as_double((static_cast<long long>(en) << 52) | highm);
+            M[l] = osum_pow2(en - 1023);
+            ea[l] = en - 1023;
+          }
         }
       }
     }

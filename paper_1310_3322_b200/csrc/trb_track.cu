@@ -59,15 +59,14 @@ __device__ unsigned long long g_warpwalk[8 * 8 * 2];
 #define TRB_OSUM_COUNT(v) ++(v)
 #define TRB_OSUM_WALK_END()                                                                        \
   do {                                                                                             \
-    if (walk_on_ && G == 8) { /* by warp class: the warp's slowest lane, summed, and counted */    \
+    if (walk_on_ && G == 8) { /* by the warp's slow-path events: walk cycles summed, counted */     \
       const unsigned wm_ = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(clock64() - walk_t0_)); \
       const bool work_ = __any_sync(0xffffffffu, j0 < j1);                                         \
-      const int cls_ = !work_ ? 2 : 1;                                                \
-      const unsigned ns_ = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nslow_));          \
-      if ((threadIdx.x & 31) == 0) {                                                               \
-        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + cls_ * 2], wm_);                               \
-        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + cls_ * 2 + 1], 1ull);                          \
-        if (cls_ == 1) atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + 8], ns_);                       \
+      const unsigned ns_ = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nslow_));          \
+      if ((threadIdx.x & 31) == 0 && work_) {                                                      \
+        const int c_ = ns_ == 0 ? 0 : ns_ <= 2 ? 1 : ns_ <= 5 ? 2 : ns_ <= 10 ? 3 : ns_ <= 20 ? 4 : ns_ <= 40 ? 5 : 6; \
+        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + c_ * 2], wm_);                                 \
+        atomicAdd(&::trb::g_warpwalk[(L == 3) * 16 + c_ * 2 + 1], 1ull);                            \
       }                                                                                            \
     }                                                                                              \
     if (walk_on_ && rank == 0 && j0 < j1) {                                                        \
@@ -1664,6 +1663,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     prepare_cluster_kernel(track_spawn_kernel, smem, G);
     const int64_t items = static_cast<int64_t>(S_) * T_;
     grid_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift_kernel, smem, G)));
+    if (const char* eg = getenv("TRB_TRACK_CLUSTERS")) grid_ = std::max(1, std::min(grid_, atoi(eg)));  // (A/B)
     d_.maxN = static_cast<int64_t>(w) * h;
     // cheap tracks run on single CTAs (split mode); a CTA then owns 1/G of
     // its cluster's scratch

@@ -39,9 +39,11 @@ torch.cuda.synchronize()
 api.debug_itlog(False)
 L.trb_debug_warp_walks(buf.ctypes.data, 1)
 w = buf.astype(np.float64)
+cls = ("0", "1-2", "3-5", "6-10", "11-20", "21-40", ">40")
 for k, nm in enumerate(("histogram", "centroid")):
     b = w[16 * k:16 * k + 16]
-    for c, cn in enumerate(("fast", "general", "idle")):
-        n = max(b[2 * c + 1], 1)
-        print(f"{nm:10s} {cn:8s} warps/step {b[2 * c + 1] / steps:9.0f}  mean walk {b[2 * c] / n / 1.965e3:7.2f} us")
-    print(f"{nm:10s} general warps: mean max-lane slow events {b[8] / max(b[3], 1):.1f}")
+    print(f"{nm}: working warps by slow-path events (sum over lanes): warps/step, mean walk us")
+    for c, cn in enumerate(cls):
+        n = b[2 * c + 1]
+        if n:
+            print(f"   {cn:>6s} {n / steps:9.0f} {b[2 * c] / n / 1.965e3:8.2f}")
