@@ -1466,6 +1466,83 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
   for (int k = threadIdx.x; k < 3 * K; k += NT) out[k] = sm.cen[k];
 }
 
+// quantize_colors (quantize.hpp:43-118) for arbitrary real-valued samples:
+// the general case has no integer structure to parallelise exactly (the D^2
+// total and the Lloyd sums are order-dependent fp64 sums), so one device
+// thread runs the reference's sequential algorithm with non-contracted
+// __d*_rn arithmetic and the device mt19937_64.  Used by the public free
+// function only; the tracker's samples are pixels (integers: quantize_kernel).
+__global__ void quantize_serial_kernel(const double* __restrict__ px, int64_t n, int k, int iters, uint64_t seed,
+                                       double* __restrict__ centers, double* __restrict__ d2,
+                                       int* __restrict__ assign, double* __restrict__ sum,
+                                       int64_t* __restrict__ count, Mt64* rng) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto sq_dist3 = [](const double* a, const double* b) {
+    const double dr = xsub(a[0], b[0]), dg = xsub(a[1], b[1]), db = xsub(a[2], b[2]);
+    return xadd(xadd(xmul(dr, dr), xmul(dg, dg)), xmul(db, db));
+  };
+  rng->seed(seed);
+  const int64_t first = rng->uniform_int(0, n - 1);  // k-means++: uniform first centre
+  for (int c = 0; c < 3; ++c) centers[c] = px[3 * first + c];
+  for (int nc = 1; nc < k; ++nc) {  // D^2-weighted picks
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double best = __longlong_as_double(0x7ff0000000000000LL);
+      for (int c = 0; c < nc; ++c) {
+        const double d = sq_dist3(&px[3 * i], &centers[3 * c]);
+        best = d < best ? d : best;
+      }
+      d2[i] = best;
+      total = xadd(total, best);
+    }
+    int64_t pick = 0;
+    if (total > 0.0) {
+      const double r = xmul(rng->uniform(), total);
+      double acc = 0.0;
+      pick = n - 1;
+      for (int64_t i = 0; i < n; ++i) {
+        acc = xadd(acc, d2[i]);
+        if (acc > r) {
+          pick = i;
+          break;
+        }
+      }
+    }
+    for (int c = 0; c < 3; ++c) centers[3 * nc + c] = px[3 * pick + c];
+  }
+  for (int it = 0; it < iters; ++it) {  // Lloyd
+    bool moved = false;
+    for (int64_t i = 0; i < n; ++i) assign[i] = q_assign(centers, k, px[3 * i], px[3 * i + 1], px[3 * i + 2]);
+    for (int c = 0; c < 3 * k; ++c) sum[c] = 0.0;
+    for (int c = 0; c < k; ++c) count[c] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const int c = assign[i];
+      sum[3 * c] = xadd(sum[3 * c], px[3 * i]);
+      sum[3 * c + 1] = xadd(sum[3 * c + 1], px[3 * i + 1]);
+      sum[3 * c + 2] = xadd(sum[3 * c + 2], px[3 * i + 2]);
+      count[c] += 1;
+    }
+    for (int c = 0; c < k; ++c) {  // centres update in order (empty ones see the partial update)
+      double nc3[3];
+      if (count[c] == 0) {
+        int64_t far = 0;
+        double far_d = -1.0;
+        for (int64_t i = 0; i < n; ++i) {
+          const double d = sq_dist3(&px[3 * i], &centers[3 * assign[i]]);
+          if (d > far_d) far_d = d, far = i;
+        }
+        for (int q = 0; q < 3; ++q) nc3[q] = px[3 * far + q];
+      } else {
+        const double m = static_cast<double>(count[c]);
+        for (int q = 0; q < 3; ++q) nc3[q] = xdiv(sum[3 * c + q], m);
+      }
+      if (nc3[0] != centers[3 * c] || nc3[1] != centers[3 * c + 1] || nc3[2] != centers[3 * c + 2]) moved = true;
+      for (int q = 0; q < 3; ++q) centers[3 * c + q] = nc3[q];
+    }
+    if (!moved) break;
+  }
+}
+
 // ------------------------------------------------------------- host side
 // Per-iteration timing log (diagnostics): enable with a device buffer of
 // 2^16 pairs; read back with read_itlog().
@@ -1842,11 +1919,28 @@ void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, u
     throw Error(TRB_INVALID_ARGUMENT,
                 "quantize_colors: " + std::to_string(n) + " pixels < k=" + std::to_string(k));
   std::vector<int> ip(static_cast<size_t>(n) * 3);
-  for (int64_t i = 0; i < 3 * n; ++i) {
+  bool integral = true;
+  for (int64_t i = 0; i < 3 * n && integral; ++i) {
     const double v = pixels[i];
-    if (!(v >= 0.0 && v <= 65535.0) || v != static_cast<double>(static_cast<int>(v)))
-      throw Error(TRB_INVALID_ARGUMENT, "device quantize_colors needs integer-valued samples in [0, 65535]");
-    ip[i] = static_cast<int>(v);
+    integral = v >= 0.0 && v <= 65535.0 && v == static_cast<double>(static_cast<int>(v));
+    if (integral) ip[i] = static_cast<int>(v);
+  }
+  if (!integral) {  // general real-valued samples: the sequential device kernel
+    DevBuf dpx, dc, dd2, das, dsum, dcnt, drng;
+    dpx.alloc(sizeof(double) * 3 * n, false);
+    dc.alloc(sizeof(double) * 3 * k, false);
+    dd2.alloc(sizeof(double) * n, false);
+    das.alloc(sizeof(int) * n, false);
+    dsum.alloc(sizeof(double) * 3 * k, false);
+    dcnt.alloc(sizeof(int64_t) * k, false);
+    drng.alloc(sizeof(Mt64), false);
+    TRB_CUDA(cudaMemcpyAsync(dpx.p, pixels, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    quantize_serial_kernel<<<1, 1, 0, st>>>(dpx.as<double>(), n, k, iters, seed, dc.as<double>(), dd2.as<double>(),
+                                            das.as<int>(), dsum.as<double>(), dcnt.as<int64_t>(), drng.as<Mt64>());
+    TRB_LAUNCH_CHECK("quantize_serial_kernel");
+    TRB_CUDA(cudaMemcpyAsync(centers, dc.p, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost, st));
+    TRB_CUDA(cudaStreamSynchronize(st));
+    return;
   }
   DevBuf dpx, dout;
   dpx.alloc(sizeof(int) * ip.size(), false);

@@ -41,6 +41,24 @@ def test_quantize_colors_vs_oracle(gpu):
         assert got.reshape(-1).tobytes() == want.tobytes(), trial
 
 
+def test_quantize_colors_real_valued_vs_oracle(gpu):
+    """Real-valued samples (tracking_test.cpp:95-121: noisy clumps, uniform
+    random colours): the sequential device kernel, bit-identical centres."""
+    rng = np.random.default_rng(5)
+    clumps = np.array([[30, 30, 30], [200, 50, 50], [60, 220, 100]], float)
+    cases = [(clumps[np.arange(60) % 3] + rng.uniform(-5.0, 5.0, (60, 3)), 3, 30, 11),
+             (rng.uniform(0.0, 255.0, (40, 3)), 4, 20, 9),
+             (rng.uniform(0.0, 255.0, (700, 3)), 16, 20, 123),
+             (np.round(rng.uniform(0, 255, (300, 3))) + 0.5, 8, 20, 77)]
+    for px, k, iters, seed in cases:
+        px = np.ascontiguousarray(px)
+        want = np.zeros(3 * k)
+        O.orc_lib().orc_quantize_colors(px.ctypes.data, len(px), k, iters, seed, want.ctypes.data)
+        got = gpu.quantize_colors(px, k, iters, seed)
+        assert got.reshape(-1).tobytes() == want.tobytes(), (len(px), k)
+        assert (gpu.quantize_colors(px, k, iters, seed) == got).all()  # deterministic
+
+
 def test_quantize_degenerate_and_errors(gpu):
     px = np.tile([50.0, 60.0, 70.0], (10, 1))
     c = gpu.quantize_colors(px, 2, 20, 3)
