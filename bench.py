@@ -269,7 +269,7 @@ def ours_main(args, rank, world, local_rank):
     clips = [recipe("C5", s) for s in shard(rank, S)]
     fill = W_DEFAULT - 1
     e2e_steps = 0 if args.no_e2e else K
-    n_frames = fill + Wm + K + K + e2e_steps
+    n_frames = fill + Wm + K + K
     assert n_frames <= 300, "recipe clips have 300 frames"
     frames = make_frames(trb, clips, n_frames, stream)
     st = trb.Streams(S, WIDTH, HEIGHT, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), device=local_rank)
@@ -293,6 +293,7 @@ def ours_main(args, rank, world, local_rank):
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
+    t_timed0 = t
     ev0.record(stream)
     for _ in range(K):
         st.step_device(ptrs[t], stream.cuda_stream)
@@ -339,10 +340,19 @@ def ours_main(args, rank, world, local_rank):
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H timed
     e2e = None
     if e2e_steps:
-        # pinned host frames and per-step pinned result rows; the pipelined
-        # API overlaps step k+1's H2D with step k's kernels, every step's
-        # result (S blob counts) is read back to the host
-        host = [[frames[s, t + k].cpu().pin_memory().numpy() for s in range(S)] for k in range(e2e_steps)]
+        # Same work as `value`: a second handle is advanced through the same
+        # fill + warm-up frames, then the SAME K frames as the device-timed
+        # region go through the host API.  Pinned host frames and per-step
+        # pinned result rows; the pipelined API overlaps step k+1's H2D with
+        # step k's kernels, every step's result (S blob counts) is read back.
+        st.synchronize()
+        del st
+        st = trb.Streams(S, WIDTH, HEIGHT, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), device=local_rank)
+        with torch.cuda.stream(stream):
+            for k in range(t_timed0):
+                st.step_device(ptrs[k], stream.cuda_stream)
+        torch.cuda.synchronize()
+        host = [[frames[s, t_timed0 + k].cpu().pin_memory().numpy() for s in range(S)] for k in range(e2e_steps)]
         res = torch.zeros((e2e_steps, S), dtype=torch.int32).pin_memory().numpy()
         barrier()
         torch.cuda.synchronize()
@@ -352,9 +362,9 @@ def ours_main(args, rank, world, local_rank):
         st.synchronize()
         torch.cuda.synchronize()
         secs = max_over_ranks(time.perf_counter() - t0, world, dev)
-        t += e2e_steps
         e2e = {"value": aggregate_fps(S, world, e2e_steps, secs), "unit": "frames/s", "h2d_bytes_per_step": S * PX,
-               "d2h_bytes_per_step": 4 * S}
+               "d2h_bytes_per_step": 4 * S,
+               "frames": "the device-timed steps' frames, through trb_streams_step_host_async (second handle)"}
     st.synchronize()
 
     value = aggregate_fps(S, world, K, ms / 1e3)
