@@ -56,7 +56,13 @@ __device__ __forceinline__ uint8_t thr_mask(uint32_t v, uint32_t bg, int thr) {
 
 }  // namespace
 
-// One thread = 16 pixels.  grid.y = stream.
+// One thread = kMotionItems x 16 pixels (block-strided 16-pixel chunks, so
+// every load / store instruction of a warp is one coalesced 512-byte run).
+// grid.y = stream.
+#ifndef TRB_MOTION_ITEMS
+#define TRB_MOTION_ITEMS 1
+#endif
+constexpr int kMotionItems = TRB_MOTION_ITEMS;
 template <int CH, typename SumT>
 __global__ void __launch_bounds__(256) motion_mean_kernel(MotionArgs a) {
   const int s = blockIdx.y;
@@ -64,7 +70,9 @@ __global__ void __launch_bounds__(256) motion_mean_kernel(MotionArgs a) {
   uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * a.px;
   SumT* __restrict__ sums = reinterpret_cast<SumT*>(a.sums) + static_cast<int64_t>(s) * a.px;
   uint8_t* __restrict__ mask = a.mask + static_cast<int64_t>(s) * a.px;
-  const int64_t chunk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int item = 0; item < kMotionItems; ++item) {
+  const int64_t chunk = (static_cast<int64_t>(blockIdx.x) * kMotionItems + item) * blockDim.x + threadIdx.x;
   const int64_t p0 = chunk * 16;
   if (p0 >= a.px) return;
   if (p0 + 16 <= a.px && a.vec_ok) {
@@ -110,6 +118,7 @@ __global__ void __launch_bounds__(256) motion_mean_kernel(MotionArgs a) {
         mask[p] = thr_mask(v, bg, a.threshold);
       }
     }
+  }
   }
 }
 
@@ -337,7 +346,7 @@ __global__ void synth_raster_kernel(uint8_t* out, int w, int h, int ch, uint8_t 
 // ---------------------------------------------------------------------------
 void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st) {
   const int64_t chunks = ceil_div64(a.px, 16);
-  dim3 grid(static_cast<unsigned>(ceil_div64(chunks, 256)), n_streams);
+  dim3 grid(static_cast<unsigned>(ceil_div64(chunks, 256 * kMotionItems)), n_streams);
   if (channels == 1) {
     if (wide_sums) motion_mean_kernel<1, uint32_t><<<grid, 256, 0, st>>>(a);
     else motion_mean_kernel<1, uint16_t><<<grid, 256, 0, st>>>(a);
