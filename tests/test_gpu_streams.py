@@ -175,3 +175,28 @@ def test_streams_overlapped_steps_without_sync(gpu):
     assert logs["1"] == logs["0"]
     out, log, _ = O.run_pipeline_cpu(clips[0], frames[0], MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), "orc")
     assert logs["1"][0] == log.tobytes()
+
+
+def test_streams_overlap_profiling_switches(gpu):
+    """Switching a handle between the overlapped path and the in-stream
+    (per-stage profiling) path every few steps, device and host-async steps
+    mixed, no host sync between steps: the track log still equals the
+    oracle's (the switch joins the tracker stream before in-stream tracking)."""
+    import torch
+    clip = recipe("C5", 7)
+    n = 100
+    frames = O.orc_frames(clip, n)[0]
+    dev = torch.from_numpy(frames).cuda()
+    host = [torch.from_numpy(frames[t]).pin_memory().numpy() for t in range(n)]
+    st = gpu.Streams(1, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+    stream = torch.cuda.Stream()
+    for t in range(n):
+        st.profile((t // 3) % 2 == 1)
+        if t % 5 == 4:
+            st.step_host_async([host[t]], None, stream.cuda_stream)
+        else:
+            st.step_device([dev[t].data_ptr()], stream.cuda_stream)
+    st.profile(False)
+    st.synchronize()
+    _, log, _ = O.run_pipeline_cpu(clip, frames, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), "orc")
+    assert st.log(0).tobytes() == log.tobytes()
