@@ -147,7 +147,11 @@ __global__ void __launch_bounds__(256) ccl_occupancy_kernel(CclArgs a, int vec_o
       for (int c = 0; c < kTileW && gx0 + c < a.w; ++c) any |= row[c] != 0;
     }
   }
-  if (__any_sync(0xffffffffu, any) && lane == 0) a.tile_list[atomicAdd(a.tile_count, 1)] = static_cast<int>(tile);
+  const bool fg = __any_sync(0xffffffffu, any);
+  if (lane == 0) {
+    if (fg) a.tile_list[atomicAdd(a.tile_count, 1)] = static_cast<int>(tile);
+    a.tile_state[tile] = static_cast<uint8_t>((a.tile_state[tile] & 2u) | (fg ? 1u : 0u));
+  }
 }
 
 __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
@@ -449,27 +453,35 @@ __global__ void __launch_bounds__(256) ccl_assign_kernel(CclArgs a) {
 }
 
 // ------------------------------------------------------------------ final
-__global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a, int vec_ok) {
+// Final labels, tile by tile (one warp per 32x32 tile, lane = column, so
+// every row is one coalesced 128-byte store): tiles holding foreground get
+// their labels; tiles whose labels were written on an earlier frame but hold
+// none now are cleared; untouched background tiles (most of a frame) are
+// skipped — the plane stays zero there from the allocation on.
+__global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a) {
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tiles) return;
   const int s = blockIdx.y;
+  const int tile = s * n_tiles + t;
+  const unsigned st = a.tile_state[tile];
+  if (!(st & 3u)) return;
+  const bool fg = st & 1u;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const int gx = tx * kTileW + lane, gy0 = ty * kTileH;
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   const int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
   int32_t* labels = a.labels + static_cast<int64_t>(s) * a.px;
   const int32_t* dense = a.slots.dense + static_cast<int64_t>(s) * a.slot_cap;
-  const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
-  if (p0 >= a.px) return;
-  if (vec_ok && p0 + 16 <= a.px) {
-    const uint4 mq = *reinterpret_cast<const uint4*>(mask + p0);
-    const uint8_t* m = reinterpret_cast<const uint8_t*>(&mq);
-    int4 out[4];
-    int* o = reinterpret_cast<int*>(out);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) o[i] = m[i] ? dense[labg[p0 + i]] : 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) __stcs(reinterpret_cast<int4*>(labels + p0) + j, out[j]);
-  } else {
-    const int64_t p1 = min(p0 + 16, a.px);
-    for (int64_t p = p0; p < p1; ++p) labels[p] = mask[p] ? dense[labg[p]] : 0;
+  const int y1 = min(a.h, gy0 + kTileH);
+  if (gx < a.w) {
+    for (int gy = gy0; gy < y1; ++gy) {
+      const int64_t p = static_cast<int64_t>(gy) * a.w + gx;
+      labels[p] = (fg && mask[p]) ? dense[labg[p]] : 0;
+    }
   }
+  if (lane == 0) a.tile_state[tile] = fg ? 3u : 0u;
 }
 
 int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
@@ -498,8 +510,7 @@ int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   TRB_LAUNCH_CHECK("ccl_scan_kernel");
   ccl_assign_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
   TRB_LAUNCH_CHECK("ccl_assign_kernel");
-  const int vec_ok = (a.px % 16 == 0);
-  ccl_final_kernel<<<dim3(static_cast<unsigned>(ceil_div64(ceil_div64(a.px, 16), 256)), S), 256, 0, st>>>(a, vec_ok);
+  ccl_final_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 32, 256)), S), 256, 0, st>>>(a);
   TRB_LAUNCH_CHECK("ccl_final_kernel");
   return 8;
 }

@@ -149,6 +149,7 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
     nblobs_[b].alloc(sizeof(int32_t) * S);
   }
   tiles_.alloc(sizeof(int32_t) * (static_cast<size_t>(tx) * ty * S + 1), false);
+  tile_state_.alloc(static_cast<size_t>(tx) * ty * S);  // zeroed: no tile labelled yet (labels_ is zeroed too)
 
   CclArgs& a = args_;
   a.labg = labg_.as<int32_t>();
@@ -183,6 +184,7 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   a.blob_cap = blob_cap_;
   a.tile_count = tiles_.as<int32_t>();
   a.tile_list = a.tile_count + 1;
+  a.tile_state = tile_state_.as<uint8_t>();
 }
 
 void CclState::run(const uint8_t* mask, cudaStream_t st, int* launches) {

@@ -100,7 +100,7 @@ class CclState {
   CclArgs args_{};
   int S_, w_, h_;
   int64_t px_, slot_cap_, blob_cap_;
-  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_[2], nblobs_[2], tiles_;
+  DevBuf labg_, labels_, slots_, nslots_, rowcount_, bitmap_, blobs_[2], nblobs_[2], tiles_, tile_state_;
   int cur_ = 0;
 };
 

@@ -84,6 +84,7 @@ struct CclArgs {
   int32_t* nblobs;      // [S]
   int32_t* tile_list;   // [S * tiles] tiles holding foreground (s * tiles + ty * tiles_x + tx)
   int32_t* tile_count;  // [1]
+  uint8_t* tile_state;  // [S * tiles] bit 0: holds foreground this frame; bit 1: its labels may be nonzero
 };
 
 // Launches the full CCL + blob-statistics chain; returns launches issued.
