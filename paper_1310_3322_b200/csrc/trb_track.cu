@@ -1035,7 +1035,7 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
 // CTA's 1/G share of the cluster scratch.
 __device__ __forceinline__ bool split_class(const TrackDev& d, int64_t g) {
   const int64_t area = static_cast<int64_t>(d.w[g]) * d.h[g];
-  const double est = max(1, d.iters[g]) * (30.0 + 0.0141 * static_cast<double>(area));
+  const double est = max(1, d.iters[g]) * (d.split_fix + d.split_perpx * static_cast<double>(area));
   return d.G > 1 && est < d.split_us && area <= ((d.maxN / d.G) & ~15LL);
 }
 
@@ -1055,7 +1055,7 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     // ~30k px + window area); 4 buckets per octave, small index = costly.
     // Split-class tracks go after every cluster-class one.
     const unsigned cost =
-        static_cast<unsigned>(max(d.iter_floor, d.iters[g])) * static_cast<unsigned>(30000 + max(1, d.w[g] * d.h[g]));
+        static_cast<unsigned>(max(d.iter_floor, d.iters[g])) * static_cast<unsigned>(d.order_fix + max(1, d.w[g] * d.h[g]));
     const int lz = __clz(cost);
     const int sub = lz <= 29 ? static_cast<int>((cost >> (29 - lz)) & 3u) : 0;
     return (split_class(d, g) ? 128 : 0) + 4 * lz + (3 - sub);
@@ -1746,6 +1746,13 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     // its cluster's scratch
     const char* es = getenv("TRB_SPLIT_US");
     d_.split_us = es ? atof(es) : 300.0;
+    auto envf = [](const char* k, double dflt) {
+      const char* e = getenv(k);
+      return e ? atof(e) : dflt;
+    };
+    d_.split_fix = envf("TRB_SPLIT_FIX", 30.0);
+    d_.split_perpx = envf("TRB_SPLIT_PERKPX", 14.1) * 1e-3;
+    d_.order_fix = static_cast<int>(envf("TRB_ORDER_FIX", 10000.0));  // A/B: 10k px ahead of 0, 5k, 30k, 65k
     const char* ef = getenv("TRB_ITER_FLOOR");
     d_.iter_floor = ef ? std::max(1, atoi(ef)) : 6;  // iteration history is noisy: order mostly by area
     d_.G = G;

@@ -63,6 +63,8 @@ struct TrackDev {
   int G;               // CTAs per cluster
   int iter_floor;      // scheduling: iterations assumed at least
   double split_us;     // tracks estimated below this (single-CTA us) run in split mode
+  double split_fix, split_perpx;  // single-CTA cost model: us per iteration + us per window pixel
+  int order_fix;       // queue order: cost = iterations x (order_fix + window px)
   // per-cluster scratch (breakpoint list, partitioned weights, bin cache)
   unsigned char* scratch;
   size_t scratch_stride;

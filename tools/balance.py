@@ -21,7 +21,7 @@ from paper_1310_3322_b200.synth import recipe  # noqa: E402
 S = 64
 stream = torch.cuda.Stream()
 clips = [recipe("C5", s) for s in range(S)]
-n = 93 + 6
+n = 93 + 12
 frames = bench.make_frames(trb, clips, n, stream)
 st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
 for t in range(93):
@@ -31,7 +31,22 @@ L = api.lib()
 L.trb_debug_cta_times.argtypes = [C.c_void_p, C.c_int]
 buf = np.zeros(2048, np.uint64)
 api.debug_itlog(True)
-for t in range(93, n):
+# back-to-back steps (the bench's issue pattern, step overlap active): the
+# per-CTA [busy, last end] accumulate over all steps, so also run them one by
+# one below for per-step spans
+L.trb_debug_cta_times(buf.ctypes.data, 1)
+t_wall = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+t_wall[0].record(stream)
+for t in range(93, 99):
+    st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
+st.join(stream.cuda_stream)
+t_wall[1].record(stream)
+torch.cuda.synchronize()
+L.trb_debug_cta_times(buf.ctypes.data, 1)
+busy = buf[0::2].astype(np.float64)
+print(f"back-to-back: 6 steps in {t_wall[0].elapsed_time(t_wall[1]):.2f} ms; mean-shift CTA busy "
+      f"{busy[busy > 0].mean() / 1e3 / 6:.0f} us per step per CTA")
+for t in range(99, n):
     L.trb_debug_cta_times(buf.ctypes.data, 1)
     st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)
     torch.cuda.synchronize()
