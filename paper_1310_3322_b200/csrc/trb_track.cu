@@ -320,12 +320,6 @@ struct BinsSrc {
   }
 };
 static_assert(BinsSrc::kRing * 16 * NT <= kOsumStageBytes, "staging ring exceeds the gather list");
-// physical index (in doubles) of partitioned element `pos` for chunk size C
-__device__ __forceinline__ int64_t bins_src_index(int pos, const UDiv32& divC, int C, int GT) {
-  const int g = static_cast<int>(divC.div(static_cast<uint32_t>(pos)));
-  const int i = pos - g * C;
-  return (static_cast<int64_t>(i >> 1) * GT + g) * 2 + (i & 1);
-}
 
 __device__ __forceinline__ unsigned u4_byte(const uint4& u, int k) {
   const unsigned lo = (k & 4) ? u.y : u.x, hi = (k & 4) ? u.w : u.z;
@@ -517,18 +511,34 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     const uint32_t* bw = reinterpret_cast<const uint32_t*>(scr.bins) + gt;
     uint32_t word = bw[0], wnext = bw[GT];  // (slack past N)
     bw += 2 * GT;
-    // vals in BinsSrc's interleaved layout for its chunk size
+    // vals in BinsSrc's interleaved layout for its chunk size: a sequence
+    // position p lives in chunk g = p / Cv at offset i = p % Cv.  The
+    // cursors carry (g, i) and advance incrementally (no division per
+    // store): per bin packed g << 20 | i in shared memory (Cv < 2^20, g <
+    // 2^11), the total segment's in registers.
     const int nseq = sm.binoff[NB], Cv = BinsSrc::chunk(nseq, GT);
     const UDiv32 divC = UDiv32::make(static_cast<uint32_t>(max(1, Cv)));
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t pos = static_cast<uint32_t>(sm.cnt[b * NT_ + t]);
+      const uint32_t g = divC.div(pos);
+      sm.cnt[b * NT_ + t] = static_cast<int>((g << 20) | (pos - g * static_cast<uint32_t>(Cv)));
+    }
+    const uint32_t cK = static_cast<uint32_t>(sm.cnt[K * NT_ + t]);
+    int gT = static_cast<int>(cK >> 20), iT = static_cast<int>(cK & 0xfffffu);
+    auto at = [&](int g, int i) { return (static_cast<int64_t>(i >> 1) * GT + g) * 2 + (i & 1); };
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
       const int b = (word >> (8 * (j & 3))) & 0xffu;
       if ((j & 3) == 3) word = wnext, wnext = *bw, bw += GT;
       if (w > 0.0) {
-        TRB_CHECK(b < K && sm.cnt[b * NT_ + t] < 2 * N && sm.cnt[K * NT_ + t] < 2 * N, "partition scatter", b,
-                  sm.cnt[K * NT_ + t]);
-        scr.vals[bins_src_index(sm.cnt[b * NT_ + t]++, divC, Cv, GT)] = w;
-        scr.vals[bins_src_index(sm.cnt[K * NT_ + t]++, divC, Cv, GT)] = w;
+        TRB_CHECK(b < K, "partition scatter", b, j);
+        const uint32_t cb = static_cast<uint32_t>(sm.cnt[b * NT_ + t]);
+        int g = static_cast<int>(cb >> 20), i = static_cast<int>(cb & 0xfffffu);
+        scr.vals[at(g, i)] = w;
+        if (++i == Cv) i = 0, ++g;
+        sm.cnt[b * NT_ + t] = static_cast<int>((static_cast<uint32_t>(g) << 20) | static_cast<uint32_t>(i));
+        scr.vals[at(gT, iT)] = w;
+        if (++iT == Cv) iT = 0, ++gT;
       }
       if (++xx == ww) xx = 0, ++yy;
     }
