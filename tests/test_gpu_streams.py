@@ -200,3 +200,26 @@ def test_streams_overlap_profiling_switches(gpu):
     st.synchronize()
     _, log, _ = O.run_pipeline_cpu(clip, frames, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), "orc")
     assert st.log(0).tobytes() == log.tobytes()
+
+
+def test_streams_c4_4k_end_to_end(gpu):
+    """BASELINE configs[3] (3840x2160, 50 blobs, crossing paths): masks,
+    labels and the track log of the batched device path vs the oracle over
+    the window fill and 7 steady frames."""
+    import torch
+    clip = recipe("C4")
+    n = 98
+    frames = O.orc_frames(clip, n)[0]
+    dev = torch.from_numpy(frames).cuda()
+    st = gpu.Streams(1, clip.width, clip.height, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+    masks, labels = [], []
+    for t in range(n):
+        st.step_device([dev[t].data_ptr()])
+        if st.has_output:
+            masks.append(sha(st.mask(0)))
+            labels.append(sha(st.labels(0)))
+    st.synchronize()
+    out, log, _ = O.run_pipeline_cpu(clip, frames, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(), "orc")
+    assert masks == [sha(m) for _, m, _, _ in out]
+    assert labels == [sha(l_) for _, _, l_, _ in out]
+    assert len(log) > 0 and st.log(0).tobytes() == log.tobytes()
