@@ -17,7 +17,7 @@ S, K = 64, 10
 clips = [recipe("C5", s) for s in range(S)]
 base = torch.cuda.Stream()
 frames = bench.make_frames(trb, clips, 93 + 3 + K, base)
-for H in (1, 2, 4, 1, 2):
+for H in (1, 2, 1, 2, 1, 2, 4):
     per = S // H
     hs = [trb.Streams(per, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG()) for _ in range(H)]
     cs = [torch.cuda.Stream() for _ in range(H)]
