@@ -295,9 +295,10 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   // NB: s.result is NOT touched before the barriers below — callers read the
   // previous run's results right up to this call (CTA 0 rewrites every
   // result, including empty segments, in phase D).
+  // (no barrier: nbp / bad are first used after phase A's barriers, and the
+  // previous run's readers finished before its closing barrier)
   if (t < 3) s.nbp[t] = 0;
   if (t < 4) s.bad[t] = 0;
-  __syncthreads();
 
   // ---------------- phase A: approximate (segmented) prefix at chunk starts
   int af = 0;
@@ -696,8 +697,8 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       if (bad) atomicOr(&s.bad[0], 8);
     }
   }
-  __syncthreads();
-  // fold the carried-in piece into each thread's first breakpoint
+  // fold the carried-in piece into each thread's first breakpoint (its own
+  // record: no barrier needed before, one after — the ranking reads all)
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     if (firstbp[l] >= 0) {
