@@ -49,9 +49,9 @@ __device__ unsigned long long g_warpwalk[8 * 8 * 2];
   const long long walk_t0_ = walk_on_ ? clock64() : 0;       \
   long long walk_t1_ = walk_t0_;                                 \
   unsigned long long nslow_ = 0, nbp_ = 0
-// per-element timestamps of global thread 0's walks (L == 3 only): g_phase[192 + k]
+// per-element timestamps of a typical walking thread (CTA 1, thread 100; L == 3 only): g_phase[192 + k]
 #define TRB_OSUM_ELEM_TRACE(k, dep) \
-  if (walk_on_ && L == 3 && rank == 0 && threadIdx.x == 0 && (k) < 32) \
+  if (walk_on_ && L == 3 && rank == 1 && threadIdx.x == 100 && (k) < 32) \
     ::trb::g_phase[192 + (k)] = clock64() - walk_t0_ + ((dep) != (dep) ? 1 : 0)
 // time to the first element's data (cursor start-up); `dep` forces the wait
 #define TRB_OSUM_WALK_FIRST(cond, dep) \

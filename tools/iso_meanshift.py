@@ -42,4 +42,4 @@ w = ph[:, 40:56].sum(axis=0)
 print(f"  walk per thread: hist {w[1] / max(1, w[12]) / 1.9e3:.2f} us, cent {w[3] / max(1, w[13]) / 1.9e3:.2f} us; "
       f"startup hist {w[14] / max(1, w[12]) / 1.9e3:.2f} cent {w[15] / max(1, w[13]) / 1.9e3:.2f}")
 tr = api.debug_phases()[3, :32]  # g_phase[192..223]: last centroid walk of thread 0
-print("thread-0 centroid walk, cycles at each element (last run):", [int(x) for x in tr[:20]])
+print("thread 100 of CTA 1, centroid walk, cycles at each element (last run):", [int(x) for x in tr[:20]])
