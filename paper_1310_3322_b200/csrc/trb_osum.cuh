@@ -72,62 +72,34 @@ constexpr int kOsumGather = 480;  // cluster-wide breakpoints gathered in CTA 0 
 constexpr int kEmptyE = INT_MIN;
 
 // ----------------------------------------------------------- piece algebra
-// A piece maps the significand X of the running sum before its first step
-// (binade e) to the significand after its last step (binade e + m):
-//     F(X) = [tie ? E(H(X) + B) : H(X)] + D,   H(X) = (X + A) >> m,
-// normalised to 0 <= A < 2^m.  m counts binade crossings inside the piece:
-// a step carrying S from binade e to e+1 that adds a with a/u_e = k + f,
-// f > 0, is X -> (X + k + 1) >> 1 (the exact (X + k + f)/2 on the doubled
-// grid rounded to nearest: f/2 < 1/2 rounds down for even X + k, (1+f)/2 >
-// 1/2 rounds up for odd); f = 0 crossings (a possible tie) stay breakpoints.
-// The family is closed under composition (floor((floor(n/2^a) + c)/2^b) =
-// floor((n + c 2^a)/2^(a+b)), E(y) = 2 ceil(y/2), E(E(y) + c) = E(y) + E(c))
-// and the normalisation keeps every term inside int64 for m <= kMaxM.
 struct Piece {
-  long long A, B, D;
-  int e;    // binade before the first step, kEmptyE = identity
-  int tie;  // E applied (see above)
-  int m;    // binade crossings
+  long long A, B;
+  int e;    // binade of every step in the piece, kEmptyE = identity
+  int tie;  // 0: X -> X + B ; 1: X -> E(X + A) + B
 };
-constexpr int kMaxM = 60;
 
-__device__ __forceinline__ Piece piece_identity() { return Piece{0, 0, 0, kEmptyE, 0, 0}; }
+__device__ __forceinline__ Piece piece_identity() { return Piece{0, 0, kEmptyE, 0}; }
 __device__ __forceinline__ long long up_even(long long y) { return y + (y & 1); }
 
-// p then q; *bad is set when q does not start where p ends (or m overflows)
+// p then q; *bad is set when two non-empty pieces disagree on the binade
 __device__ __forceinline__ Piece compose(const Piece& p, const Piece& q, int* bad) {
   if (q.e == kEmptyE) return p;
   if (p.e == kEmptyE) return q;
-  if (p.e + p.m != q.e || p.m + q.m > kMaxM) *bad = 1;
+  if (p.e != q.e) *bad = 1;
   Piece r;
   r.e = p.e;
-  r.m = p.m + q.m;
-  const long long c = p.D + q.A;  // added to p's output before q's shift
-  if (p.tie && q.m == 0) {        // q.A == 0: q is an add or an add + tie after p's tie
-    r.A = p.A, r.B = p.B, r.tie = 1, r.D = (q.tie ? up_even(c + q.B) : c) + q.D;
-    return r;
+  if (!q.tie) {
+    r.tie = p.tie, r.A = p.A, r.B = p.B + q.B;
+  } else if (!p.tie) {
+    r.tie = 1, r.A = p.B + q.A, r.B = q.B;
+  } else {
+    r.tie = 1, r.A = p.A, r.B = up_even(p.B + q.A) + q.B;
   }
-  long long A, Q;  // H_r(X) + Q is q's shifted input
-  if (!p.tie) {    // ((X + A_p) >> m_p) + c, then >> m_q
-    A = p.A + ((c & ((1LL << q.m) - 1)) << p.m);
-    Q = c >> q.m;
-  } else {  // (E(Z) + c) >> m_q = (ceil(Z/2) + (c >> 1)) >> (m_q - 1), Z = H_p + B_p
-    const long long t1 = p.B + 1;
-    const long long A1 = p.A + ((t1 & 1) << p.m);
-    const long long t2 = (t1 >> 1) + (c >> 1);
-    const int sh = q.m - 1;
-    A = A1 + ((t2 & ((1LL << sh) - 1)) << (p.m + 1));
-    Q = t2 >> sh;
-  }
-  r.A = A, r.tie = q.tie;
-  if (q.tie) r.B = q.B + Q, r.D = q.D;
-  else r.B = 0, r.D = q.D + Q;
   return r;
 }
 
 __device__ __forceinline__ long long apply(const Piece& p, long long X) {
-  const long long h = (X + p.A) >> p.m;
-  return (p.tie ? up_even(h + p.B) : h) + p.D;
+  return p.tie ? up_even(X + p.A) + p.B : X + p.B;
 }
 
 __device__ __forceinline__ int osum_exp(double x) {  // binade of a positive normal double, else kEmptyE
@@ -231,14 +203,13 @@ __device__ __forceinline__ void osum_step_safe(Piece& pc, double a, double M, in
   const double d = xsub(a, xsub(y, M));
   const long long r = __double_as_longlong(y) - __double_as_longlong(M);
   const double hu = __longlong_as_double(__double_as_longlong(M) - (53LL << 52));  // u/2
-  if (fabs(d) == hu) {  // a/u = k + 1/2: X -> E(X + k)
+  if (fabs(d) == hu) {  // a/u = k + 1/2
     Piece q;
-    q.e = e, q.tie = 1, q.m = 0, q.A = 0, q.B = d > 0.0 ? r : r - 1, q.D = 0;
+    q.e = e, q.tie = 1, q.A = d > 0.0 ? r : r - 1, q.B = 0;
     pc = compose(pc, q, &tbad);
-  } else if (pc.e == kEmptyE) {
-    pc.D = r, pc.e = e;
   } else {
-    pc.D += r;
+    pc.B += r;
+    pc.e = e;
   }
 }
 
@@ -247,10 +218,8 @@ __device__ __forceinline__ Piece shfl_up_piece(const Piece& p, int o) {
   Piece r;
   r.A = __shfl_up_sync(0xffffffffu, p.A, o);
   r.B = __shfl_up_sync(0xffffffffu, p.B, o);
-  r.D = __shfl_up_sync(0xffffffffu, p.D, o);
   r.e = __shfl_up_sync(0xffffffffu, p.e, o);
   r.tie = __shfl_up_sync(0xffffffffu, p.tie, o);
-  r.m = __shfl_up_sync(0xffffffffu, p.m, o);
   return r;
 }
 
@@ -549,10 +518,7 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
         }
         if (ok) {
 #pragma unroll
-          for (int l = 0; l < L; ++l) {
-            if (pc[l].e == kEmptyE) pc[l].e = ea[l], pc[l].D = 0;
-            pc[l].D += r[l], P[l] = Pn[l];
-          }
+          for (int l = 0; l < L; ++l) pc[l].B += r[l], pc[l].e = ea[l], P[l] = Pn[l];
           continue;
         }
       }
@@ -601,32 +567,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
             safe = true;
           }
         }
-        // a binade crossing e -> e+1 with both prefixes inside their binades
-        // (margins): the step is the piece X -> (X + k + 1) >> 1 when a/u_e
-        // = k + f has f > 0 (f = 0 may round to even: breakpoint)
-        bool crossed = false;
-        if (!safe && Pp > 0.0 && !(SEG && start) && pc[l].m < kMaxM) {
-          const long long bp_ = __double_as_longlong(Pp), bn_ = __double_as_longlong(Pn);
-          const int eb = static_cast<int>(bp_ >> 52);
-          if (static_cast<int>(bn_ >> 52) == eb + 1 && eb > 64 && eb < 1981 && (bp_ & kMant) >= lowm &&
-              (bp_ & kMant) <= highm && (bn_ & kMant) >= lowm && (bn_ & kMant) <= highm) {
-            const int e = eb - 1023;
-            const double tq = xmul(vl, osum_pow2(52 - e));  // a / u_e, exact (power-of-two scaling)
-            const long long k = __double2ll_rd(tq);
-            if (static_cast<double>(k) != tq) {
-              Piece q;
-              q.e = e, q.m = 1, q.tie = 0, q.A = (k + 1) & 1, q.B = 0, q.D = (k + 1) >> 1;
-              pc[l] = compose(pc[l], q, &tbad);
-              hi[l] = __longlong_as_double((static_cast<long long>(eb + 1) << 52) | highm);
-              M[l] = osum_pow2(e + 1);
-              ea[l] = e + 1;
-              crossed = true;
-            }
-          }
-        }
         if (safe) {
           osum_step_safe(pc[l], vl, M[l], ea[l], tbad);
-        } else if (!crossed) {
+        } else {
           TRB_OSUM_COUNT(nbp_);
           const int idx = atomicAdd(&s.nbp[l], 1);
           if (idx < cap_lane) {
@@ -833,14 +776,12 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
       auto run_piece = [&](const Piece& p) {
         if (p.e == kEmptyE) return;
         const int pe = (p.e > -1000 && p.e < 1000) ? p.e : 0;
-        const int pm = (p.m >= 0 && p.m <= kMaxM && pe + p.m < 1000) ? p.m : 0;
-        ok &= osum_exp(S) == pe && pm == p.m;
-        // S = X * 2^(pe-52) with X its 53-bit significand: integer ops only;
-        // the result lives in binade pe + m
+        ok &= osum_exp(S) == pe;
+        // S = X * 2^(pe-52) with X its 53-bit significand: integer ops only
         const long long X = (__double_as_longlong(S) & kMant) | (1LL << 52);
         const long long X2 = apply(p, X);
         ok &= X2 >= (1LL << 52) && X2 < (1LL << 53);
-        S = __longlong_as_double((static_cast<long long>(pe + pm + 1023) << 52) | (X2 & kMant));
+        S = __longlong_as_double((static_cast<long long>(pe + 1023) << 52) | (X2 & kMant));
       };
       for (int q = q0; q < q1; ++q) {
         TRB_CHECK(q >= 0 && q < cap_g, "replay read", q, n);
