@@ -41,6 +41,22 @@ def test_no_device_fails_loudly_without_gpu():
         trb.label_blocked(np.zeros(64, np.uint8), 8, 8)
 
 
+def test_argument_errors_before_any_device_work():
+    """New entry points reject bad arguments with the C ABI's status codes
+    (1 = invalid argument) before touching a device."""
+    L = trb.lib()
+    L.trb_streams_join.argtypes = [C.c_void_p, C.c_void_p]
+    assert L.trb_streams_join(None, None) == 1
+    assert b"null argument" in L.trb_last_error()
+    L.trb_morph_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    buf = C.c_void_p(1)
+    assert L.trb_morph_device(None, buf, 16, 16, 1, 3, None) == 1
+    assert L.trb_morph_device(buf, buf, 0, 16, 1, 3, None) == 1
+    assert b"positive dimensions" in L.trb_last_error()
+    assert L.trb_morph_device(buf, buf, 16, 16, 1, 9, None) == 1
+    assert b"unknown morphology op" in L.trb_last_error()
+
+
 def test_config_validation_messages():
     L = trb.lib()
     assert L.trb_motion_config_validate(C.byref(MOTION_CFG(window=1))) == 2
