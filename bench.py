@@ -401,7 +401,9 @@ def ours_main(args, rank, world, local_rank):
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": ms_achieved / peak,
                 "traffic": dram_traffic("meanshift_dram_bytes.json"), "bytes_per_launch": ms_bytes,
                 "note": "exact-order fp64 sums (sequential-sum reproduction) make this kernel latency/"
-                        "barrier bound, not bandwidth bound; see DESIGN.md"}
+                        "barrier bound, not bandwidth bound: ncu IPC ~1.2 of 4, ~26% of warp-stall samples "
+                        "in cluster-barrier waits, ~550 cycles per element-walk step on an idle GPU; "
+                        "profiles/r01_meanshift_ncu_full.txt, DESIGN.md 3.4"}
     path_gbs = PATH_BYTES_PER_PX * S * PX / (ms / K / 1e3) / 1e9
     line = {
         "metric": "frames/sec (1080p, device-timed) motion+segment+track", "value": value, "unit": "frames/s",
