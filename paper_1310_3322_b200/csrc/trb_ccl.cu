@@ -125,6 +125,14 @@ __device__ __forceinline__ int run_start_at(uint32_t starts, int p) {  // start 
   return 31 - __clz(x);
 }
 
+// Tile-list entries carry (stream, tile x, tile y) packed, so the list
+// walkers need no integer division: s < 2^11, tx, ty < 2^10 (checked on
+// the host, CclState).
+__device__ __forceinline__ int tile_pack(int s, int tx, int ty) { return (s << 20) | (ty << 10) | tx; }
+__device__ __forceinline__ void tile_unpack(int v, int& s, int& tx, int& ty) {
+  s = v >> 20, ty = (v >> 10) & 1023, tx = v & 1023;
+}
+
 // Tiles holding foreground: one warp per 32x32 tile (lane = row, 32 bytes
 // per lane), appended to a compact list that the local and seam kernels
 // walk — most of a frame is background (C5: ~8 % foreground).
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(256) ccl_occupancy_kernel(CclArgs a, int vec_o
   }
   const bool fg = __any_sync(0xffffffffu, any);
   if (lane == 0) {
-    if (fg) a.tile_list[atomicAdd(a.tile_count, 1)] = static_cast<int>(tile);
+    if (fg) a.tile_list[atomicAdd(a.tile_count, 1)] = tile_pack(s, tx, ty);
     a.tile_state[tile] = static_cast<uint8_t>((a.tile_state[tile] & 2u) | (fg ? 1u : 0u));
   }
 }
@@ -163,14 +171,33 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   __shared__ int n_comp, slot_base_id;
 
   const int n_list = *a.tile_count;
-  const int n_tiles = a.tiles_x * a.tiles_y;
+  const int w = threadIdx.x >> 5, c = threadIdx.x & 31;
+  // this thread's 4 mask bytes of a listed tile (rows w, w+8, w+16, w+24)
+  auto load_rows = [&](int it, uint32_t& bits) {
+    bits = 0;
+    if (it >= n_list) return;
+    int s_, tx_, ty_;
+    tile_unpack(a.tile_list[it], s_, tx_, ty_);
+    const uint8_t* m_ = a.mask + static_cast<int64_t>(s_) * a.px;
+    const int gx_ = tx_ * kTileW + c;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int gy_ = ty_ * kTileH + w + 8 * rr;
+      if (gy_ < a.h && gx_ < a.w && m_[static_cast<int64_t>(gy_) * a.w + gx_] != 0) bits |= 1u << rr;
+    }
+  };
+  uint32_t next_bits;
+  load_rows(blockIdx.x, next_bits);
   for (int it = blockIdx.x; it < n_list; it += gridDim.x) {
-  const int tile = a.tile_list[it];
-  const int s = tile / n_tiles, tl = tile - s * n_tiles;
-  const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
+  int s, tx, ty;
+  tile_unpack(a.tile_list[it], s, tx, ty);
   int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
-  const int tx0 = (tl % a.tiles_x) * kTileW, ty0 = (tl / a.tiles_x) * kTileH;
-  const int w = threadIdx.x >> 5, c = threadIdx.x & 31, gx = tx0 + c;
+  const int tx0 = tx * kTileW, ty0 = ty * kTileH;
+  const int gx = tx0 + c;
+  // the next listed tile's mask bytes are requested before this one is
+  // labelled (their latency overlaps the work below)
+  const uint32_t cur_bits = next_bits;
+  load_rows(it + gridDim.x, next_bits);
   __syncthreads();  // the previous tile is done with the shared arrays
   if (threadIdx.x == 0) n_comp = 0;
 
@@ -179,8 +206,8 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
   uint32_t mine = 0;  // bit rr: pixel (row w + 8*rr, column c) is foreground
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr) {
-    const int r = w + 8 * rr, gy = ty0 + r;
-    const bool fg = gy < a.h && gx < a.w && mask[static_cast<int64_t>(gy) * a.w + gx] != 0;
+    const int r = w + 8 * rr;
+    const bool fg = (cur_bits >> rr) & 1u;
     const uint32_t m = __ballot_sync(0xffffffffu, fg);
     if (c == 0) rowm[r] = m, starts[r] = m & ~(m << 1);
     mine |= static_cast<uint32_t>(fg) << rr;
@@ -291,8 +318,7 @@ __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
 
 // ------------------------------------------------------------------ merge
 // One thread per tile-seam pixel: 32 top-seam + 32 left-seam per tile.
-__device__ __forceinline__ void ccl_merge_one(const CclArgs& a, int s, int tile, int j) {
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+__device__ __forceinline__ void ccl_merge_one(const CclArgs& a, int s, int tx, int ty, int j) {
   const uint8_t* mask = a.mask + static_cast<int64_t>(s) * a.px;
   const int32_t* labg = a.labg + static_cast<int64_t>(s) * a.px;
   int* parent = a.slots.parent + static_cast<int64_t>(s) * a.slot_cap;
@@ -327,12 +353,11 @@ __device__ __forceinline__ void ccl_merge_one(const CclArgs& a, int s, int tile,
 // right of the seam must be foreground.  Grid-stride over list x 64.
 __global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
   const int64_t total = static_cast<int64_t>(*a.tile_count) * 64;
-  const int n_tiles = a.tiles_x * a.tiles_y;
   for (int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gid < total;
        gid += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int lt = a.tile_list[gid >> 6];
-    const int s = lt / n_tiles, tile = lt - s * n_tiles;
-    ccl_merge_one(a, s, tile, static_cast<int>(gid & 63));
+    int s, tx, ty;
+    tile_unpack(a.tile_list[gid >> 6], s, tx, ty);
+    ccl_merge_one(a, s, tx, ty, static_cast<int>(gid & 63));
   }
 }
 

@@ -134,6 +134,8 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
   validate_seg(cfg, w, h);
   px_ = static_cast<int64_t>(w) * h;
   const int tx = ceil_div(w, kTileW), ty = ceil_div(h, kTileH);
+  if (tx > 1024 || ty > 1024 || S > 2047)  // packed tile-list entries (trb_ccl.cu: tile_pack)
+    throw Error(TRB_CONFIG_ERROR, "labelling supports frames up to 32768 x 32768 and 2047 streams per handle");
   slot_cap_ = static_cast<int64_t>(tx) * ty * kMaxTileComps;
   blob_cap_ = px_ / 2 + 1;
   const int wpr = ceil_div(w, 32);
