@@ -255,7 +255,32 @@ def make_frames(trb, clips, n_frames, stream):
     return buf
 
 
+_HOST_AFFINITY = None  # the process's cores before bind_to_gpu_numa_node (the CPU baseline uses them all)
+
+
+def bind_to_gpu_numa_node(local_rank):
+    """Run this rank on the host cores local to its GPU (NVML affinity): the
+    pinned staging / frame buffers are then first-touched on the GPU's NUMA
+    node, so the e2e H2D copies do not cross the socket interconnect."""
+    global _HOST_AFFINITY
+    _HOST_AFFINITY = os.sched_getaffinity(0)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        pynvml.nvmlShutdown()
+        return len(cpus)
+    except Exception:
+        return 0
+
+
 def ours_main(args, rank, world, local_rank):
+    bind_to_gpu_numa_node(local_rank)
     import torch
     import torch.distributed as dist
     import paper_1310_3322_b200 as trb
@@ -425,6 +450,8 @@ def ours_main(args, rank, world, local_rank):
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if _HOST_AFFINITY:
+            os.sched_setaffinity(0, _HOST_AFFINITY)  # the reference baseline gets every host core
         threads = cpu_threads(args.cpu_threads)
         fps, frames_done, secs, kind = run_reference_cpu(threads, threads, 2, 0)
         line["cpu_baseline"] = {
