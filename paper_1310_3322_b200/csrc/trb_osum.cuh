@@ -232,8 +232,10 @@ __device__ __noinline__ void osum_serial(int N, int nseg, int C, int GT, const S
 #pragma unroll
   for (int l = 0; l < L; ++l) S[l] = 0.0;
   int cs = -1;
-  for (int g = 0; g * C < N; ++g) {  // chunk by chunk, in order
-    const int a0 = g * C, a1 = min(N, a0 + C);
+  for (int g = 0; g < GT; ++g) {  // chunk by chunk, in order
+    int a0, a1;
+    Src::bounds(N, GT, g, a0, a1);
+    if (a0 >= a1) continue;
     auto cur = src.begin(a0, g, C, GT);
     for (int jb = a0; jb < a1; jb += Src::kUnroll)
 #pragma unroll
@@ -264,9 +266,10 @@ __device__ __noinline__ void osum_serial(int N, int nseg, int C, int GT, const S
 }
 
 // One run of the engine.
-//   C = Src::chunk(N, GT) elements per cluster thread;
+//   Src::bounds(N, GT, gt, j0, j1): thread gt's chunk [j0, j1) (contiguous,
+//   in thread order; Src::max_chunk bounds its length);
 //   Src::Cursor cur = src.begin(j0, gt, C, GT);  cur.next(k, start, seg, has, v)
-//   walks elements j0 = gt*C, j0+1, ... of thread gt's chunk, k = (j - j0) %
+//   walks elements j0, j0+1, ... of thread gt's chunk, k = (j - j0) %
 //   Src::kUnroll (the loops unroll by kUnroll so k is static) (the source may
 //   store chunks interleaved: element gt*C + i at i*GT + gt); `start` marks a segment start (SEG only), `has`
 //   whether the element contributes, v[L] its values (>= 0).
@@ -280,8 +283,9 @@ __device__ void osum_run(const Grp& cl, int N, int nseg, const Src& src, OsumSha
   const int NT = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int GT = G * NT, gt = rank * NT + t;
-  const int C = Src::chunk(N, GT);
-  const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
+  const int C = Src::max_chunk(N, GT);  // longest chunk (error budget below)
+  int j0, j1;
+  Src::bounds(N, GT, gt, j0, j1);
   // relative error bound of every approximate prefix P:
   //   delta = (N + 2C + 96 + G) * 2^-52
   // mantissa bounds (units of 2^-52 of the binade) equivalent to a relative

@@ -275,6 +275,11 @@ struct BinsSrc {
   int K;
   uint4* stage;    // [kRing][blockDim.x] 16-byte slots
   static __device__ __forceinline__ int chunk(int N, int GT) { return (N + GT - 1) / GT; }
+  static __device__ __forceinline__ int max_chunk(int N, int GT) { return chunk(N, GT); }
+  static __device__ __forceinline__ void bounds(int N, int GT, int gt, int& j0, int& j1) {
+    const int C = chunk(N, GT);
+    j0 = min(N, gt * C), j1 = min(N, j0 + C);
+  }
   struct Cursor {
     const BinsSrc* s;
     const double2* p;  // next block to request
@@ -344,6 +349,26 @@ struct CentroidSrc {
   int x0, y0, ww;
   uint32_t* stage;    // [kRing][blockDim.x] 4-byte slots
   static __device__ __forceinline__ int chunk(int N, int GT) { return ((N + GT - 1) / GT + 3) & ~3; }
+  // The first warp of the group (the young sum: its running sums still cross
+  // a binade every few chunks, one divergent slow step per crossing) takes a
+  // quarter-length chunk each; the other threads share the rest evenly.
+  // Every chunk is a multiple of 4 pixels and they stay in thread order.
+  static constexpr int kYoung = 32;
+  static __device__ __forceinline__ int young_chunk(int N, int GT) { return max(4, (chunk(N, GT) >> 2) & ~3); }
+  static __device__ __forceinline__ int rest_chunk(int N, int GT) {
+    const int Y = kYoung * young_chunk(N, GT);
+    return N <= Y ? 4 : ((N - Y + (GT - kYoung) - 1) / (GT - kYoung) + 3) & ~3;
+  }
+  static __device__ __forceinline__ int max_chunk(int N, int GT) { return max(young_chunk(N, GT), rest_chunk(N, GT)); }
+  static __device__ __forceinline__ void bounds(int N, int GT, int gt, int& j0, int& j1) {
+    const int Cy = young_chunk(N, GT);
+    if (gt < kYoung) {
+      j0 = min(N, gt * Cy), j1 = min(N, j0 + Cy);
+    } else {
+      const int C1 = rest_chunk(N, GT);
+      j0 = min(N, kYoung * Cy + (gt - kYoung) * C1), j1 = min(N, j0 + C1);
+    }
+  }
   struct Cursor {
     const CentroidSrc* s;
     const uint32_t* p;  // next word to request
@@ -418,8 +443,9 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
   // chunks of a multiple of 4 pixels (CentroidSrc's chunking): every thread
   // owns whole words of bins, stored chunk-interleaved
-  const int GT = G * NT_, gt = rank * NT_ + t, C = CentroidSrc::chunk(N, GT);
-  const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
+  const int GT = G * NT_, gt = rank * NT_ + t;
+  int j0, j1;
+  CentroidSrc::bounds(N, GT, gt, j0, j1);
   const int NB = K + 1;
   for (int b = 0; b < NB; ++b) sm.cnt[b * NT_ + t] = 0;
   {
