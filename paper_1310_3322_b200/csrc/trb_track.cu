@@ -355,18 +355,24 @@ struct CentroidSrc {
   // Every chunk is a multiple of 4 pixels and they stay in thread order.
   static constexpr int kYoung = 32;
   static __device__ __forceinline__ int young_chunk(int N, int GT) { return max(4, (chunk(N, GT) >> 2) & ~3); }
+  static __device__ __forceinline__ int half_chunk(int N, int GT) { return max(4, (chunk(N, GT) >> 1) & ~3); }
   static __device__ __forceinline__ int rest_chunk(int N, int GT) {
-    const int Y = kYoung * young_chunk(N, GT);
-    return N <= Y ? 4 : ((N - Y + (GT - kYoung) - 1) / (GT - kYoung) + 3) & ~3;
+    const int Y = kYoung * (young_chunk(N, GT) + half_chunk(N, GT));
+    return N <= Y ? 4 : ((N - Y + (GT - 2 * kYoung) - 1) / (GT - 2 * kYoung) + 3) & ~3;
   }
-  static __device__ __forceinline__ int max_chunk(int N, int GT) { return max(young_chunk(N, GT), rest_chunk(N, GT)); }
+  static __device__ __forceinline__ int max_chunk(int N, int GT) {
+    return max(max(young_chunk(N, GT), half_chunk(N, GT)), rest_chunk(N, GT));
+  }
+  // warp 0: quarter chunks, warp 1: half chunks, the rest evenly
   static __device__ __forceinline__ void bounds(int N, int GT, int gt, int& j0, int& j1) {
-    const int Cy = young_chunk(N, GT);
+    const int Cy = young_chunk(N, GT), Ch = half_chunk(N, GT);
     if (gt < kYoung) {
       j0 = min(N, gt * Cy), j1 = min(N, j0 + Cy);
+    } else if (gt < 2 * kYoung) {
+      j0 = min(N, kYoung * Cy + (gt - kYoung) * Ch), j1 = min(N, j0 + Ch);
     } else {
       const int C1 = rest_chunk(N, GT);
-      j0 = min(N, kYoung * Cy + (gt - kYoung) * C1), j1 = min(N, j0 + C1);
+      j0 = min(N, kYoung * (Cy + Ch) + (gt - 2 * kYoung) * C1), j1 = min(N, j0 + C1);
     }
   }
   struct Cursor {
