@@ -1787,7 +1787,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     // cheap tracks run on single CTAs (split mode); a CTA then owns 1/G of
     // its cluster's scratch
     const char* es = getenv("TRB_SPLIT_US");
-    d_.split_us = es ? atof(es) : 300.0;
+    d_.split_us = es ? atof(es) : 200.0;  // A/B after the graded chunks: 150-200 ahead of 100, 300, 400
     auto envf = [](const char* k, double dflt) {
       const char* e = getenv(k);
       return e ? atof(e) : dflt;
