@@ -1794,7 +1794,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     };
     d_.split_fix = envf("TRB_SPLIT_FIX", 30.0);
     d_.split_perpx = envf("TRB_SPLIT_PERKPX", 14.1) * 1e-3;
-    d_.order_fix = static_cast<int>(envf("TRB_ORDER_FIX", 10000.0));  // A/B: 10k px ahead of 0, 5k, 30k, 65k
+    d_.order_fix = static_cast<int>(envf("TRB_ORDER_FIX", 5000.0));  // A/B (4 x 4 runs): 5k px ahead of 10k, 20k, 30k
     const char* ef = getenv("TRB_ITER_FLOOR");
     d_.iter_floor = ef ? std::max(1, atoi(ef)) : 6;  // iteration history is noisy: order mostly by area
     d_.G = G;
