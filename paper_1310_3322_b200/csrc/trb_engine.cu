@@ -390,8 +390,15 @@ void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host
   uint8_t* stage = staging_[b].as<uint8_t>();
   // the copy may start once the step kStaging back (same buffer) is done with it
   TRB_CUDA(cudaStreamWaitEvent(copy_, consumed_[b], 0));
-  for (int s = 0; s < S_; ++s)
-    TRB_CUDA(cudaMemcpyAsync(stage + fb * s, frames[s], fb, cudaMemcpyHostToDevice, copy_));
+  // one copy per run of frames that sit back to back in host memory (a
+  // capture ring or a batched decoder hands them over that way): fewer,
+  // larger DMA transfers
+  for (int s = 0; s < S_;) {
+    int e = s + 1;
+    while (e < S_ && frames[e] == frames[e - 1] + fb) ++e;
+    TRB_CUDA(cudaMemcpyAsync(stage + fb * s, frames[s], fb * (e - s), cudaMemcpyHostToDevice, copy_));
+    s = e;
+  }
   TRB_CUDA(cudaEventRecord(copied_[b], copy_));
   std::vector<const uint8_t*> dev(S_);
   for (int s = 0; s < S_; ++s) dev[s] = stage + fb * s;

@@ -74,7 +74,7 @@ def test_streams_distinct_c5_streams_device_inputs(gpu):
         assert per[s]["log"].tobytes() == log.tobytes()
 
 
-@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("pinned", [True, False, "contiguous"])
 def test_streams_pipelined_host_steps_match_golden(gpu, pinned):
     """step_host_async (H2D on the copy stream into double-buffered staging,
     overlapping the previous step; results land asynchronously): per-step
@@ -83,15 +83,20 @@ def test_streams_pipelined_host_steps_match_golden(gpu, pinned):
     name, clip, n, window = "c1_pipeline", recipe("C1"), 160, 91
     g = np.load(os.path.join(GOLD, name + ".npz"))
     frames = O.orc_frames(clip, n)[0]
-    if pinned:
+    if pinned == "contiguous":  # both streams' frames back to back: one coalesced H2D copy per step
+        pairs = [torch.from_numpy(np.stack([frames[t], frames[t]])).pin_memory().numpy() for t in range(n)]
+        res = torch.zeros((n, 2), dtype=torch.int32).pin_memory().numpy()
+    elif pinned:
         host = [torch.from_numpy(frames[t]).pin_memory().numpy() for t in range(n)]
+        pairs = [[host[t], host[t]] for t in range(n)]
         res = torch.zeros((n, 2), dtype=torch.int32).pin_memory().numpy()
     else:
         host = [frames[t].copy() for t in range(n)]
+        pairs = [[host[t], host[t]] for t in range(n)]
         res = np.zeros((n, 2), np.int32)
     st = gpu.Streams(2, clip.width, clip.height, clip.channels, MOTION_CFG(window=window), SEG_CFG(), TRACKER_CFG())
     for t in range(n):
-        st.step_host_async([host[t], host[t]], res[t])
+        st.step_host_async([pairs[t][0], pairs[t][1]], res[t])
     st.synchronize()
     emitted = res[window - 1:]
     for s in range(2):
