@@ -203,8 +203,40 @@ int trb_tracker_frames_processed(const trb_tracker* t, int* n);
 typedef struct trb_streams trb_streams;
 int trb_streams_create(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
                        const trb_seg_config* sc, const trb_tracker_config* tc, int device, trb_streams** out);
+/* Capacities of a streams handle.  The reference's track list and log are
+ * unbounded std::vectors (tracking.hpp:237-238); on the device they are
+ * bounded per stream.  A step that would exceed either bound FAILS: the
+ * device records a sticky error, and the next step / synchronize /
+ * download call returns TRB_CAPACITY (the tracker state is no longer the
+ * reference's).  The log is a ring: entries stay until drained
+ * (trb_streams_drain_log), so a long-running stream that drains now and
+ * then never overflows. */
+typedef struct trb_streams_options {
+  int32_t track_cap; /* live tracks per stream, default 256 */
+  int32_t _pad;
+  int64_t log_cap;   /* undrained log entries held per stream, default 65536 */
+} trb_streams_options;
+void trb_default_streams_options(trb_streams_options* o);
+int trb_streams_create_ex(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
+                          const trb_seg_config* sc, const trb_tracker_config* tc, const trb_streams_options* opt,
+                          int device, trb_streams** out);
+/* Per-step results of the host path, what Tracker::process / label_blocked
+ * hand back to the reference's caller for the frame: every stream's blob
+ * count and blob table (the first blob_cap records; n_blobs may exceed it),
+ * and the log entries the frame appended (tracking.hpp:203; the first
+ * log_cap of n_log).  All pointers are PINNED host memory (cudaMallocHost)
+ * or NULL (region skipped); arrays are [n_streams] / [n_streams][cap]. */
+typedef struct trb_step_output {
+  int32_t* n_blobs;
+  trb_blob* blobs;
+  int32_t blob_cap;
+  int32_t log_cap;
+  int32_t* n_log;
+  trb_track_log_entry* log;
+} trb_step_output;
 int trb_streams_destroy(trb_streams* s);
-/* frames: host array of n_streams DEVICE pointers (w*h*channels bytes each).
+/* frames: host array of n_streams DEVICE pointers (w*h*channels bytes each;
+ * any alignment — 16-byte aligned frames take the vector path).
  * cuda_stream: cudaStream_t to launch on (NULL = the handle's own).
  * Step overlap: motion + CCL of a step run on cuda_stream; its tracking runs
  * on the handle's internal stream and overlaps the NEXT step's motion + CCL.
@@ -234,7 +266,15 @@ int trb_streams_step_host(trb_streams* s, const uint8_t* const* frames, int32_t*
  * valid until trb_streams_synchronize (or a later synchronous call). */
 int trb_streams_step_host_async(trb_streams* s, const uint8_t* const* frames, int32_t* result_host,
                                 void* cuda_stream);
+/* step_host_async with the step's results (trb_step_output) copied back
+ * on the device's own schedule: valid after trb_streams_synchronize. */
+int trb_streams_step_host_async_out(trb_streams* s, const uint8_t* const* frames, const trb_step_output* out,
+                                    void* cuda_stream);
 int trb_streams_synchronize(trb_streams* s);
+/* Copy up to cap undrained track-log entries of `stream` (oldest first)
+ * into out, release them from the device ring; *n = entries copied.
+ * trb_streams_download_log / log_size see only undrained entries. */
+int trb_streams_drain_log(trb_streams* s, int stream, trb_track_log_entry* out, int64_t cap, int64_t* n);
 int trb_streams_frames_seen(const trb_streams* s, int* n);
 /* 1 once the window is full (a mask/labels/blobs exist for the last step) */
 int trb_streams_has_output(const trb_streams* s, int* has);

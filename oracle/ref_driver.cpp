@@ -24,6 +24,7 @@
 #include "teamrec/synth.hpp"
 #include "teamrec/tracking.hpp"
 #include "../include/trb.h"
+#include "plane_hash.h"
 
 using namespace teamrec;
 
@@ -555,6 +556,75 @@ int ref_run_streams(int n_streams, int threads, int w, int h, int ch, const uint
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// ---- per-frame detail of the reference per-frame loop (parity tests) ----
+// Same loop as ref_run_streams.  For stream s and steady frame k (frames
+// with a mask, counted from 0): hashes[(s*n_frames + k)*2 + {0,1}] =
+// plane_hash of the mask bytes / the int32 label image, nblobs[s*n_frames+k]
+// = blob count, blobs[(s*n_frames + k)*bcap + i] = the first bcap blobs.
+// The whole track log goes to logs[s*lcap + i] (first lcap), its length to
+// nlog[s].  steady[s] = steady frames.
+int ref_run_streams_detail(int n_streams, int threads, int w, int h, int ch, const uint8_t* const* frames,
+                           int n_frames, const trb_motion_config* mc, const trb_seg_config* sc,
+                           const trb_tracker_config* tc, int64_t* steady, uint64_t* hashes, int32_t* nblobs,
+                           trb_blob* blobs, int bcap, trb_track_log_entry* logs, int64_t lcap, int64_t* nlog) {
+  std::atomic<int> next{0};
+  std::atomic<int> failed{0};
+  std::string err;
+  auto worker = [&]() {
+    try {
+      for (;;) {
+        const int s = next.fetch_add(1);
+        if (s >= n_streams) return;
+        MotionDetector det(to_motion(mc), w, h);
+        Tracker tracker(to_tracker(tc));
+        const SegmentationConfig seg = to_seg(sc);
+        const std::size_t fb = static_cast<std::size_t>(w) * h * ch;
+        int64_t k = 0;
+        for (int t = 0; t < n_frames; ++t) {
+          Frame f = make_frame(frames[s] + fb * t, w, h, ch, t);
+          auto mask = det.push(ch == 1 ? f : grayscale(f));
+          if (!mask) continue;
+          const Labeling lab = label_blocked(*mask, seg, Backend::sequential());
+          tracker.process(f, lab.blobs, Backend::sequential());
+          const int64_t row = static_cast<int64_t>(s) * n_frames + k;
+          hashes[2 * row] = trb_plane_hash(mask->bits.data(), static_cast<int64_t>(mask->bits.size()));
+          hashes[2 * row + 1] =
+              trb_plane_hash(lab.labels.data(), static_cast<int64_t>(lab.labels.size() * sizeof(int)));
+          nblobs[row] = static_cast<int32_t>(lab.blobs.size());
+          for (int i = 0; i < bcap && i < static_cast<int>(lab.blobs.size()); ++i)
+            put_blob(lab.blobs[i], blobs + row * bcap + i);
+          ++k;
+        }
+        steady[s] = k;
+        const auto& log = tracker.log();
+        nlog[s] = static_cast<int64_t>(log.size());
+        for (int64_t i = 0; i < lcap && i < static_cast<int64_t>(log.size()); ++i) {
+          trb_track_log_entry& o = logs[static_cast<int64_t>(s) * lcap + i];
+          std::memset(&o, 0, sizeof(o));
+          o.frame = log[i].frame;
+          o.track_id = log[i].track_id;
+          o.x = log[i].x;
+          o.y = log[i].y;
+          o.w = log[i].w;
+          o.h = log[i].h;
+          o.status = log[i].status == TrackStatus::Lost ? TRB_TRACK_LOST : TRB_TRACK_ACTIVE;
+        }
+      }
+    } catch (const std::exception& e) {
+      if (failed.fetch_add(1) == 0) err = e.what();
+    }
+  };
+  std::vector<std::thread> pool;
+  const int nt = std::max(1, std::min(threads, n_streams));
+  for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  if (failed.load()) {
+    g_err = err;
+    return TRB_INVALID_ARGUMENT;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -84,6 +84,9 @@ uint64_t orc_mix_seed(uint64_t seed, uint64_t salt) {
 }
 
 double orc_libm_hypot(double x, double y) { return hypot(x, y); }
+void orc_libm_hypot_n(const double* x, const double* y, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = hypot(x[i], y[i]);
+}
 
 /* ======================================================================
  * Motion (motion.hpp)
@@ -801,3 +804,6 @@ int orc_synth_next(orc_synth* s, uint8_t* out, int32_t* rects) {
   }
   return 0;
 }
+
+#include "plane_hash.h"
+uint64_t orc_plane_hash(const void* data, int64_t n) { return trb_plane_hash(data, n); }

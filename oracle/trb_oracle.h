@@ -106,6 +106,10 @@ int orc_synth_next(orc_synth* s, uint8_t* out, int32_t* rects);
 /* libm hypot (what std::hypot resolves to); tests pin the product's
  * device replica of glibc's algorithm against it. */
 double orc_libm_hypot(double x, double y);
+void orc_libm_hypot_n(const double* x, const double* y, int64_t n, double* out);
+/* plane_hash.h digest of n bytes (test infrastructure: GPU planes vs the
+ * reference's, oracle/ref_driver.cpp ref_run_streams_detail) */
+uint64_t orc_plane_hash(const void* data, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,20 @@ class TRACK(C.Structure):
                 ("lost_frames", C.c_int32), ("k", C.c_int32), ("cx", C.c_double), ("cy", C.c_double)]
 
 
+class STREAMS_OPTS(C.Structure):
+    """trb_streams_options: per-stream track and track-log capacities."""
+    _fields_ = [("track_cap", C.c_int32), ("_pad", C.c_int32), ("log_cap", C.c_int64)]
+
+    def __init__(self, track_cap=256, log_cap=1 << 16):
+        super().__init__(track_cap, 0, log_cap)
+
+
+class STEP_OUTPUT(C.Structure):
+    """trb_step_output: host (pinned) targets of a step's results."""
+    _fields_ = [("n_blobs", C.c_void_p), ("blobs", C.c_void_p), ("blob_cap", C.c_int32), ("log_cap", C.c_int32),
+                ("n_log", C.c_void_p), ("log", C.c_void_p)]
+
+
 BLOB_DTYPE = np.dtype([("label", "<i4"), ("area", "<i4"), ("x_min", "<i4"), ("y_min", "<i4"), ("x_max", "<i4"),
                        ("y_max", "<i4"), ("cx", "<f8"), ("cy", "<f8")])
 LOG_DTYPE = np.dtype([("frame", "<i4"), ("track_id", "<i4"), ("x", "<f8"), ("y", "<f8"), ("w", "<i4"),

@@ -23,8 +23,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from .abi import (BLOB, BLOB_DTYPE, LOG_DTYPE, LOGE, MOTION_CFG, SEG_CFG, TRACK, TRACKER_CFG, blobs_to_array,
-                  log_to_array)
+from .abi import (BLOB, BLOB_DTYPE, LOG_DTYPE, LOGE, MOTION_CFG, SEG_CFG, STEP_OUTPUT, STREAMS_OPTS, TRACK,
+                  TRACKER_CFG, blobs_to_array, log_to_array)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 # TRB_LIB selects another in-tree build of the library (A/B experiments)
@@ -116,6 +116,10 @@ def _declare(L):
         "trb_tracker_frames_processed": [vp, C.POINTER(C.c_int)],
         "trb_streams_create": [i32, i32, i32, i32, C.POINTER(MOTION_CFG), C.POINTER(SEG_CFG),
                                C.POINTER(TRACKER_CFG), i32, C.POINTER(vp)],
+        "trb_streams_create_ex": [i32, i32, i32, i32, C.POINTER(MOTION_CFG), C.POINTER(SEG_CFG),
+                                  C.POINTER(TRACKER_CFG), C.POINTER(STREAMS_OPTS), i32, C.POINTER(vp)],
+        "trb_streams_step_host_async_out": [vp, vp, C.POINTER(STEP_OUTPUT), vp],
+        "trb_streams_drain_log": [vp, i32, vp, i64, C.POINTER(C.c_int64)],
         "trb_streams_destroy": [vp],
         "trb_streams_step_device": [vp, vp, vp],
         "trb_streams_step_host": [vp, vp, vp, vp],
@@ -163,7 +167,8 @@ def _declare(L):
         f = getattr(L, name)
         f.argtypes = args
         f.restype = C.c_int
-    for name in ("trb_default_motion_config", "trb_default_seg_config", "trb_default_tracker_config"):
+    for name in ("trb_default_motion_config", "trb_default_seg_config", "trb_default_tracker_config",
+                 "trb_default_streams_options"):
         getattr(L, name).restype = None
 
 
@@ -449,25 +454,75 @@ def quantize_colors(pixels: np.ndarray, k: int, iters: int, seed: int, device: i
 
 
 # --------------------------------------------------------------- streams
+class StepOutput:
+    """Pinned host targets for one step's results (trb_step_output): per
+    stream the blob count, the first `blob_cap` blobs and the log entries
+    the frame appended (first `log_cap`).  Read after Streams.synchronize()."""
+
+    def __init__(self, n_streams: int, blob_cap: int = 64, log_cap: int = 32):
+        import torch  # pinned host memory (cudaMallocHost through torch's caching host allocator)
+        self.n, self.blob_cap, self.log_cap = n_streams, blob_cap, log_cap
+        pin = lambda nbytes: torch.empty(max(16, nbytes), dtype=torch.uint8).pin_memory()
+        self._bufs = [pin(4 * n_streams), pin(4 * n_streams), pin(BLOB_DTYPE.itemsize * n_streams * blob_cap),
+                      pin(LOG_DTYPE.itemsize * n_streams * log_cap)]
+        b = self._bufs
+        self.n_blobs = b[0].numpy()[:4 * n_streams].view(np.int32)
+        self.n_log = b[1].numpy()[:4 * n_streams].view(np.int32)
+        self.blobs = b[2].numpy()[:BLOB_DTYPE.itemsize * n_streams * blob_cap].view(BLOB_DTYPE).reshape(
+            n_streams, blob_cap)
+        self.log = b[3].numpy()[:LOG_DTYPE.itemsize * n_streams * log_cap].view(LOG_DTYPE).reshape(n_streams, log_cap)
+        self.c = STEP_OUTPUT(b[0].data_ptr(), b[2].data_ptr() if blob_cap else None, blob_cap, log_cap,
+                             b[1].data_ptr(), b[3].data_ptr() if log_cap else None)
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes the device writes back per step."""
+        return 8 * self.n + (BLOB_DTYPE.itemsize * self.blob_cap + LOG_DTYPE.itemsize * self.log_cap) * self.n
+
+    def stream_blobs(self, s: int) -> np.ndarray:
+        return self.blobs[s, :min(int(self.n_blobs[s]), self.blob_cap)].copy()
+
+    def stream_log(self, s: int) -> np.ndarray:
+        return self.log[s, :min(int(self.n_log[s]), self.log_cap)].copy()
+
+
 class Streams:
     """The batched device-resident front end (run_vision, harness.hpp:412-450)
-    for n independent streams of one geometry."""
+    for n independent streams of one geometry.  track_cap / log_cap bound the
+    live tracks and the undrained track-log entries per stream
+    (trb_streams_options); exceeding either fails the step (CapacityError)."""
 
     def __init__(self, n_streams: int, width: int, height: int, channels: int = 1,
                  motion: Optional[MOTION_CFG] = None, seg: Optional[SEG_CFG] = None,
-                 tracker: Optional[TRACKER_CFG] = TRACKER_CFG(), device: int = 0):
+                 tracker: Optional[TRACKER_CFG] = TRACKER_CFG(), device: int = 0, track_cap: int = 256,
+                 log_cap: int = 1 << 16):
         self.n, self.width, self.height, self.channels = n_streams, width, height, channels
         self.motion = motion if motion is not None else MOTION_CFG()
         self.seg = seg if seg is not None else SEG_CFG()
         self.tracker = tracker
+        self.opts = STREAMS_OPTS(track_cap, log_cap)
         h = C.c_void_p()
-        _check(lib().trb_streams_create(n_streams, width, height, channels, C.byref(self.motion),
-                                        C.byref(self.seg), C.byref(tracker) if tracker is not None else None,
-                                        device, C.byref(h)))
+        _check(lib().trb_streams_create_ex(n_streams, width, height, channels, C.byref(self.motion),
+                                           C.byref(self.seg), C.byref(tracker) if tracker is not None else None,
+                                           C.byref(self.opts), device, C.byref(h)))
         self._h = h
         self._ptrs = (C.c_void_p * n_streams)()
 
+    def _frame_count(self, frames) -> None:
+        if len(frames) != self.n:
+            raise InvalidArgument(f"expected {self.n} frames (one per stream), got {len(frames)}")
+
+    def _host_frames(self, frames, ptrs) -> None:
+        """Host frames: C-contiguous uint8 arrays of width*height*channels."""
+        self._frame_count(frames)
+        need = self.width * self.height * self.channels
+        for i, f in enumerate(frames):
+            if not isinstance(f, np.ndarray) or f.dtype != np.uint8 or not f.flags["C_CONTIGUOUS"] or f.size != need:
+                raise InvalidArgument(f"frame {i}: expected a C-contiguous uint8 array of {need} bytes")
+            ptrs[i] = f.ctypes.data
+
     def step_device(self, frame_ptrs: Sequence[int], cuda_stream: int = 0) -> None:
+        self._frame_count(frame_ptrs)
         for i, p in enumerate(frame_ptrs):
             self._ptrs[i] = p
         _check(lib().trb_streams_step_device(self._h, self._ptrs, C.c_void_p(cuda_stream)))
@@ -475,27 +530,49 @@ class Streams:
     def step_device_warp(self, frame_ptrs: Sequence[int], homographies, cuda_stream: int = 0) -> None:
         """MotionConfig(warp=1): warp every stream's frame by its homography
         (n_streams x 3 x 3) before it enters the window (stream_detect)."""
+        self._frame_count(frame_ptrs)
         for i, p in enumerate(frame_ptrs):
             self._ptrs[i] = p
         hm = np.ascontiguousarray(homographies, dtype=np.float64).reshape(-1)
+        if hm.size != 9 * self.n:
+            raise InvalidArgument(f"expected {self.n} homographies (3x3 each)")
         _check(lib().trb_streams_step_device_warp(self._h, self._ptrs, _ptr(hm), C.c_void_p(cuda_stream)))
+
+    def _result(self, result):
+        if result is None:
+            return None
+        if result.dtype != np.int32 or result.size < self.n or not result.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument(f"result: expected a contiguous int32 array of {self.n} entries")
+        return _ptr(result)
 
     def step_host(self, frames: Sequence[np.ndarray], result: Optional[np.ndarray] = None,
                   cuda_stream: int = 0) -> None:
-        for i, f in enumerate(frames):
-            self._ptrs[i] = f.ctypes.data
-        rp = _ptr(result) if result is not None else None
-        _check(lib().trb_streams_step_host(self._h, self._ptrs, rp, C.c_void_p(cuda_stream)))
+        self._host_frames(frames, self._ptrs)
+        _check(lib().trb_streams_step_host(self._h, self._ptrs, self._result(result), C.c_void_p(cuda_stream)))
 
-    def step_host_async(self, frames: Sequence[np.ndarray], result: Optional[np.ndarray] = None,
-                        cuda_stream: int = 0) -> None:
+    def step_host_async(self, frames: Sequence[np.ndarray], result=None, cuda_stream: int = 0) -> None:
         """Pipelined step_host: queued work only; `frames` and `result` must
-        stay alive (and unmodified) until synchronize()."""
-        ptrs = (C.c_void_p * len(frames))()
-        for i, f in enumerate(frames):
-            ptrs[i] = f.ctypes.data
-        rp = _ptr(result) if result is not None else None
-        _check(lib().trb_streams_step_host_async(self._h, ptrs, rp, C.c_void_p(cuda_stream)))
+        stay alive (and unmodified) until synchronize().  `result` is an int32
+        array (blob counts) or a StepOutput (blob tables + the frame's log
+        entries)."""
+        ptrs = (C.c_void_p * self.n)()
+        self._host_frames(frames, ptrs)
+        if isinstance(result, StepOutput):
+            if result.n != self.n:
+                raise InvalidArgument("StepOutput was made for another stream count")
+            _check(lib().trb_streams_step_host_async_out(self._h, ptrs, C.byref(result.c), C.c_void_p(cuda_stream)))
+            return
+        _check(lib().trb_streams_step_host_async(self._h, ptrs, self._result(result), C.c_void_p(cuda_stream)))
+
+    def drain_log(self, s: int) -> np.ndarray:
+        """The track-log entries of stream s not drained yet (oldest first);
+        they are released from the device ring."""
+        n = C.c_int64(0)
+        _check(lib().trb_streams_log_size(self._h, s, C.byref(n)))
+        arr = (LOGE * max(1, n.value))()
+        got = C.c_int64(0)
+        _check(lib().trb_streams_drain_log(self._h, s, arr, n.value, C.byref(got)))
+        return log_to_array(arr, got.value)
 
     def synchronize(self) -> None:
         _check(lib().trb_streams_synchronize(self._h))

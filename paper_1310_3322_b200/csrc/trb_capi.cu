@@ -359,7 +359,8 @@ void device_blob_features(const int32_t* labels, int64_t px, const uint8_t* fram
                           int n, double* mean, double* aspect, cudaStream_t st) {
   if (n <= 0) return;
   trb::DevBuf sums;
-  sums.alloc(sizeof(unsigned long long) * n);  // zeroed
+  sums.alloc(sizeof(unsigned long long) * n, false);
+  TRB_CUDA(cudaMemsetAsync(sums.p, 0, sizeof(unsigned long long) * n, st));  // ordered before the atomics
   blob_feature_sum_kernel<<<static_cast<unsigned>(trb::ceil_div64(trb::ceil_div64(px, 16), 256)), 256, 0, st>>>(
       labels, px, frame, ch, n, sums.as<unsigned long long>());
   TRB_LAUNCH_CHECK("blob_feature_sum_kernel");
@@ -512,8 +513,18 @@ int trb_tracker_frames_processed(const trb_tracker* t, int* n) {
 }
 
 // ------------------------------------------------------------- streams
+void trb_default_streams_options(trb_streams_options* o) {
+  if (o) *o = trb_streams_options{256, 0, 1 << 16};
+}
+
 int trb_streams_create(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
                        const trb_seg_config* sc, const trb_tracker_config* tc, int device, trb_streams** out) {
+  return trb_streams_create_ex(n_streams, width, height, channels, mc, sc, tc, nullptr, device, out);
+}
+
+int trb_streams_create_ex(int n_streams, int width, int height, int channels, const trb_motion_config* mc,
+                          const trb_seg_config* sc, const trb_tracker_config* tc, const trb_streams_options* opt,
+                          int device, trb_streams** out) {
   return guard([&] {
     need(out != nullptr, "null argument");
     *out = nullptr;
@@ -524,7 +535,12 @@ int trb_streams_create(int n_streams, int width, int height, int channels, const
     if (tc) t = *tc;
     auto h = std::make_unique<trb_streams>();
     h->device = device;
-    h->s = std::make_unique<trb::Streams>(n_streams, width, height, channels, m, s, t, tc != nullptr);
+    trb_streams_options o{256, 0, 1 << 16};
+    if (opt) o = *opt;
+    need(o.track_cap >= 1 && o.track_cap <= (1 << 20), "track_cap must be in [1, 2^20]");
+    need(o.log_cap >= 1, "log_cap must be >= 1");
+    h->s = std::make_unique<trb::Streams>(n_streams, width, height, channels, m, s, t, tc != nullptr, o.track_cap,
+                                          o.log_cap);
     *out = h.release();
   });
 }
@@ -619,6 +635,26 @@ int trb_streams_step_host_async(trb_streams* s, const uint8_t* const* frames, in
   });
 }
 
+int trb_streams_step_host_async_out(trb_streams* s, const uint8_t* const* frames, const trb_step_output* out,
+                                    void* cuda_stream) {
+  return guard([&] {
+    need(s && frames && out, "null argument");
+    TRB_CUDA(cudaSetDevice(s->device));
+    s->s->step_host_async(frames, nullptr, static_cast<cudaStream_t>(cuda_stream), out);
+  });
+}
+
+int trb_streams_drain_log(trb_streams* s, int stream, trb_track_log_entry* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    need(s && out && n, "null argument");
+    need(s->s->tracker() != nullptr, "streams were created without a tracker");
+    need(stream >= 0 && stream < s->s->S(), "stream index out of range");
+    TRB_CUDA(cudaSetDevice(s->device));
+    TRB_CUDA(cudaDeviceSynchronize());
+    *n = s->s->tracker()->drain_log(stream, out, cap, s->s->stream());
+  });
+}
+
 int trb_streams_synchronize(trb_streams* s) {
   return guard([&] {
     need(s != nullptr, "null argument");
@@ -695,7 +731,7 @@ int trb_streams_download_log(trb_streams* s, int stream, trb_track_log_entry* ou
     need(s->s->tracker() != nullptr, "streams were created without a tracker");
     TRB_CUDA(cudaSetDevice(s->device));
     TRB_CUDA(cudaDeviceSynchronize());
-    s->s->tracker()->check_errors(s->s->stream());
+    s->s->tracker()->check_errors(s->s->stream(), false);  // the entries held are valid after a log overflow
     s->s->tracker()->log(stream, out, cap, s->s->stream());
   });
 }

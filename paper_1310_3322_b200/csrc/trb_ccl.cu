@@ -540,4 +540,19 @@ int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   return 8;
 }
 
+
+namespace {
+__global__ void __launch_bounds__(128) pack_blobs_kernel(const trb_blob* blobs, int64_t stride, const int32_t* nblobs,
+                                                         trb_blob* out, int bcap) {
+  const int s = blockIdx.x, n = min(nblobs[s], bcap);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[static_cast<int64_t>(s) * bcap + i] = blobs[s * stride + i];
+}
+}  // namespace
+
+void launch_pack_blobs(const trb_blob* blobs, int64_t stride, const int32_t* nblobs, trb_blob* out, int bcap,
+                       int n_streams, cudaStream_t st) {
+  pack_blobs_kernel<<<n_streams, 128, 0, st>>>(blobs, stride, nblobs, out, bcap);
+  TRB_LAUNCH_CHECK("pack_blobs_kernel");
+}
+
 }  // namespace trb

@@ -65,7 +65,7 @@ MotionState::MotionState(const trb_motion_config& cfg, int S, int w, int h, int 
 }
 
 bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st,
-                       int* launches) {
+                       int* launches, bool frames_aligned) {
   const int W = cfg_.window;
   MotionArgs a{};
   a.frames = frames_dev;
@@ -84,7 +84,7 @@ bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t*
   a.threshold = cfg_.threshold;
   a.W = static_cast<uint32_t>(W);
   a.div = FastDiv::make(2u * static_cast<uint32_t>(W));
-  a.vec_ok = (px_ % 16 == 0);
+  a.vec_ok = (px_ % 16 == 0) && frames_aligned;
   if (cfg_.method == TRB_BG_MEAN) {
     launch_motion_mean(a, ch_, wide_, S_, st);
     ++*launches;
@@ -200,7 +200,7 @@ void CclState::run(const uint8_t* mask, cudaStream_t st, int* launches) {
 
 // ----------------------------------------------------------------- streams
 Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const trb_seg_config& sc,
-                 const trb_tracker_config& tc, bool with_tracker)
+                 const trb_tracker_config& tc, bool with_tracker, int track_cap, int64_t log_cap)
     : S_(S), w_(w), h_(h), ch_(ch), mc_(mc) {
   if (S < 1) throw Error(TRB_INVALID_ARGUMENT, "need at least one stream");
   if (ch != 1 && ch != 3) throw Error(TRB_INVALID_ARGUMENT, "frame channels must be 1 or 3");
@@ -209,7 +209,9 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   px_ = static_cast<int64_t>(w) * h;
   motion_ = std::make_unique<MotionState>(mc, S, w, h, ch);
   ccl_ = std::make_unique<CclState>(S, w, h, sc);
-  if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S);
+  if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S, track_cap, log_cap);
+  err_host_.alloc(sizeof(int32_t));
+  *err_host_.as<int32_t>() = 0;
   mask_.alloc(static_cast<size_t>(px_) * S);
   if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S * 2);  // raw mask + 2-pass scratch
   // ring of per-step frame-pointer tables: a table is rewritten only after
@@ -222,6 +224,9 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   TRB_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   TRB_CUDA(cudaStreamCreateWithFlags(&trk_, cudaStreamNonBlocking));
   if (const char* e = getenv("TRB_OVERLAP")) overlap_ = atoi(e) != 0;
+  // host-path staging ring, allocated up front: a step never cudaMallocs
+  // (that would serialise the device inside the first host steps)
+  for (int i = 0; i < kStaging; ++i) staging_[i].alloc(static_cast<size_t>(px_) * ch_ * S_, false);
   for (int i = 0; i < kStaging; ++i) {
     TRB_CUDA(cudaEventCreateWithFlags(&copied_[i], cudaEventDisableTiming));
     TRB_CUDA(cudaEventCreateWithFlags(&consumed_[i], cudaEventDisableTiming));
@@ -270,7 +275,9 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
   int launches = 0;
   overlap = overlap && tracker_ && !profiling_;
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[0], st));
-  const bool emitted = motion_->push(frames_dev, mask_.as<uint8_t>(), mask_tmp_.as<uint8_t>(), st, &launches);
+  const bool emitted =
+      motion_->push(frames_dev, mask_.as<uint8_t>(), mask_tmp_.as<uint8_t>(), st, &launches, frames_aligned_);
+  has_output_ = emitted;
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[1], st));
   const int b = ccl_->next_buffer();
   if (emitted) {
@@ -283,6 +290,8 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
     TRB_CUDA(cudaStreamWaitEvent(trk_, ccl_ev_[b], 0));
     tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), trk_, &launches,
                       nullptr);
+    TRB_CUDA(cudaMemcpyAsync(err_host_.p, tracker_->err_word(), sizeof(int32_t), cudaMemcpyDeviceToHost, trk_));
+    if (pending_out_) output_(pending_out_, trk_, &launches);  // before CCL(t+2) may reuse this blob table
     TRB_CUDA(cudaEventRecord(trk_ev_[b], trk_));
     trk_pending_[b] = true;
     last_trk_ = b;
@@ -290,10 +299,13 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
     if (done) TRB_CUDA(cudaEventRecord(done, trk_));
   } else {
     if (last_trk_ >= 0) join(st), last_trk_ = -1;  // back to in-stream tracking (profiling, warp mode)
-    if (emitted && tracker_)
+    if (emitted && tracker_) {
       tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches,
                         profiling_ ? prof_ev_[3] : nullptr);
-    else if (profiling_)
+      TRB_CUDA(cudaMemcpyAsync(err_host_.p, tracker_->err_word(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
+    if (pending_out_) output_(pending_out_, st, &launches);
+    if (!(emitted && tracker_) && profiling_)
       TRB_CUDA(cudaEventRecord(prof_ev_[3], st));
     if (done) TRB_CUDA(cudaEventRecord(done, st));
   }
@@ -330,6 +342,7 @@ const uint8_t* const* Streams::upload_ptrs_(const uint8_t* const* frames, cudaSt
 
 void Streams::step_device_warp(const uint8_t* const* frames, const double* h9s, cudaStream_t st) {
   if (!st) st = own_;
+  check_sticky_errors();
   if (!h9s) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const size_t fb = static_cast<size_t>(px_) * ch_;
   if (!warp_buf_.p) {
@@ -341,6 +354,7 @@ void Streams::step_device_warp(const uint8_t* const* frames, const double* h9s, 
     invs_dev_.alloc(sizeof(double) * 9 * S_ * kPtrSlots, false);
     invs_host_.alloc(sizeof(double) * 9 * S_ * kPtrSlots);
   }
+  frames_aligned_ = true;  // the motion kernel reads the warped planes (own buffers)
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(frames, st);  // waits for the slot's previous use
   double* ih = static_cast<double*>(invs_host_.p) + static_cast<size_t>(slot) * 9 * S_;
@@ -354,7 +368,13 @@ void Streams::step_device_warp(const uint8_t* const* frames, const double* h9s, 
 
 void Streams::step_device(const uint8_t* const* frames, cudaStream_t st) {
   if (!st) st = own_;
+  check_sticky_errors();
   if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
+  frames_aligned_ = true;  // caller frames at any offset: misaligned ones take the scalar path
+  for (int s = 0; s < S_; ++s) {
+    if (!frames[s]) throw Error(TRB_INVALID_ARGUMENT, "null frame pointer for stream " + std::to_string(s));
+    if (reinterpret_cast<uintptr_t>(frames[s]) & 15) frames_aligned_ = false;
+  }
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(frames, st);
   run_(dp, st, overlap_, slot_ev_[slot]);
@@ -371,7 +391,9 @@ void CUDART_CB copy_result(void* p) {
   std::memcpy(r->dst, r->src, r->bytes);
   delete r;
 }
-bool is_pinned(const void* p) {
+}  // namespace
+
+bool is_pinned_host(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
@@ -379,15 +401,71 @@ bool is_pinned(const void* p) {
   }
   return a.type == cudaMemoryTypeHost;
 }
-}  // namespace
 
-void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st) {
+void Streams::check_sticky_errors() {
+  const int32_t e = *static_cast<volatile int32_t*>(err_host_.p);
+  if (e & 1) throw Error(TRB_CAPACITY, "tracker: track capacity exceeded (raise trb_streams_options.track_cap)");
+  if (e & 2)
+    throw Error(TRB_CAPACITY,
+                "tracker: track-log ring full (drain it with trb_streams_drain_log or raise trb_streams_options.log_cap)");
+}
+
+// The step's results packed on the device (blob counts, the first blob_cap
+// blobs, the frame's log entries) and copied to the caller's host buffers on
+// the stream of the step's last reader.
+void Streams::output_(const trb_step_output* out, cudaStream_t rs, int* launches) {
+  const int bcap = out->blobs ? std::max(0, out->blob_cap) : 0;
+  const int lcap = (out->log && tracker_) ? std::max(0, out->log_cap) : 0;
+  const size_t hdr = sizeof(int32_t) * 2 * S_;
+  const size_t bbytes = sizeof(trb_blob) * static_cast<size_t>(S_) * bcap;
+  const size_t lbytes = sizeof(trb_track_log_entry) * static_cast<size_t>(S_) * lcap;
+  if (bcap != out_bcap_ || lcap != out_lcap_) {
+    TRB_CUDA(cudaStreamSynchronize(rs));
+    out_dev_.alloc(hdr + bbytes + lbytes + 16, false);
+    out_bcap_ = bcap, out_lcap_ = lcap;
+  }
+  char* base = out_dev_.as<char>();
+  int32_t* nb = reinterpret_cast<int32_t*>(base);
+  int32_t* nl = nb + S_;
+  trb_blob* bl = reinterpret_cast<trb_blob*>(base + hdr);
+  trb_track_log_entry* lg = reinterpret_cast<trb_track_log_entry*>(base + hdr + bbytes);
+  if (!has_output_) {
+    TRB_CUDA(cudaMemsetAsync(base, 0, hdr, rs));
+  } else if (tracker_) {
+    tracker_->pack_step(ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), nb, bl, bcap, nl, lg, lcap, rs);
+    ++*launches;
+  } else {
+    TRB_CUDA(cudaMemcpyAsync(nb, ccl_->nblobs(), sizeof(int32_t) * S_, cudaMemcpyDeviceToDevice, rs));
+    TRB_CUDA(cudaMemsetAsync(nl, 0, sizeof(int32_t) * S_, rs));
+    if (bcap > 0) launch_pack_blobs(ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), bl, bcap, S_, rs), ++*launches;
+  }
+  struct Region {
+    void* dst;
+    const void* src;
+    size_t n;
+  } regs[4] = {{out->n_blobs, nb, sizeof(int32_t) * S_}, {out->n_log, nl, sizeof(int32_t) * S_},
+               {out->blobs, bl, bbytes}, {out->log, lg, lbytes}};
+  for (const Region& r : regs) {
+    if (!r.dst || r.n == 0) continue;
+    if (is_pinned_host(r.dst)) {
+      TRB_CUDA(cudaMemcpyAsync(r.dst, r.src, r.n, cudaMemcpyDeviceToHost, rs));
+    } else {
+      throw Error(TRB_INVALID_ARGUMENT, "trb_step_output buffers must be pinned host memory (cudaMallocHost)");
+    }
+  }
+}
+
+void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host, cudaStream_t st,
+                              const trb_step_output* out) {
   if (!st) st = own_;
+  check_sticky_errors();
   if (mc_.warp == 1) throw Error(TRB_INVALID_ARGUMENT, "warp mode homography requires per-frame homographies");
   const size_t fb = static_cast<size_t>(px_) * ch_;
+  for (int s = 0; s < S_; ++s)
+    if (!frames[s]) throw Error(TRB_INVALID_ARGUMENT, "null frame pointer for stream " + std::to_string(s));
   const int b = host_step_++ % kStaging;
-  if (!staging_[b].p) staging_[b].alloc(fb * S_, false);
-  uint8_t* stage = staging_[b].as<uint8_t>();
+  uint8_t* stage = staging_[b].as<uint8_t>();  // allocated with the handle (no cudaMalloc inside a step)
+  frames_aligned_ = true;                       // staging planes sit at multiples of the frame size
   // the copy may start once the step kStaging back (same buffer) is done with it
   TRB_CUDA(cudaStreamWaitEvent(copy_, consumed_[b], 0));
   // one copy per run of frames that sit back to back in host memory (a
@@ -405,14 +483,22 @@ void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host
   const int slot = ptr_slot_;
   const uint8_t* const* dp = upload_ptrs_(dev.data(), st);
   TRB_CUDA(cudaStreamWaitEvent(st, copied_[b], 0));
-  const cudaStream_t last_reader = run_(dp, st, overlap_, slot_ev_[slot]);
+  pending_out_ = out;
+  cudaStream_t last_reader;
+  try {
+    last_reader = run_(dp, st, overlap_, slot_ev_[slot]);
+  } catch (...) {
+    pending_out_ = nullptr;
+    throw;
+  }
+  pending_out_ = nullptr;
   TRB_CUDA(cudaEventRecord(consumed_[b], last_reader));  // tracking read the frames too
   if (result_host) {
     const size_t rb = sizeof(int32_t) * S_;
     if (!has_output_) {
       TRB_CUDA(cudaMemsetAsync(ccl_->nblobs(), 0, rb, st));
     }
-    if (is_pinned(result_host)) {
+    if (is_pinned_host(result_host)) {
       TRB_CUDA(cudaMemcpyAsync(result_host, ccl_->nblobs(), rb, cudaMemcpyDeviceToHost, st));
     } else {  // pageable: through a pinned buffer, copied out when the stream gets there
       if (!result_pinned_.p) result_pinned_.alloc(rb);

@@ -29,7 +29,12 @@ struct DevBuf {
     release();
     TRB_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
     n = bytes;
-    if (zero) TRB_CUDA(cudaMemset(p, 0, bytes ? bytes : 16));
+    if (zero) {
+      // Every consumer runs on a non-blocking stream, which does not order
+      // after the legacy stream: finish the clear before anyone can launch.
+      TRB_CUDA(cudaMemsetAsync(p, 0, bytes ? bytes : 16, 0));
+      TRB_CUDA(cudaStreamSynchronize(0));
+    }
   }
   template <typename T>
   T* as() const {
@@ -58,6 +63,7 @@ struct PinnedBuf {
   }
 };
 
+bool is_pinned_host(const void* p);
 void validate_motion(const trb_motion_config& c);
 void validate_seg(const trb_seg_config& c, int w, int h);
 void validate_tracker(const trb_tracker_config& c);
@@ -67,7 +73,10 @@ class MotionState {
   MotionState(const trb_motion_config& cfg, int S, int w, int h, int ch);
   // frames_dev: device array [S] of device frame pointers.  Writes the
   // masks (device, S*px) when the window is full; returns true then.
-  bool push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st, int* launches);
+  // frames_aligned: every frame pointer is 16-byte aligned (the 16-byte
+  // vector path needs it; otherwise the scalar path runs)
+  bool push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st, int* launches,
+            bool frames_aligned = true);
   void background(uint8_t* out_dev, cudaStream_t st);  // stream 0 only
   int frames_seen() const { return frames_seen_; }
   const trb_motion_config& cfg() const { return cfg_; }
@@ -110,7 +119,7 @@ class TrackerState;  // trb_track.cu
 class Streams {
  public:
   Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const trb_seg_config& sc,
-          const trb_tracker_config& tc, bool with_tracker);
+          const trb_tracker_config& tc, bool with_tracker, int track_cap = 256, int64_t log_cap = 1 << 16);
   ~Streams();
   void step_device(const uint8_t* const* frames_host_array_of_dev_ptrs, cudaStream_t st);
   // MotionConfig::warp == per-frame homography (stream_detect, motion.hpp:
@@ -123,7 +132,12 @@ class Streams {
   // (overlapping the previous step's kernels) into one of two staging
   // buffers; result_host is written when `st` reaches this step (valid after
   // synchronize()); frames_host must stay untouched until then.
-  void step_host_async(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st);
+  void step_host_async(const uint8_t* const* frames_host, int32_t* result_host, cudaStream_t st,
+                       const trb_step_output* out = nullptr);
+  // Throws the tracker's sticky capacity error once the device reported it
+  // (mirrored into pinned memory after every step: raised at most a step
+  // or two after the step that overflowed, and at synchronize()).
+  void check_sticky_errors();
   // Make `st` wait for every step issued so far (the tracker of the last
   // step runs on an internal stream; see run_).
   void join(cudaStream_t st);
@@ -157,6 +171,7 @@ class Streams {
   int S_, w_, h_, ch_;
   int64_t px_;
   trb_motion_config mc_;
+  bool frames_aligned_ = true;  // the current step's frame pointers are 16-byte aligned
   std::unique_ptr<MotionState> motion_;
   std::unique_ptr<CclState> ccl_;
   std::unique_ptr<TrackerState> tracker_;
@@ -171,6 +186,12 @@ class Streams {
   DevBuf warp_buf_, warp_ptrs_, invs_dev_;  // warped frames, their pointer table, inverses [slot][S][9]
   PinnedBuf invs_host_;
   PinnedBuf result_pinned_;
+  PinnedBuf err_host_;          // mirror of the tracker's error word
+  DevBuf out_dev_;              // packed step output (trb_step_output regions)
+  int out_bcap_ = -1, out_lcap_ = -1;
+  PinnedBuf out_bounce_;        // pageable trb_step_output targets go through here
+  void output_(const trb_step_output* out, cudaStream_t last_reader, int* launches);
+  const trb_step_output* pending_out_ = nullptr;  // set by step_host_async for run_
   cudaStream_t copy_ = nullptr;
   cudaEvent_t copied_[kStaging] = {}, consumed_[kStaging] = {};
   int host_step_ = 0;

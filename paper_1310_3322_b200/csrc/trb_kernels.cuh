@@ -89,6 +89,9 @@ struct CclArgs {
 
 // Launches the full CCL + blob-statistics chain; returns launches issued.
 int launch_ccl(const CclArgs& a, int n_streams, cudaStream_t st);
+// the first bcap blobs of every stream's table into out[S][bcap]
+void launch_pack_blobs(const trb_blob* blobs, int64_t stride, const int32_t* nblobs, trb_blob* out, int bcap,
+                       int n_streams, cudaStream_t st);
 
 // ------------------------------------------------------------ tracking
 struct TrackerDev;  // defined in trb_track.cu

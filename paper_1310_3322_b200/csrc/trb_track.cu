@@ -1246,7 +1246,7 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
 // geometry and success conditions (:208-234), lost counting and retirement
 // (:197-201) and the log (:203-204).
 __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
-  __shared__ int sh_n, sh_ncur, sh_next_id, sh_hit, sh_ok;
+  __shared__ int sh_n, sh_ncur, sh_next_id, sh_ok;
   __shared__ double sh_min[2][NT / 32];
   const int s = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -1274,12 +1274,12 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
   for (int i = 0; i < nb; ++i) {
     if (matched[i]) continue;  // uniform
     const trb_blob b = blobs[i];
-    if (t == 0) sh_hit = 0;
-    __syncthreads();
-    for (int k = sh_n + t; k < sh_ncur; k += NT)
-      if (gate(b, list[k])) sh_hit = 1;
-    __syncthreads();
-    if (sh_hit) continue;
+    // any of this frame's earlier spawns gates the blob: one barrier that
+    // also publishes the vote (no shared flag that a fast thread could reset
+    // for the next blob while slower warps still read it)
+    int hit = 0;
+    for (int k = sh_n + t; k < sh_ncur && !hit; k += NT) hit = gate(b, list[k]);
+    if (__syncthreads_or(hit)) continue;
     // spawn_track: the id is consumed even when the spawn fails (:210)
     const int id = sh_next_id;
     int tw = max(3, b.x_max - b.x_min + 1), th = max(3, b.y_max - b.y_min + 1);
@@ -1326,7 +1326,10 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
             break;
           }
         if (slot < 0 || sh_ncur >= d.T) {
+          // the reference would append a track here; this handle cannot:
+          // the step fails (sticky error, raised by the host at the next call)
           d.err[s] |= 1;
+          atomicOr(d.err_any, 1);
         } else {
           const int64_t g = slot_index(d, s, slot);
           d.used[g] = 1;
@@ -1368,13 +1371,18 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
   const int nl = sh_ncur;
   const int64_t base = d.n_log[s];
   const int frame = d.frame_no[s];
+  // the log is a ring of log_cap entries per stream: entries [tail, head)
+  // are held until the host drains them (trb_streams_drain_log); a step
+  // whose entries do not fit fails (sticky error) instead of overwriting
+  const bool fits = base + nl - d.log_tail[s] <= d.log_cap;
+  if (!fits && t == 0) {
+    atomicOr(&d.err[s], 2);
+    atomicOr(d.err_any, 2);
+  }
   trb_track_log_entry* log = d.log + static_cast<int64_t>(s) * d.log_cap;
-  for (int k = t; k < nl; k += NT) {
-    const int64_t pos = base + k;
-    if (pos >= d.log_cap) {
-      atomicOr(&d.err[s], 2);
-      continue;
-    }
+  if (t == 0) d.step_log_base[s] = base;
+  for (int k = t; k < nl && fits; k += NT) {
+    const int64_t pos = (base + k) % d.log_cap;
     const int64_t g = slot_index(d, s, list[k]);
     trb_track_log_entry e;
     e.frame = frame;
@@ -1389,7 +1397,7 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
   }
   __syncthreads();
   if (t == 0) {
-    d.n_log[s] = base + nl;
+    d.n_log[s] = base + (fits ? nl : 0);  // a step that does not fit logs nothing (and fails)
     d.frame_no[s] = frame + 1;
   }
 }
@@ -1729,11 +1737,13 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   validate_tracker(cfg);
   const int64_t n = static_cast<int64_t>(S) * T_;
   // int32 block: n_list,next_id,frame_no,err (4*S) + list, id,w,h,status,lost,used,pending (8*n)
-  i32_.alloc(sizeof(int32_t) * (4 * S + 9 * n));
+  if (track_cap < 1 || track_cap > (1 << 20)) throw Error(TRB_INVALID_ARGUMENT, "track capacity must be in [1, 2^20]");
+  if (log_cap < 1) throw Error(TRB_INVALID_ARGUMENT, "track-log capacity must be >= 1");
+  i32_.alloc(sizeof(int32_t) * (4 * S + 9 * n + 1));
   f64_.alloc(sizeof(double) * n * (2 + 4 * K_));
   lut_.alloc(static_cast<size_t>(n) * 256);
   log_.alloc(sizeof(trb_track_log_entry) * log_cap_ * S, false);
-  nlog_.alloc(sizeof(int64_t) * S);
+  nlog_.alloc(sizeof(int64_t) * 3 * S);  // head, tail, last frame's base
   // the cluster grid and breakpoint scratch are sized at the first process()
   // call, once the frame geometry (shared-memory need) is known
   int32_t* p = i32_.as<int32_t>();
@@ -1743,12 +1753,15 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   p += 4 * S;
   d_.list = p, d_.id = p + n, d_.w = p + 2 * n, d_.h = p + 3 * n, d_.status = p + 4 * n, d_.lost = p + 5 * n;
   d_.used = p + 6 * n, d_.pending = p + 7 * n, d_.iters = p + 8 * n;
+  d_.err_any = p + 9 * n;
   double* f = f64_.as<double>();
   d_.cx = f, d_.cy = f + n, d_.centers = f + 2 * n, d_.hist = f + 2 * n + 3 * K_ * n;
   d_.lut = lut_.as<uint8_t>();
   d_.log = log_.as<trb_track_log_entry>();
   d_.log_cap = log_cap_;
   d_.n_log = nlog_.as<int64_t>();
+  d_.log_tail = d_.n_log + S;
+  d_.step_log_base = d_.n_log + 2 * S;
   work_.alloc(sizeof(int32_t) * (2 * n + 4));
   d_.work = work_.as<int32_t>();
   d_.work_n = d_.work + n;
@@ -1816,13 +1829,15 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   *launches += 4;
 }
 
-void TrackerState::check_errors(cudaStream_t st) {
+void TrackerState::check_errors(cudaStream_t st, bool log_too) {
   std::vector<int32_t> e(S_);
   TRB_CUDA(cudaMemcpyAsync(e.data(), d_.err, sizeof(int32_t) * S_, cudaMemcpyDeviceToHost, st));
   TRB_CUDA(cudaStreamSynchronize(st));
   for (int s = 0; s < S_; ++s) {
     if (e[s] & 1) throw Error(TRB_CAPACITY, "tracker: track capacity exceeded on stream " + std::to_string(s));
-    if (e[s] & 2) throw Error(TRB_CAPACITY, "tracker: device track-log capacity exceeded on stream " + std::to_string(s));
+    if ((e[s] & 2) && log_too)
+      throw Error(TRB_CAPACITY, "tracker: track-log ring full on stream " + std::to_string(s) +
+                                    " (drain it with trb_streams_drain_log or raise trb_streams_options.log_cap)");
   }
 }
 
@@ -1871,18 +1886,72 @@ void TrackerState::track_model(int s, int i, double* centers, double* hist, cuda
 }
 
 int64_t TrackerState::log_size(int s, cudaStream_t st) {
-  int64_t n = 0;
-  TRB_CUDA(cudaMemcpyAsync(&n, d_.n_log + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int64_t ht[2] = {0, 0};
+  TRB_CUDA(cudaMemcpyAsync(&ht[0], d_.n_log + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaMemcpyAsync(&ht[1], d_.log_tail + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   TRB_CUDA(cudaStreamSynchronize(st));
+  return std::min(ht[0] - ht[1], log_cap_);
+}
+
+// entries [tail, tail + n) of the ring of stream s, oldest first
+static int64_t copy_log_ring(const TrackDev& d, int s, int64_t cap, trb_track_log_entry* out, int64_t* tail_out,
+                             cudaStream_t st) {
+  int64_t ht[2] = {0, 0};
+  TRB_CUDA(cudaMemcpyAsync(&ht[0], d.n_log + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaMemcpyAsync(&ht[1], d.log_tail + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  const int64_t tail = ht[1], n = std::min(std::min(ht[0] - tail, d.log_cap), cap);
+  const trb_track_log_entry* ring = d.log + static_cast<int64_t>(s) * d.log_cap;
+  const int64_t p0 = tail % d.log_cap, n0 = std::min(n, d.log_cap - p0);
+  if (n0 > 0)
+    TRB_CUDA(cudaMemcpyAsync(out, ring + p0, sizeof(trb_track_log_entry) * n0, cudaMemcpyDeviceToHost, st));
+  if (n > n0)
+    TRB_CUDA(cudaMemcpyAsync(out + n0, ring, sizeof(trb_track_log_entry) * (n - n0), cudaMemcpyDeviceToHost, st));
+  TRB_CUDA(cudaStreamSynchronize(st));
+  *tail_out = tail;
   return n;
 }
 
 void TrackerState::log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st) {
-  const int64_t n = std::min(log_size(s, st), std::min(cap, log_cap_));
-  if (n > 0)
-    TRB_CUDA(cudaMemcpyAsync(out, d_.log + static_cast<int64_t>(s) * log_cap_, sizeof(trb_track_log_entry) * n,
-                             cudaMemcpyDeviceToHost, st));
+  int64_t tail = 0;
+  copy_log_ring(d_, s, cap, out, &tail, st);
+}
+
+int64_t TrackerState::drain_log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st) {
+  int64_t tail = 0;
+  const int64_t n = copy_log_ring(d_, s, cap, out, &tail, st);
+  tail += n;
+  TRB_CUDA(cudaMemcpyAsync(d_.log_tail + s, &tail, sizeof(int64_t), cudaMemcpyHostToDevice, st));
   TRB_CUDA(cudaStreamSynchronize(st));
+  return n;
+}
+
+namespace {
+// One CTA per stream: the step's blob table and log entries, packed
+__global__ void __launch_bounds__(128) pack_step_kernel(TrackDev d, const trb_blob* blobs, int64_t blob_stride,
+                                                        const int32_t* nblobs, int32_t* n_blobs_out,
+                                                        trb_blob* blobs_out, int bcap, int32_t* n_log_out,
+                                                        trb_track_log_entry* log_out, int lcap) {
+  const int s = blockIdx.x;
+  const int nb = nblobs[s];
+  const int64_t base = d.step_log_base[s];
+  const int nl = static_cast<int>(d.n_log[s] - base);
+  if (threadIdx.x == 0) n_blobs_out[s] = nb, n_log_out[s] = nl;
+  const trb_blob* src = blobs + static_cast<int64_t>(s) * blob_stride;
+  trb_blob* dst = blobs_out + static_cast<int64_t>(s) * bcap;
+  for (int i = threadIdx.x; i < min(nb, bcap); i += blockDim.x) dst[i] = src[i];
+  const trb_track_log_entry* ring = d.log + static_cast<int64_t>(s) * d.log_cap;
+  trb_track_log_entry* ldst = log_out + static_cast<int64_t>(s) * lcap;
+  for (int i = threadIdx.x; i < min(nl, lcap); i += blockDim.x) ldst[i] = ring[(base + i) % d.log_cap];
+}
+}  // namespace
+
+void TrackerState::pack_step(const trb_blob* blobs, int64_t blob_stride, const int32_t* nblobs, int32_t* n_blobs_out,
+                             trb_blob* blobs_out, int bcap, int32_t* n_log_out, trb_track_log_entry* log_out, int lcap,
+                             cudaStream_t st) {
+  pack_step_kernel<<<S_, 128, 0, st>>>(d_, blobs, blob_stride, nblobs, n_blobs_out, blobs_out, bcap, n_log_out,
+                                       log_out, lcap);
+  TRB_LAUNCH_CHECK("pack_step_kernel");
 }
 
 int TrackerState::frames_processed(int s, cudaStream_t st) {

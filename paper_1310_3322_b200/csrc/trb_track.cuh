@@ -36,6 +36,7 @@ struct TrackDev {
   int32_t* next_id;
   int32_t* frame_no;
   int32_t* err;  // bit0 track-capacity overflow, bit1 log overflow
+  int32_t* err_any;  // OR of every stream's err (one word the host mirrors each step)
   // per slot [S][T]
   int32_t *id, *w, *h, *status, *lost, *used, *pending;
   int32_t* iters;  // mean-shift iterations of the last frame (scheduling hint)
@@ -49,9 +50,11 @@ struct TrackDev {
   const int32_t* nblobs;
   uint8_t* matched;  // [S][blob_stride] scratch
   // log
-  trb_track_log_entry* log;
+  trb_track_log_entry* log;  // [S][log_cap] ring
   int64_t log_cap;
-  int64_t* n_log;  // [S]
+  int64_t* n_log;     // [S] head: entries ever logged
+  int64_t* log_tail;  // [S] entries drained by the host
+  int64_t* step_log_base;  // [S] head before the last frame's entries
   // meanshift work queue (largest window first)
   int32_t* work;       // [S*T]
   int32_t* work_n;
@@ -84,10 +87,22 @@ class TrackerState {
   int num_tracks(int s, cudaStream_t st);
   void tracks(int s, trb_track* out, int cap, cudaStream_t st);
   void track_model(int s, int i, double* centers, double* hist, cudaStream_t st);
+  // entries logged and not drained yet (the whole log when never drained)
   int64_t log_size(int s, cudaStream_t st);
   void log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st);
+  // copy up to cap undrained entries out and release them; returns the count
+  int64_t drain_log(int s, trb_track_log_entry* out, int64_t cap, cudaStream_t st);
+  // the last processed frame's results packed for one D2H: per stream the
+  // blob count, the first bcap blobs, the number of log entries of the frame
+  // and its first lcap entries (regions as trb_step_output, device memory)
+  void pack_step(const trb_blob* blobs, int64_t blob_stride, const int32_t* nblobs, int32_t* n_blobs_out,
+                 trb_blob* blobs_out, int bcap, int32_t* n_log_out, trb_track_log_entry* log_out, int lcap,
+                 cudaStream_t st);
+  const int32_t* err_word() const { return d_.err_any; }
+  int track_cap() const { return T_; }
+  int64_t log_cap() const { return log_cap_; }
   int frames_processed(int s, cudaStream_t st);
-  void check_errors(cudaStream_t st);
+  void check_errors(cudaStream_t st, bool log_too = true);
   const trb_tracker_config& cfg() const { return cfg_; }
 
  private:

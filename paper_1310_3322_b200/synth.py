@@ -243,3 +243,22 @@ def raster_host(clip: Clip, rects: Sequence[Tuple[int, int, int, int]]):
         f[iy:iy + h, ix:ix + w, :] = np.array(s.color[:clip.channels] if clip.channels == 3 else s.color[:1],
                                               dtype=np.uint8)
     return f.reshape(-1) if clip.channels == 1 else f.reshape(-1)
+
+
+def device_frames(clips: Sequence[Clip], n_frames: int, cuda_stream: int = 0, device=None):
+    """Frames 0..n_frames-1 of every clip rasterised on the device (one
+    launch per clip): a uint8 tensor [S, n_frames, w*h*ch].  The integer
+    rects come from Clip.rects (synth.hpp:307-314's lround on the host); the
+    device only paints them (later shapes overwrite earlier ones).  This is
+    the bench's input path; tests hash it against the reference synth."""
+    import torch
+    from . import api
+    c0 = clips[0]
+    fb = c0.width * c0.height * c0.channels
+    buf = torch.empty((len(clips), n_frames, fb), dtype=torch.uint8, device=device or "cuda")
+    for s, c in enumerate(clips):
+        rects = [c.rects(t) for t in range(n_frames)]
+        api.synth_raster_frames(buf[s, 0].data_ptr(), fb, c.width, c.height, c.channels, c.background, rects,
+                                c.colors(), cuda_stream)
+    torch.cuda.synchronize()
+    return buf

@@ -22,7 +22,7 @@ ORACLE_DIR = os.path.join(ROOT, "oracle")
 ORC_SO = os.path.join(ORACLE_DIR, "liborc.so")
 REF_SO = os.path.join(ORACLE_DIR, "_ref", "libteamrec_ref.so")
 
-from paper_1310_3322_b200.abi import (BLOB, LOGE, MOTION_CFG, SEG_CFG, TRACK, TRACKER_CFG, blobs_to_array,  # noqa: E402
+from paper_1310_3322_b200.abi import (BLOB, BLOB_DTYPE, LOG_DTYPE, LOGE, MOTION_CFG, SEG_CFG, TRACK, TRACKER_CFG, blobs_to_array,  # noqa: E402
                                       log_to_array)
 
 
@@ -91,6 +91,9 @@ def orc_lib():
         L.orc_warp_frame.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_blob_features.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_plane_hash.restype = C.c_uint64
+        L.orc_plane_hash.argtypes = [C.c_void_p, C.c_int64]
+        L.orc_libm_hypot_n.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_libm_hypot.restype = C.c_double
         L.orc_libm_hypot.argtypes = [C.c_double, C.c_double]
         _orc = L
@@ -149,8 +152,55 @@ def ref_lib():
         L.ref_run_streams.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                       C.POINTER(MOTION_CFG), C.POINTER(SEG_CFG), C.POINTER(TRACKER_CFG), C.c_void_p,
                                       C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
+        L.ref_run_streams_detail.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                             C.POINTER(MOTION_CFG), C.POINTER(SEG_CFG), C.POINTER(TRACKER_CFG),
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                             C.c_int64, C.c_void_p]
         _ref = L
     return _ref
+
+
+def libm_hypot(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """The live glibc hypot, element by element (C loop)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    out = np.empty_like(x)
+    orc_lib().orc_libm_hypot_n(x.ctypes.data, y.ctypes.data, x.size, out.ctypes.data)
+    return out
+
+
+def plane_hash(a: np.ndarray) -> int:
+    """oracle/plane_hash.h digest of an array's bytes."""
+    a = np.ascontiguousarray(a)
+    return int(orc_lib().orc_plane_hash(a.ctypes.data, a.nbytes))
+
+
+def ref_run_streams_detail(frames_per_stream, w, h, ch, mcfg, scfg, tcfg, threads, bcap=64, lcap=4096):
+    """The unmodified reference per-frame loop (push -> label_blocked ->
+    Tracker::process) over each stream's frames ([n_frames, w*h*ch] uint8),
+    streams on `threads` host threads.  Per stream: dict(hashes [k,2] of
+    mask/labels per steady frame, nblobs [k], blobs [k, bcap], log)."""
+    L = ref_lib()
+    S = len(frames_per_stream)
+    nf = frames_per_stream[0].shape[0]
+    ptrs = (C.c_void_p * S)(*[f.ctypes.data for f in frames_per_stream])
+    steady = np.zeros(S, np.int64)
+    hashes = np.zeros((S, nf, 2), np.uint64)
+    nblobs = np.zeros((S, nf), np.int32)
+    blobs = np.zeros((S, nf, bcap), BLOB_DTYPE)
+    logs = np.zeros((S, lcap), LOG_DTYPE)
+    nlog = np.zeros(S, np.int64)
+    rc = L.ref_run_streams_detail(S, threads, w, h, ch, ptrs, nf, C.byref(mcfg), C.byref(scfg), C.byref(tcfg),
+                                  steady.ctypes.data, hashes.ctypes.data, nblobs.ctypes.data, blobs.ctypes.data,
+                                  bcap, logs.ctypes.data, lcap, nlog.ctypes.data)
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    out = []
+    for s in range(S):
+        k = int(steady[s])
+        assert nlog[s] <= lcap, "raise lcap"
+        out.append(dict(hashes=hashes[s, :k], nblobs=nblobs[s, :k], blobs=blobs[s, :k], log=logs[s, :nlog[s]]))
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -62,13 +62,14 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import bench
-        mine = bench.shard(rank, STREAMS_PER_RANK)
+        mine = bench.shard(rank, world, STREAMS_PER_RANK)
         digests = {s: _stream_digest(s) for s in mine}
         gathered = [None] * world
         dist.all_gather_object(gathered, {"streams": mine, "digests": digests})
         # per-rank "device time": rank r is slower by r ms; the job time is the max
         t = bench.max_over_ranks(10.0 + rank, world)
-        fps = bench.aggregate_fps(STREAMS_PER_RANK, world, 5, t / 1e3)
+        frames = bench.sum_over_ranks(STREAMS_PER_RANK * 5, world)
+        fps = bench.aggregate_fps(frames, t / 1e3)
         q.put((rank, gathered, t, fps))
     finally:
         dist.destroy_process_group()
@@ -105,15 +106,39 @@ def test_two_rank_sharding_and_timing():
 def test_reference_arm_runs_on_rank0_only(capsys):
     import bench
 
-    class A:
-        cpu_threads, steps, warmup, gpus = 1, 1, 0, 2
-    bench.reference_main(A(), rank=1, world=2)
+    args = bench.parse(["--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-threads", "1"])
+    bench.reference_main(args, rank=1, world=2)
     assert capsys.readouterr().out == ""
 
 
 def test_single_rank_helpers():
     import bench
-    assert bench.shard(0, 64) == list(range(64))
-    assert bench.shard(3, 4) == [12, 13, 14, 15]
+    assert bench.shard(0, 1, 64) == list(range(64))
+    assert bench.shard(3, 4, 4) == [12, 13, 14, 15]
+    # strong scaling: 64 streams over G GPUs, stream s on GPU floor(s*G/64)
+    for g in (1, 2, 4, 8):
+        parts = [bench.shard(r, g, 0, 64) for r in range(g)]
+        assert sorted(x for p in parts for x in p) == list(range(64))
+        assert all(len(p) == 64 // g for p in parts)
+        assert all(s * g // 64 == r for r, p in enumerate(parts) for s in p)
     assert bench.max_over_ranks(2.5, 1) == 2.5
-    assert bench.aggregate_fps(64, 1, 20, 0.2) == pytest.approx(6400.0)
+    assert bench.aggregate_fps(64 * 20, 0.2) == pytest.approx(6400.0)
+
+
+@pytest.mark.parametrize("extra,per_rank", [([], 64), (["--streams-total", "64"], 32)])
+def test_bench_gpus_flag_launches_that_many_ranks(extra, per_rank):
+    """`python bench.py --gpus 2` (no torchrun) re-launches itself with two
+    ranks; the ranks report world size 2 and disjoint shards covering the
+    job (weak: 64 streams per rank; strong: 64 streams over the job)."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"] + extra,
+                         capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    shards = line["shards"]
+    assert [len(x) for x in shards] == [per_rank, per_rank]
+    assert sorted(shards[0] + shards[1]) == list(range(2 * per_rank if not extra else 64))
+    assert line["max_over_ranks"] == 2.0
