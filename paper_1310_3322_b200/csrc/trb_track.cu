@@ -101,6 +101,7 @@ __device__ unsigned long long g_warpwalk[8 * 8 * 2];
 #endif
 
 #include "trb_track.cuh"
+#include "trb_xsum.cuh"
 
 namespace trb {
 
@@ -675,6 +676,233 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
   }
 }
 
+// ------------------------------------------------------ mean-shift, v2
+// The same meanshift_step / histogram_opt (tracking.hpp:79-157) on the
+// chunk-classified engine (trb_xsum.cuh): the K+1 histogram sums run straight
+// from raster order (no partition, no HBM scratch), the centroid's 3 sums
+// likewise.  Gray frames with the per-track gray->bin table (the tracker's
+// case) and K + 1 <= xs::kMaxL; everything else runs the v1 path above.
+struct V2Smem {
+  xs::Shared* xs;
+  Grp grp;
+  double* buf;    // [(K+1) * NT] scan / integer totals
+  float* ftot;    // [(K+1) * NT]
+  double* wsum;   // [(K+1) * 32]
+  double* ux2;    // [W]
+  double* uy2;    // [H + 1]
+  double* cen;    // [K*3]
+  double* q;      // [K]
+  double* p;      // [K]
+  double* wsq;    // [K]
+  double* bct;    // [K]
+  int* iscal;     // [16]
+  uint8_t* lut;   // [256]
+  static size_t bytes(int K, int W, int H) {
+    const int L = K + 1;
+    return sizeof(xs::Shared) + 16 + sizeof(double) * (static_cast<size_t>(L) * NT + L * 32 + W + H + 1 + 7 * K) +
+           sizeof(float) * L * NT + sizeof(int) * 16 + 256 + 16 * 16;
+  }
+  __device__ void carve(void* base, int K, int W, int H) {
+    char* p_ = static_cast<char*>(base);
+    auto take = [&](size_t n) {
+      char* r = p_;
+      p_ += (n + 15) & ~size_t(15);
+      return r;
+    };
+    const int L = K + 1;
+    xs = reinterpret_cast<xs::Shared*>(take(sizeof(xs::Shared)));
+    grp = Grp::cluster();
+    buf = reinterpret_cast<double*>(take(sizeof(double) * L * NT));
+    ftot = reinterpret_cast<float*>(take(sizeof(float) * L * NT));
+    wsum = reinterpret_cast<double*>(take(sizeof(double) * L * 32));
+    ux2 = reinterpret_cast<double*>(take(sizeof(double) * W));
+    uy2 = reinterpret_cast<double*>(take(sizeof(double) * (H + 1)));
+    cen = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
+    q = reinterpret_cast<double*>(take(sizeof(double) * K));
+    p = reinterpret_cast<double*>(take(sizeof(double) * K));
+    wsq = reinterpret_cast<double*>(take(sizeof(double) * K));
+    bct = reinterpret_cast<double*>(take(sizeof(double) * K));
+    iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
+    lut = reinterpret_cast<uint8_t*>(take(256));
+  }
+};
+
+// histogram elements: raster order over the window, value = the
+// Epanechnikov weight (tracking.hpp:86-91; uniform: 1), lane = the bin
+struct HistSrc2 {
+  const uint8_t* frame;
+  int fw, x0, y0, ww;
+  const double* ux2;
+  const double* uy2;
+  const uint8_t* lut;
+  int epan;
+  __device__ __forceinline__ double weight(int xx, double uy) const {
+    if (!epan) return 1.0;
+    const double t = xsub(1.0, xadd(ux2[xx], uy));
+    return (0.0 < t) ? t : 0.0;  // std::max(0.0, t)
+  }
+  struct Cursor {
+    const HistSrc2* s;
+    const uint8_t* row;
+    int xx, yy;
+    double uy;
+    __device__ __forceinline__ void next(bool& has, int& sel, double* v) {
+      sel = s->lut[row[xx]];
+      const double w = s->weight(xx, uy);
+      has = w > 0.0;  // if (wgt <= 0.0) continue;
+      v[0] = w;
+      if (++xx == s->ww) xx = 0, ++yy, row += s->fw, uy = s->uy2[yy];
+    }
+  };
+  __device__ Cursor begin(int j0) const {
+    Cursor c;
+    c.s = this;
+    c.yy = j0 / ww;
+    c.xx = j0 - c.yy * ww;
+    c.row = frame + static_cast<int64_t>(y0 + c.yy) * fw + x0;
+    c.uy = uy2[c.yy];
+    return c;
+  }
+  __device__ void get(int j, bool& has, int& sel, double* v) const {
+    const int yy = j / ww, xx = j - yy * ww;
+    sel = lut[frame[static_cast<int64_t>(y0 + yy) * fw + x0 + xx]];
+    const double w = weight(xx, uy2[yy]);
+    has = w > 0.0;
+    v[0] = w;
+  }
+};
+
+// centroid elements: every window pixel whose bin has p > 0, values
+// (w, w*x, w*y) with w = sqrt(q/p) of its bin (tracking.hpp:137-145)
+struct CentSrc2 {
+  const uint8_t* frame;
+  int fw, x0, y0, ww;
+  const uint8_t* lut;
+  const double* wsq;  // < 0 when p[b] <= 0
+  struct Cursor {
+    const CentSrc2* s;
+    const uint8_t* row;
+    int xx;
+    double xd, yd;
+    __device__ __forceinline__ void next(bool& has, int& sel, double* v) {
+      const double w = s->wsq[s->lut[row[xx]]];
+      sel = 0;
+      has = w >= 0.0;
+      v[0] = w;
+      v[1] = xmul(w, xd);
+      v[2] = xmul(w, yd);
+      xd = xadd(xd, 1.0);
+      if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0), row += s->fw;
+    }
+  };
+  __device__ Cursor begin(int j0) const {
+    Cursor c;
+    c.s = this;
+    const int yy = j0 / ww;
+    c.xx = j0 - yy * ww;
+    c.row = frame + static_cast<int64_t>(y0 + yy) * fw + x0;
+    c.xd = static_cast<double>(x0 + c.xx);
+    c.yd = static_cast<double>(y0 + yy);
+    return c;
+  }
+  __device__ void get(int j, bool& has, int& sel, double* v) const {
+    const int yy = j / ww, xx = j - yy * ww;
+    const double w = wsq[lut[frame[static_cast<int64_t>(y0 + yy) * fw + x0 + xx]]];
+    sel = 0;
+    has = w >= 0.0;
+    v[0] = w;
+    v[1] = xmul(w, static_cast<double>(x0 + xx));
+    v[2] = xmul(w, static_cast<double>(y0 + yy));
+  }
+};
+
+__device__ void fill_u2_v2(V2Smem& sm, const Win& r, double cx, double cy, int w, int h) {
+  const double hx = static_cast<double>(w) / 2.0, hy = static_cast<double>(h) / 2.0;
+  for (int i = threadIdx.x; i < r.x1 - r.x0; i += blockDim.x) {
+    const double ux = xdiv(xsub(static_cast<double>(r.x0 + i), cx), hx);
+    sm.ux2[i] = xmul(ux, ux);
+  }
+  for (int i = threadIdx.x; i <= r.y1 - r.y0; i += blockDim.x) {
+    const double uy = xdiv(xsub(static_cast<double>(r.y0 + i), cy), hy);
+    sm.uy2[i] = i < r.y1 - r.y0 ? xmul(uy, uy) : 0.0;
+  }
+}
+
+// histogram_opt on the v2 engine; the normalised histogram to out[K].
+__device__ bool window_histogram2(const uint8_t* frame, int fw, int fh, double cx, double cy, int w, int h, int K,
+                                  int epan, V2Smem& sm, double* out) {
+  const Win r = clip_window(fw, fh, cx, cy, w, h);
+  if (r.empty()) return false;
+  fill_u2_v2(sm, r, cx, cy, w, h);
+  __syncthreads();
+  const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
+  HistSrc2 hs{frame, fw, r.x0, r.y0, ww, sm.ux2, sm.uy2, sm.lut, epan};
+  xs::xsum_run<1, true>(sm.grp, N, K, hs, *sm.xs, sm.buf, sm.ftot, sm.wsum, g_trb_stats);
+  const double total = sm.xs->res[0];
+  if (!(total > 0.0)) {
+    __syncthreads();
+    return false;
+  }
+  for (int b = threadIdx.x; b < K; b += blockDim.x) out[b] = xdiv(sm.xs->res[1 + b], total);
+  __syncthreads();
+  return true;
+}
+
+// meanshift_step (tracking.hpp:125-157) on the v2 engine; the track's model
+// sits in sm.cen / sm.q / sm.lut.  cx, cy, status updated in place.
+__device__ void meanshift_device2(const uint8_t* frame, int fw, int fh, double& cx, double& cy, int w, int h,
+                                  int& status, int K, int max_iters, double eps, V2Smem& sm) {
+  if (threadIdx.x == 0) sm.iscal[10] = 0;
+  if (status != TRB_TRACK_ACTIVE) return;
+  if (threadIdx.x == 0) atomicAdd(&g_trb_stats[9], 1ull);
+  for (int it = 0; it < max_iters; ++it) {
+    if (threadIdx.x == 0) {
+      sm.iscal[10] = it + 1;
+      if (sm.grp.rank_ == 0) {
+        const Win rw = clip_window(fw, fh, cx, cy, w, h);
+        atomicAdd(&g_trb_stats[5], 1ull);
+        atomicAdd(&g_trb_stats[11], static_cast<unsigned long long>(rw.empty() ? 0 : (rw.x1 - rw.x0) * (rw.y1 - rw.y0)));
+      }
+    }
+    const bool ok = window_histogram2(frame, fw, fh, cx, cy, w, h, K, 1, sm, sm.p);
+    if (ok)
+      for (int b = threadIdx.x; b < K; b += blockDim.x) {
+        sm.bct[b] = xsqrt(xmul(sm.p[b], sm.q[b]));
+        sm.wsq[b] = sm.p[b] <= 0.0 ? -1.0 : xsqrt(xdiv(sm.q[b], sm.p[b]));
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int lost = !ok;
+      if (ok) {
+        double bc = 0.0;  // bhattacharyya, tracking.hpp:114-119 (in bin order)
+        for (int i = 0; i < K; ++i) bc = xadd(bc, sm.bct[i]);
+        lost = !(bc > 0.0);
+      }
+      sm.iscal[0] = lost;
+    }
+    __syncthreads();
+    if (sm.iscal[0]) {
+      status = TRB_TRACK_LOST;
+      return;
+    }
+    const Win r = clip_window(fw, fh, cx, cy, w, h);
+    const int ww = r.x1 - r.x0;
+    CentSrc2 cs{frame, fw, r.x0, r.y0, ww, sm.lut, sm.wsq};
+    xs::xsum_run<3, false>(sm.grp, ww * (r.y1 - r.y0), 0, cs, *sm.xs, sm.buf, sm.ftot, sm.wsum, g_trb_stats);
+    const double sw = sm.xs->res[0], sx = sm.xs->res[1], sy = sm.xs->res[2];
+    __syncthreads();
+    if (sw <= 0.0) {
+      status = TRB_TRACK_LOST;
+      return;
+    }
+    const double nx = xdiv(sx, sw), ny = xdiv(sy, sw);
+    const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
+    cx = nx;
+    cy = ny;
+    if (shift < eps) break;
+  }
+}
+
 // ------------------------------------------------------------- k-means
 // Integer-valued RGB samples; the window of a frame or an explicit list.
 struct FrameWindowSrc {
@@ -1241,6 +1469,73 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(T
   }
 }
 
+// v2 mean-shift kernel: the same persistent queue (costliest first, split
+// mode for cheap tracks) over meanshift_device2; no HBM scratch.
+__device__ void meanshift_item2(const TrackDev& d, int q, V2Smem& sm, bool lead) {
+  const int K = d.K;
+  const int item = d.work[q];
+  const int s = item / d.T, i = item - s * d.T;
+  const int slot = d.list[static_cast<int64_t>(s) * d.T + i];
+  const int64_t g = slot_index(d, s, slot);
+  int status = d.status[g];
+  if (status != TRB_TRACK_ACTIVE) return;
+  for (int k = threadIdx.x; k < 3 * K; k += NT) sm.cen[k] = d.centers[g * 3 * K + k];
+  for (int k = threadIdx.x; k < K; k += NT) sm.q[k] = d.hist[g * K + k];
+  for (int k = threadIdx.x; k < 256; k += NT) sm.lut[k] = d.lut[g * 256 + k];
+  __syncthreads();
+  double cx = d.cx[g], cy = d.cy[g];
+  meanshift_device2(d.frames[s], d.W, d.H, cx, cy, d.w[g], d.h[g], status, K, d.max_iters, d.eps, sm);
+  sm.grp.sync();  // every CTA has read the track before the leader updates it
+  if (lead) {
+    d.cx[g] = cx;
+    d.cy[g] = cy;
+    d.status[g] = status;
+    d.iters[g] = sm.iscal[10];
+  }
+}
+
+__global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(TrackDev d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  V2Smem sm;
+  sm.carve(smem_raw, d.K, d.W, d.H);
+  const int rank = static_cast<int>(cl.block_rank());
+  const int n_work = *d.work_n;
+  bool split = false;
+  for (;;) {
+    if (!split) {
+      if (rank == 0 && threadIdx.x == 0) {
+        const int q = atomicAdd(d.work_head, 1);
+        sm.iscal[8] = q < n_work ? q : -1;
+      }
+      cl.sync();
+      sm.iscal[11] = *cl.map_shared_rank(&sm.iscal[8], 0);
+      cl.sync();
+    } else {
+      if (threadIdx.x == 0) {
+        const int q = atomicAdd(d.work_head, 1);
+        sm.iscal[11] = q < n_work ? q : -1;
+      }
+      __syncthreads();
+    }
+    const int q = sm.iscal[11];
+    __syncthreads();
+    if (q < 0) break;
+    bool to_split = false;
+    if (!split) {
+      const int item = d.work[q];
+      const int s = item / d.T, i = item - s * d.T;
+      const int64_t g = slot_index(d, s, d.list[static_cast<int64_t>(s) * d.T + i]);
+      to_split = split_class(d, g);
+    }
+    meanshift_item2(d, q, sm, (split || rank == 0) && threadIdx.x == 0);
+    if (to_split) {
+      split = true;
+      sm.grp = Grp::single();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- gate
 // One CTA per stream: spawn gating (tracking.hpp:185-195), spawn_track's
 // geometry and success conditions (:208-234), lost counting and retirement
@@ -1476,6 +1771,36 @@ struct OneArgs {
   int64_t maxN;
 };
 
+// One cluster: meanshift_step or histogram_opt on a single explicit track,
+// on the v2 engine (gray frames, K + 1 <= xs::kMaxL).
+__global__ void __launch_bounds__(NT) track_one2_kernel(OneArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  V2Smem sm;
+  sm.carve(smem_raw, a.K, a.W, a.H);
+  for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
+  if (a.target)
+    for (int k = threadIdx.x; k < a.K; k += NT) sm.q[k] = a.target[k];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    const double dv = v;
+    sm.lut[v] = static_cast<uint8_t>(q_assign(sm.cen, a.K, dv, dv, dv));
+  }
+  __syncthreads();
+  const bool lead = cl.block_rank() == 0;
+  if (a.mode == 0) {
+    double cx = a.cx, cy = a.cy;
+    int status = a.status;
+    meanshift_device2(a.frame, a.W, a.H, cx, cy, a.w, a.h, status, a.K, a.max_iters, a.eps, sm);
+    if (lead && threadIdx.x == 0) a.out[0] = cx, a.out[1] = cy, a.out[2] = status;
+  } else {
+    const bool ok = window_histogram2(a.frame, a.W, a.H, a.cx, a.cy, a.w, a.h, a.K, a.epan, sm, sm.p);
+    if (lead) {
+      for (int k = threadIdx.x; k < a.K; k += NT) a.out[k] = sm.p[k];
+      if (threadIdx.x == 0) a.out[a.K] = ok ? 1.0 : 0.0;
+    }
+  }
+}
+
 // One cluster: meanshift_step or histogram_opt on a single explicit track.
 __global__ void __launch_bounds__(NT) track_one_kernel(OneArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1676,6 +2001,22 @@ static size_t check_smem(int K, int W, int H) {
   return b;
 }
 
+// The v2 engine (trb_xsum.cuh) serves gray frames with K + 1 <= xs::kMaxL
+// when TRB_ENGINE=2 (under validation); default: the v1 engine (trb_osum.cuh).
+static bool engine_v2(int K, int CH) {
+  static const int sel = [] {
+    const char* e = getenv("TRB_ENGINE");
+    return e ? atoi(e) : 1;
+  }();
+  return sel == 2 && CH == 1 && K + 1 <= xs::kMaxL;
+}
+
+static size_t check_smem_v2(int K, int W, int H) {
+  const size_t b = V2Smem::bytes(K, W, H);
+  if (b > 220 * 1024) throw Error(TRB_CONFIG_ERROR, "tracker frame size exceeds the device shared-memory budget");
+  return b;
+}
+
 // Cluster size of the tracker kernels (CTAs per track).  TRB_CLUSTER
 // overrides; sizes above 8 use the non-portable cluster attribute.
 static int cluster_size() {
@@ -1819,9 +2160,22 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     d_.scratch = bp_.as<unsigned char>();
     smem_set_ = smem;
   }
+  const bool v2 = engine_v2(K_, ch);
+  if (v2 && smem2_ == 0) {
+    smem2_ = check_smem_v2(K_, w, h);
+    prepare_cluster_kernel(track_meanshift2_kernel, smem2_, G);
+    const int64_t items = static_cast<int64_t>(S_) * T_;
+    grid2_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift2_kernel, smem2_, G)));
+    if (const char* eg = getenv("TRB_TRACK_CLUSTERS")) grid2_ = std::max(1, std::min(grid2_, atoi(eg)));
+    if (getenv("TRB_VERBOSE"))
+      fprintf(stderr, "[trb] tracker v2: %d clusters of %d CTAs, %zu B dynamic smem per CTA\n", grid2_, G, smem2_);
+  }
   track_schedule_kernel<<<1, 1024, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_schedule_kernel");
-  launch_cluster(track_meanshift_kernel, grid_, G, smem, st, d_);
+  if (v2)
+    launch_cluster(track_meanshift2_kernel, grid2_, G, smem2_, st, d_);
+  else
+    launch_cluster(track_meanshift_kernel, grid_, G, smem, st, d_);
   if (after_meanshift) TRB_CUDA(cudaEventRecord(after_meanshift, st));
   track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
@@ -1977,6 +2331,12 @@ static void scratch_for(OneArgs& a) {
 
 static void launch_one(const OneArgs& a, size_t smem, cudaStream_t st) {
   const int G = cluster_size();
+  if (engine_v2(a.K, a.CH)) {
+    const size_t s2 = check_smem_v2(a.K, a.W, a.H);
+    prepare_cluster_kernel(track_one2_kernel, s2, G);
+    launch_cluster(track_one2_kernel, 1, G, s2, st, a);
+    return;
+  }
   prepare_cluster_kernel(track_one_kernel, smem, G);
   launch_cluster(track_one_kernel, 1, G, smem, st, a);
 }

@@ -112,8 +112,8 @@ class TrackerState {
   DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_;
   TrackDev d_{};
   int64_t matched_cap_ = 0;
-  int grid_ = 0;
-  size_t smem_set_ = 0;
+  int grid_ = 0, grid2_ = 0;
+  size_t smem_set_ = 0, smem2_ = 0;
 };
 
 // device diagnostics counters (see g_trb_stats in trb_track.cu)
