@@ -663,8 +663,8 @@ STAT_NAMES = ("osum_calls", "osum_sums", "osum_fallback_sums", "osum_breakpoints
               "meanshift_iters", "spawns", "lloyd_iters", "empty_cluster_passes", "tracks_advanced",
               "", "meanshift_window_px", "fast_warps", "", "general_warps", "",
               "bad_scan_merge", "bad_phaseB_merge", "bad_bp_overflow", "bad_cross_cta", "bad_fold_carry",
-              "bad_fold_merge", "bad_verify_start", "bad_verify_end", "bad_final_start", "bad_final_end",
-              "many_bp_centroid", "many_bp_total", "many_bp_bin", "max_bp")
+              "bad_fold_merge", "bad_verify_start", "bad_verify_end", "rec_fixed_lanes", "rec_selected_lanes",
+              "rec_heads", "", "max_bp_cta", "max_bp")
 
 
 def debug_stats(reset: bool = False) -> dict:

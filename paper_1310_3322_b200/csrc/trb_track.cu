@@ -101,6 +101,8 @@ __device__ unsigned long long g_warpwalk[8 * 8 * 2];
 #endif
 
 #include "trb_track.cuh"
+// v2 engine phase marks (diagnostics build): hist run slots 1..7, centroid 9..15
+#define TRB_XS_MARK(k) TRB_PHASE(1 + (k) + (NF == 1 ? 0 : 8), rank, G)
 #include "trb_xsum.cuh"
 
 namespace trb {
@@ -685,10 +687,11 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
 struct V2Smem {
   xs::Shared* xs;
   Grp grp;
-  double* buf;    // [(K+1) * NT] scan / integer totals
+  double* buf;    // [(K+1) * NT] scan / integer totals / gathered records
+  int all_cap;    // gathered records that fit in buf
   float* ftot;    // [(K+1) * NT]
   double* wsum;   // [(K+1) * 32]
-  double* ux2;    // [W]
+  double* ux2;    // [W]      (global, this CTA's slice: L1-resident; keeps shared memory for the engine)
   double* uy2;    // [H + 1]
   double* cen;    // [K*3]
   double* q;      // [K]
@@ -699,10 +702,12 @@ struct V2Smem {
   uint8_t* lut;   // [256]
   static size_t bytes(int K, int W, int H) {
     const int L = K + 1;
-    return sizeof(xs::Shared) + 16 + sizeof(double) * (static_cast<size_t>(L) * NT + L * 32 + W + H + 1 + 7 * K) +
+    (void)W, (void)H;
+    return sizeof(xs::Shared) + 16 + sizeof(double) * (static_cast<size_t>(L) * NT + L * 32 + 7 * K) +
            sizeof(float) * L * NT + sizeof(int) * 16 + 256 + 16 * 16;
   }
-  __device__ void carve(void* base, int K, int W, int H) {
+  static __host__ __device__ size_t u2_doubles(int W, int H) { return static_cast<size_t>(W) + H + 1; }  // per CTA
+  __device__ void carve(void* base, int K, int W, int H, double* u2_base) {
     char* p_ = static_cast<char*>(base);
     auto take = [&](size_t n) {
       char* r = p_;
@@ -713,10 +718,11 @@ struct V2Smem {
     xs = reinterpret_cast<xs::Shared*>(take(sizeof(xs::Shared)));
     grp = Grp::cluster();
     buf = reinterpret_cast<double*>(take(sizeof(double) * L * NT));
+    all_cap = static_cast<int>(sizeof(double) * L * NT / sizeof(xs::Rec2));
     ftot = reinterpret_cast<float*>(take(sizeof(float) * L * NT));
     wsum = reinterpret_cast<double*>(take(sizeof(double) * L * 32));
-    ux2 = reinterpret_cast<double*>(take(sizeof(double) * W));
-    uy2 = reinterpret_cast<double*>(take(sizeof(double) * (H + 1)));
+    ux2 = u2_base + static_cast<size_t>(blockIdx.x) * u2_doubles(W, H);
+    uy2 = ux2 + W;
     cen = reinterpret_cast<double*>(take(sizeof(double) * 3 * K));
     q = reinterpret_cast<double*>(take(sizeof(double) * K));
     p = reinterpret_cast<double*>(take(sizeof(double) * K));
@@ -837,7 +843,7 @@ __device__ bool window_histogram2(const uint8_t* frame, int fw, int fh, double c
   __syncthreads();
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
   HistSrc2 hs{frame, fw, r.x0, r.y0, ww, sm.ux2, sm.uy2, sm.lut, epan};
-  xs::xsum_run<1, true>(sm.grp, N, K, hs, *sm.xs, sm.buf, sm.ftot, sm.wsum, g_trb_stats);
+  xs::xsum_run<1, true>(sm.grp, N, K, hs, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap, g_trb_stats);
   const double total = sm.xs->res[0];
   if (!(total > 0.0)) {
     __syncthreads();
@@ -864,6 +870,12 @@ __device__ void meanshift_device2(const uint8_t* frame, int fw, int fh, double& 
         atomicAdd(&g_trb_stats[11], static_cast<unsigned long long>(rw.empty() ? 0 : (rw.x1 - rw.x0) * (rw.y1 - rw.y0)));
       }
     }
+#ifdef TRB_DIAG
+    {
+      const Win rw = clip_window(fw, fh, cx, cy, w, h);
+      TRB_PHASE_BEGIN(rw.empty() ? 0 : (rw.x1 - rw.x0) * (rw.y1 - rw.y0), sm.grp.rank_);
+    }
+#endif
     const bool ok = window_histogram2(frame, fw, fh, cx, cy, w, h, K, 1, sm, sm.p);
     if (ok)
       for (int b = threadIdx.x; b < K; b += blockDim.x) {
@@ -888,7 +900,8 @@ __device__ void meanshift_device2(const uint8_t* frame, int fw, int fh, double& 
     const Win r = clip_window(fw, fh, cx, cy, w, h);
     const int ww = r.x1 - r.x0;
     CentSrc2 cs{frame, fw, r.x0, r.y0, ww, sm.lut, sm.wsq};
-    xs::xsum_run<3, false>(sm.grp, ww * (r.y1 - r.y0), 0, cs, *sm.xs, sm.buf, sm.ftot, sm.wsum, g_trb_stats);
+    xs::xsum_run<3, false>(sm.grp, ww * (r.y1 - r.y0), 0, cs, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap,
+                           g_trb_stats);
     const double sw = sm.xs->res[0], sx = sm.xs->res[1], sy = sm.xs->res[2];
     __syncthreads();
     if (sw <= 0.0) {
@@ -899,6 +912,7 @@ __device__ void meanshift_device2(const uint8_t* frame, int fw, int fh, double& 
     const double shift = glibc_hypot(xsub(nx, cx), xsub(ny, cy));
     cx = nx;
     cy = ny;
+    TRB_PHASE(16, sm.grp.rank_, sm.grp.size_);
     if (shift < eps) break;
   }
 }
@@ -1498,7 +1512,7 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   V2Smem sm;
-  sm.carve(smem_raw, d.K, d.W, d.H);
+  sm.carve(smem_raw, d.K, d.W, d.H, d.u2);
   const int rank = static_cast<int>(cl.block_rank());
   const int n_work = *d.work_n;
   bool split = false;
@@ -1769,6 +1783,7 @@ struct OneArgs {
   unsigned char* scratch;
   size_t scratch_stride;
   int64_t maxN;
+  double* u2;  // v2: per-CTA ux2/uy2 slices
 };
 
 // One cluster: meanshift_step or histogram_opt on a single explicit track,
@@ -1777,10 +1792,11 @@ __global__ void __launch_bounds__(NT) track_one2_kernel(OneArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   V2Smem sm;
-  sm.carve(smem_raw, a.K, a.W, a.H);
+  sm.carve(smem_raw, a.K, a.W, a.H, a.u2);
   for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
   if (a.target)
     for (int k = threadIdx.x; k < a.K; k += NT) sm.q[k] = a.target[k];
+  __syncthreads();  // the gray -> bin table reads every centre
   for (int v = threadIdx.x; v < 256; v += blockDim.x) {
     const double dv = v;
     sm.lut[v] = static_cast<uint8_t>(q_assign(sm.cen, a.K, dv, dv, dv));
@@ -2167,6 +2183,8 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     const int64_t items = static_cast<int64_t>(S_) * T_;
     grid2_ = static_cast<int>(std::min<int64_t>(items, max_clusters(track_meanshift2_kernel, smem2_, G)));
     if (const char* eg = getenv("TRB_TRACK_CLUSTERS")) grid2_ = std::max(1, std::min(grid2_, atoi(eg)));
+    u2_.alloc(sizeof(double) * V2Smem::u2_doubles(w, h) * static_cast<size_t>(grid2_) * G, false);
+    d_.u2 = u2_.as<double>();
     if (getenv("TRB_VERBOSE"))
       fprintf(stderr, "[trb] tracker v2: %d clusters of %d CTAs, %zu B dynamic smem per CTA\n", grid2_, G, smem2_);
   }
@@ -2333,8 +2351,12 @@ static void launch_one(const OneArgs& a, size_t smem, cudaStream_t st) {
   const int G = cluster_size();
   if (engine_v2(a.K, a.CH)) {
     const size_t s2 = check_smem_v2(a.K, a.W, a.H);
+    thread_local DevBuf u2;
+    u2.alloc(sizeof(double) * V2Smem::u2_doubles(a.W, a.H) * G, false);
+    OneArgs b = a;
+    b.u2 = u2.as<double>();
     prepare_cluster_kernel(track_one2_kernel, s2, G);
-    launch_cluster(track_one2_kernel, 1, G, s2, st, a);
+    launch_cluster(track_one2_kernel, 1, G, s2, st, b);
     return;
   }
   prepare_cluster_kernel(track_one_kernel, smem, G);

@@ -72,6 +72,7 @@ struct TrackDev {
   unsigned char* scratch;
   size_t scratch_stride;
   int64_t maxN;
+  double* u2;  // v2 engine: per-CTA ux2 / uy2 (W + H + 1 doubles each)
 };
 
 class TrackerState {
@@ -109,7 +110,7 @@ class TrackerState {
   trb_tracker_config cfg_;
   int S_, T_, K_;
   int64_t log_cap_;
-  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_;
+  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_, u2_;
   TrackDev d_{};
   int64_t matched_cap_ = 0;
   int grid_ = 0, grid2_ = 0;

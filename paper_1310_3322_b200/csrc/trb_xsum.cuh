@@ -39,29 +39,41 @@
 
 #include "trb_osum.cuh"
 
+#ifndef TRB_XS_MARK
+#define TRB_XS_MARK(k) ((void)0)
+#endif
+
 namespace trb {
 namespace xs {
 
 constexpr int kQ = 3;         // selected lanes held in registers per pass
 constexpr int kMaxL = 20;     // lanes per run (NF + K): K <= 16 bins + total
-constexpr int kRecCta = 320;  // breakpoint records per CTA per run
-constexpr int kRecAll = 768;  // gathered records per run (cluster)
+constexpr int kRecCta = 768;   // breakpoint records per CTA per run (a single-CTA group holds them all)
 constexpr long long kMant = (1LL << 52) - 1;
 
 enum { kNone = 0, kSafe = 1, kGeneral = 2, kHead = 3 };
+enum { kRecStep = 0, kRecHead = 1, kRecTie = 2 };
 
 struct Rec {
-  double v;       // step: the element value; head: the exact sum of the head chunk
+  double v;       // step: the element value; head: the exact head sum; tie piece: the bits of A
   long long ip;   // lane integer prefix at the record (thread-local, then CTA, then cluster)
-  int j;          // element index (order of records of a lane)
+  long long b;    // tie piece: B
+  int key;        // 4*j + sub: the order of a lane's records (sub 0 piece flush, 1 step, 2 chunk-end flush)
   uint8_t lane;
-  uint8_t kind;   // 0 step, 1 head
+  uint8_t kind;
   uint16_t lrank; // rank among this CTA's records of the lane
 };
-static_assert(sizeof(Rec) == 24, "Rec layout");
+static_assert(sizeof(Rec) == 32, "Rec layout");
+// a gathered record (cluster order), placed in the free scan buffer
+struct Rec2 {
+  double v;
+  long long ip, b;
+  int kind, pad;
+};
+static_assert(sizeof(Rec2) == 32, "Rec2 layout");
 
-// Static shared memory of the engine (the per-thread x per-lane scan buffer
-// is dynamic: L * blockDim.x 8-byte words).
+// Static shared memory of the engine (the per-thread x per-lane scan buffers
+// are dynamic).
 struct Shared {
   double cta_tot[kMaxL];        // phase A: this CTA's approximate lane totals (read remotely)
   long long cta_ip[kMaxL];      // phase C: this CTA's lane integer totals (read remotely)
@@ -77,16 +89,17 @@ struct Shared {
   double res[kMaxL];
   int fail;
   Rec rec[kRecCta];
-  Rec all[kRecAll];
 };
 
 struct LaneSt {
-  long long B;  // sum of the integer steps since the chunk start (units of the lane's binade at that time)
-  double M;     // 2^e of the binade the integer steps use
-  double hi;    // general: arm bound (largest prefix still safe in binade e), -1 disarmed
-  double P;     // general: running approximate prefix; head: exact running sum
+  long long B;       // integer steps since the chunk start, outside tie pieces (units of the binade at the time)
+  long long pA, pB;  // the open tie piece X -> E(X + pA) + pB (pt = 1)
+  double M;          // 2^e of the binade the integer steps use
+  double hi;         // general: arm bound (largest prefix still safe in binade e), -1 disarmed
+  double P;          // general: running approximate prefix; head: exact running sum
   int mode;
-  int bin;      // selected lanes: the bin (-1 = empty slot)
+  int bin;           // selected lanes: the bin (-1 = empty slot)
+  int pt;            // a tie piece is open
 };
 
 struct Ctx {
@@ -98,31 +111,51 @@ struct Ctx {
 __device__ __forceinline__ double pow2(int eb) {  // eb = biased exponent
   return __longlong_as_double(static_cast<long long>(eb) << 52);
 }
+__device__ __forceinline__ long long up_even(long long y) { return y + (y & 1); }
 
-__device__ __forceinline__ void emit(const Ctx& c, int lane, int kind, double v, long long ip, int j) {
+__device__ __forceinline__ void emit(const Ctx& c, int lane, int kind, double v, long long ip, long long b, int key) {
   const int idx = atomicAdd(&c.s->nrec, 1);
   if (idx < kRecCta) {
     Rec& r = c.s->rec[idx];
-    r.v = v, r.ip = ip, r.j = j, r.lane = static_cast<uint8_t>(lane), r.kind = static_cast<uint8_t>(kind);
+    r.v = v, r.ip = ip, r.b = b, r.key = key, r.lane = static_cast<uint8_t>(lane), r.kind = static_cast<uint8_t>(kind);
     r.lrank = 0;
   } else {
     c.s->fail = 1;  // overflow: every CTA learns it through cta_flag
   }
 }
 
-// An integer step of binade M = 2^e: false on a tie (a/u = k + 1/2).
-__device__ __forceinline__ bool int_step(double a, double M, long long& B) {
-  const double y = xadd(M, a);
-  const double d = xsub(a, xsub(y, M));
-  const double hu = __longlong_as_double(__double_as_longlong(M) - (53LL << 52));  // u/2
-  if (fabs(d) == hu) return false;
-  B += __double_as_longlong(y) - __double_as_longlong(M);
-  return true;
+// A step of binade M = 2^e that stays in the binade: X -> X + RN(a/u), or on
+// a tie (a/u = k + 1/2) X -> E(X + k), E = round up to even.  Plain steps add
+// to B; from the first tie on, the steps compose into a tie piece
+// (E(X + A) + B composed with +r or with tie(k) keeps that form, because
+// E(X + A) is even: E(E(X + A) + y) = E(X + A) + E(y)) — one record per
+// piece instead of one per tie (a lane summing one repeated value can tie on
+// every element of a binade).
+__device__ __forceinline__ void int_step(LaneSt& L, double a) {
+  const double y = xadd(L.M, a);
+  const double d = xsub(a, xsub(y, L.M));
+  const double hu = __longlong_as_double(__double_as_longlong(L.M) - (53LL << 52));  // u/2
+  const long long r = __double_as_longlong(y) - __double_as_longlong(L.M);
+  if (fabs(d) == hu) {
+    const long long k = d > 0.0 ? r : r - 1;
+    if (!L.pt) L.pt = 1, L.pA = k, L.pB = 0;
+    else L.pB = up_even(L.pB + k);
+  } else if (L.pt) {
+    L.pB += r;
+  } else {
+    L.B += r;
+  }
+}
+
+__device__ __forceinline__ void flush_piece(LaneSt& L, int lane, int key, const Ctx& c) {
+  if (!L.pt) return;
+  emit(c, lane, kRecTie, __longlong_as_double(L.pA), L.B, L.pB, key);
+  L.pt = 0;
 }
 
 // Chunk classification from its approximate start / end prefixes.
 __device__ __forceinline__ void classify(LaneSt& L, bool present, double p0, double p1, const Ctx& c) {
-  L.B = 0, L.hi = -1.0, L.M = 1.0, L.P = 0.0;
+  L.B = 0, L.hi = -1.0, L.M = 1.0, L.P = 0.0, L.pt = 0, L.pA = 0, L.pB = 0;
   if (!present) {
     L.mode = kNone;
     return;
@@ -152,7 +185,7 @@ __device__ __forceinline__ void general_step(LaneSt& L, double a, int j, int lan
   const double Pp = L.P, Pn = xadd(Pp, a);
   L.P = Pn;
   if (Pn <= L.hi) {
-    if (!int_step(a, L.M, L.B)) emit(c, lane, 0, a, L.B, j);
+    int_step(L, a);
     return;
   }
   if (a == 0.0) return;  // a zero step never changes S
@@ -160,12 +193,14 @@ __device__ __forceinline__ void general_step(LaneSt& L, double a, int j, int lan
   const int eb = static_cast<int>(bp >> 52);
   if (Pp > 0.0 && eb == static_cast<int>(bn >> 52) && eb > 64 && eb < 1982 && (bp & kMant) >= c.lowm &&
       (bn & kMant) <= c.highm) {
+    if (L.pt && pow2(eb) != L.M) flush_piece(L, lane, 4 * j, c);  // a piece never spans two binades
     L.hi = __longlong_as_double((static_cast<long long>(eb) << 52) | c.highm);
     L.M = pow2(eb);
-    if (!int_step(a, L.M, L.B)) emit(c, lane, 0, a, L.B, j);
+    int_step(L, a);
     return;
   }
-  emit(c, lane, 0, a, L.B, j);
+  flush_piece(L, lane, 4 * j, c);
+  emit(c, lane, kRecStep, a, L.B, 0, 4 * j + 1);
   L.hi = -1.0;
   const int en = static_cast<int>(bn >> 52);
   if (Pn > 0.0 && en > 64 && en < 1982 && (bn & kMant) >= c.lowm) {  // re-arm from the replayed step's prefix
@@ -176,12 +211,18 @@ __device__ __forceinline__ void general_step(LaneSt& L, double a, int j, int lan
 
 __device__ __forceinline__ void step(LaneSt& L, double a, int j, int lane, const Ctx& c) {
   if (L.mode == kSafe) {
-    if (!int_step(a, L.M, L.B)) emit(c, lane, 0, a, L.B, j);
+    int_step(L, a);
   } else if (L.mode == kHead) {
     L.P = xadd(L.P, a);
   } else if (L.mode == kGeneral) {
     general_step(L, a, j, lane, c);
   }
+}
+
+// end of a lane's pass over the chunk: close a tie piece, emit a head's sum
+__device__ __forceinline__ void finish_lane(LaneSt& L, int lane, int j0, int j1, const Ctx& c) {
+  if (L.mode == kHead) emit(c, lane, kRecHead, L.P, 0, 0, 4 * j0);
+  flush_piece(L, lane, 4 * (j1 - 1) + 2, c);
 }
 
 __device__ __forceinline__ void swap_lane(LaneSt& a, LaneSt& b) {
@@ -236,7 +277,19 @@ __device__ __forceinline__ double add_units(double S, long long n, bool& ok) {
   ok &= S > 0.0 && e > 0 && e < 2047 && n > 0;
   const long long X = (b & kMant) | (1LL << 52);
   const long long X2 = X + n;
-  ok &= X2 < (1LL << 53);
+  ok &= X2 >= (1LL << 52) && X2 < (1LL << 53);
+  return __longlong_as_double((e << 52) | (X2 & kMant));
+}
+
+// S (exact, positive normal) through a tie piece of its own binade:
+// X -> E(X + A) + B.
+__device__ __forceinline__ double apply_tie(double S, long long A, long long B, bool& ok) {
+  const long long b = __double_as_longlong(S);
+  const long long e = b >> 52;
+  ok &= S > 0.0 && e > 0 && e < 2047;
+  const long long X = (b & kMant) | (1LL << 52);
+  const long long X2 = up_even(X + A) + B;
+  ok &= X2 >= (1LL << 52) && X2 < (1LL << 53);
   return __longlong_as_double((e << 52) | (X2 & kMant));
 }
 
@@ -248,9 +301,11 @@ __device__ __forceinline__ double add_units(double S, long long n, bool& ok) {
 // buf: dynamic shared scratch of L * blockDim.x 8-byte words, ftot: L *
 // blockDim.x floats, wsum: L * 32 8-byte words.
 // Results: s.res[l], identical in every CTA of the group, on return.
+// all_cap: Rec2 records that fit in buf (its full allocation, which may
+// exceed this run's L * blockDim.x words).
 template <int NF, bool SEL, class Src>
 __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s, double* buf, float* ftot,
-                         double* wsumd, unsigned long long* stats) {
+                         double* wsumd, int all_cap, unsigned long long* stats) {
   const int NT = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int GT = G * NT, gt = rank * NT + t;
@@ -303,6 +358,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
 #pragma unroll
     for (int l = 0; l < NF; ++l) buf[l * NT + t] = aF[l];
   }
+  TRB_XS_MARK(0);
   // own chunk totals (float: only the chunk-end prefix needs them, with the
   // widened upper margin highm_end)
   for (int l = 0; l < L; ++l) ftot[l * NT + t] = static_cast<float>(buf[l * NT + t]);
@@ -321,6 +377,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     s.carry[l] = cr;
   }
   __syncthreads();
+  TRB_XS_MARK(1);
   // start / end prefix of this thread's chunk for lane l (own entries only:
   // the integer totals overwrite them lane by lane during phase B)
   auto p0 = [&](int l) { return xadd(s.carry[l], buf[l * NT + t]); };
@@ -331,7 +388,12 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
 #pragma unroll
   for (int l = 0; l < NF; ++l) classify(F[l], anyf, p0(l), p1(l), c), F[l].bin = l;
   // the scan buffer entries of this thread are read at lane setup only; the
-  // lane's integer total overwrites them at the end of its pass
+  // lane's integer total overwrites them at the end of its pass, absent
+  // lanes get 0 now (own column only: no other thread reads it)
+  for (int l = 0; l < L; ++l) {
+    const bool present = l < NF ? anyf : ((mask >> (l - NF)) & 1u) != 0;
+    if (!present) reinterpret_cast<long long*>(buf)[l * NT + t] = 0;
+  }
   unsigned rem = mask;
   bool first = true;
   for (;;) {
@@ -371,7 +433,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     if (first) {
 #pragma unroll
       for (int l = 0; l < NF; ++l) {
-        if (F[l].mode == kHead) emit(c, l, 1, F[l].P, 0, j0);
+        finish_lane(F[l], l, j0, j1, c);
         reinterpret_cast<long long*>(buf)[l * NT + t] = F[l].B;
       }
     }
@@ -379,15 +441,15 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     for (int q = 0; q < kQ; ++q) {
       if (Q[q].bin < 0) continue;
       const int l = NF + Q[q].bin;
-      if (Q[q].mode == kHead) emit(c, l, 1, Q[q].P, 0, j0);
+      finish_lane(Q[q], l, j0, j1, c);
       reinterpret_cast<long long*>(buf)[l * NT + t] = Q[q].B;
     }
     first = false;
     if (!SEL || !rem) break;
   }
-  // (lanes this chunk never touched hold 0.0 == integer 0)
 
   // ---------------- phase C: integer prefixes, ranked records, gather, replay
+  TRB_XS_MARK(2);
   __syncthreads();
   long long* ibuf = reinterpret_cast<long long*>(buf);
   cta_exscan<long long>(ibuf, L, s.cta_ip, reinterpret_cast<long long*>(wsumd));
@@ -397,19 +459,22 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
   for (int i = t; i < nrec; i += NT) {
     Rec& r = s.rec[i];
     // the record's owner thread: chunks are contiguous, owner = (j - CTA start) / C
-    const int owner = min(NT - 1, max(0, r.j / max(1, C) - rank * NT));
+    const int owner = min(NT - 1, max(0, (r.key >> 2) / max(1, C) - rank * NT));
     r.ip += ibuf[r.lane * NT + owner];
     int rk = 0;
     for (int q = 0; q < nrec; ++q) {
       const Rec& o = s.rec[q];
-      rk += (o.lane == r.lane) & (o.j < r.j);
+      rk += (o.lane == r.lane) & (o.key < r.key);
     }
     r.lrank = static_cast<uint16_t>(rk);
     atomicAdd(&s.cta_cnt[r.lane], 1);
+    if (stats) atomicAdd(&stats[r.kind == 1 ? 26 : (r.lane < NF ? 24 : 25)], 1ull);
   }
   if (t == 0) s.cta_flag = s.fail | (s.nrec > kRecCta ? 1 : 0);
   __syncthreads();
+  TRB_XS_MARK(3);
   cl.sync();  // ranked records, counts and integer totals of every CTA are visible
+  TRB_XS_MARK(4);
   for (int i = t; i < G * L; i += NT) {
     const int r = i / L, l = i - r * L;
     const Shared* rs = (r == rank) ? &s : cl.map_shared_rank(&s, r);
@@ -426,10 +491,14 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     }
     s.lane_base[L] = base;
     for (int r = 0; r < G; ++r) fl |= s.gflag[r];
-    s.fail = fl | (base > kRecAll ? 2 : 0);
+    s.fail = fl | (base > all_cap ? 2 : 0);
   }
   __syncthreads();
   const bool failed = s.fail != 0;
+  // the gathered list goes into the scan buffer: free now (the integer
+  // prefixes were folded into this CTA's records before the barrier, and no
+  // other CTA reads it)
+  Rec2* all = reinterpret_cast<Rec2*>(buf);
   if (!failed) {
     // pull every CTA's records into place: lane base + records of the lane in
     // lower CTAs + rank inside the source CTA; integer prefix + lower CTAs' totals
@@ -442,12 +511,14 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
         int before = 0;
         long long ipc = 0;
         for (int q = 0; q < r; ++q) before += s.gcnt[q][l], ipc += s.gip[q][l];
-        rc.ip += ipc;
-        s.all[s.lane_base[l] + before + rc.lrank] = rc;
+        Rec2 g;
+        g.v = rc.v, g.ip = rc.ip + ipc, g.b = rc.b, g.kind = rc.kind, g.pad = 0;
+        all[s.lane_base[l] + before + rc.lrank] = g;
       }
     }
   }
   __syncthreads();
+  TRB_XS_MARK(5);
   // replay, one thread per lane
   if (!failed) {
     for (int l = t; l < L; l += NT) {
@@ -457,11 +528,13 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
       long long ipp = 0;
       bool ok = true;
       for (int q = s.lane_base[l]; q < s.lane_base[l + 1]; ++q) {
-        const Rec rc = s.all[q];
+        const Rec2 rc = all[q];
         S = add_units(S, rc.ip - ipp, ok);
-        if (rc.kind == 1) {
+        if (rc.kind == kRecHead) {  // the exact state is +0 before a head
           ok &= S == 0.0;
           S = rc.v;
+        } else if (rc.kind == kRecTie) {
+          S = apply_tie(S, __double_as_longlong(rc.v), rc.b, ok);
         } else {
           S = xadd(S, rc.v);
         }
@@ -473,6 +546,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     }
   }
   __syncthreads();
+  TRB_XS_MARK(6);
   if (stats && t == 0 && rank == 0) {
     atomicAdd(&stats[0], 1ull);
     atomicAdd(&stats[1], static_cast<unsigned long long>(L));
@@ -482,6 +556,14 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     if (s.fail & 1) atomicAdd(&stats[18], 1ull);
     if (s.fail & 2) atomicAdd(&stats[19], 1ull);
     if (s.fail & 4) atomicAdd(&stats[22], 1ull);
+    atomicMax(&stats[29], static_cast<unsigned long long>(s.lane_base[L]));
+    unsigned long long mx = 0;
+    for (int r = 0; r < G; ++r) {
+      int n = 0;
+      for (int l = 0; l < L; ++l) n += s.gcnt[r][l];
+      mx = max(mx, static_cast<unsigned long long>(n));
+    }
+    atomicMax(&stats[28], mx);
   }
   if (s.fail) {  // exact serial fallback: one thread per lane over every element
     for (int l = t; l < L; l += NT) {
