@@ -50,6 +50,12 @@ constexpr int kQ = 3;         // selected lanes held in registers per pass
 constexpr int kMaxL = 20;     // lanes per run (NF + K): K <= 16 bins + total
 constexpr int kRecCta = 768;   // breakpoint records per CTA per run (a single-CTA group holds them all)
 constexpr long long kMant = (1LL << 52) - 1;
+// lean loop for all-safe chunks (measured slower: register pressure, warp
+// divergence against the young-sum warps; kept for experiments)
+#ifndef TRB_XS_FAST
+#define TRB_XS_FAST 0
+#endif
+constexpr bool kFastWalk = TRB_XS_FAST != 0;
 
 enum { kNone = 0, kSafe = 1, kGeneral = 2, kHead = 3 };
 enum { kRecStep = 0, kRecHead = 1, kRecTie = 2 };
@@ -85,6 +91,7 @@ struct Shared {
   long long gip[kMaxCluster][kMaxL];
   int gcnt[kMaxCluster][kMaxL];
   int gflag[kMaxCluster];
+  unsigned wmask[32];           // phase A: lanes present per warp
   int lane_base[kMaxL + 1];
   double res[kMaxL];
   int fail;
@@ -236,9 +243,14 @@ __device__ __forceinline__ void swap_lane(LaneSt& a, LaneSt& b) {
 // tot[l] receives the CTA total.  T = double (approximate prefixes) or
 // long long (integer prefixes, exact).
 template <typename T>
-__device__ void cta_exscan(T* buf, int L, T* tot, T* wsum /* [L][32] scratch */) {
+__device__ void cta_exscan(T* buf, int L, unsigned lmask, T* tot, T* wsum /* [L][32] scratch */) {
+  // only the lanes present in this CTA (lmask): every other lane's entries
+  // are 0 already and stay so, its CTA total is 0
   const int NT = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
-  for (int l = 0; l < L; ++l) {
+  for (int l = t; l < L; l += NT)
+    if (!((lmask >> l) & 1u)) tot[l] = T(0);
+  for (unsigned m = lmask; m; m &= m - 1) {
+    const int l = __ffs(m) - 1;
     const T v = buf[l * NT + t];
     T incl = v;
 #pragma unroll
@@ -252,7 +264,10 @@ __device__ void cta_exscan(T* buf, int L, T* tot, T* wsum /* [L][32] scratch */)
     if (lane == 31) wsum[l * 32 + wid] = incl;
   }
   __syncthreads();
-  for (int l = wid; l < L; l += nw) {  // warp offsets per lane (one warp per lane, lanes = warps of the CTA)
+  int idx = 0;
+  for (unsigned m = lmask; m; m &= m - 1, ++idx) {  // warp offsets: the idx-th present lane on warp idx % nw
+    if (idx % nw != wid) continue;
+    const int l = __ffs(m) - 1;
     const T v = lane < nw ? wsum[l * 32 + lane] : T(0);
     T incl = v;
 #pragma unroll
@@ -264,7 +279,10 @@ __device__ void cta_exscan(T* buf, int L, T* tot, T* wsum /* [L][32] scratch */)
     if (lane == 31) tot[l] = incl;
   }
   __syncthreads();
-  for (int l = 0; l < L; ++l) buf[l * NT + t] += wsum[l * 32 + wid];
+  for (unsigned m = lmask; m; m &= m - 1) {
+    const int l = __ffs(m) - 1;
+    buf[l * NT + t] += wsum[l * 32 + wid];
+  }
   __syncthreads();
 }
 
@@ -362,8 +380,16 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
   // own chunk totals (float: only the chunk-end prefix needs them, with the
   // widened upper margin highm_end)
   for (int l = 0; l < L; ++l) ftot[l * NT + t] = static_cast<float>(buf[l * NT + t]);
+  // lanes present in this CTA (fixed lanes: any element; selected: its bin)
+  const unsigned tmask = (mask << NF) | (anyf ? ((1u << NF) - 1u) : 0u);
+  {
+    const unsigned wm = __reduce_or_sync(0xffffffffu, tmask);
+    if ((t & 31) == 0) s.wmask[t >> 5] = wm;
+  }
   __syncthreads();
-  cta_exscan<double>(buf, L, s.cta_tot, wsumd);
+  unsigned lmask = 0;
+  for (int w = 0; w < (NT >> 5); ++w) lmask |= s.wmask[w];
+  cta_exscan<double>(buf, L, lmask, s.cta_tot, wsumd);
   cl.sync();  // every CTA's totals are visible; every CTA finished the previous run's pulls
   if (t == 0) s.nrec = 0, s.fail = 0;
   for (int i = t; i < G * L; i += NT) {
@@ -411,7 +437,93 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
     }
     if (!first && Q[0].bin < 0) break;
     auto cu = src.begin(j0);
-    for (int j = j0; j < j1; ++j) {
+    int j = j0;
+    // common case: every lane of this pass is a safe chunk (no open piece):
+    // a lean loop of integer steps; the first tie (or anything else) hands
+    // the element and the rest of the chunk to the general loop below
+    bool fast = kFastWalk;
+    if (first)
+#pragma unroll
+      for (int l = 0; l < NF; ++l) fast &= F[l].mode == kSafe || F[l].mode == kNone;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) fast &= Q[q].mode == kSafe || Q[q].bin < 0;
+    if (fast) {
+      long long BF[NF], BQ[kQ];
+#pragma unroll
+      for (int l = 0; l < NF; ++l) BF[l] = 0;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) BQ[q] = 0;
+      bool bail = false;
+      bool bh;
+      int bsel;
+      double bv[NF];
+      for (; j < j1; ++j) {
+        bool has;
+        int sel;
+        double v[NF];
+        cu.next(has, sel, v);
+        if (!has) continue;
+        bool tie = false;
+        long long rF[NF];
+        if (first) {
+#pragma unroll
+          for (int l = 0; l < NF; ++l) {
+            const double M = F[l].M;
+            const double y = xadd(M, v[l]);
+            const double d = xsub(v[l], xsub(y, M));
+            tie |= fabs(d) == __longlong_as_double(__double_as_longlong(M) - (53LL << 52));
+            rF[l] = F[l].mode == kSafe ? __double_as_longlong(y) - __double_as_longlong(M) : 0;
+          }
+        }
+        long long rQ = 0;
+        int qi = -1;
+        if (SEL) {
+#pragma unroll
+          for (int q = 0; q < kQ; ++q)
+            if (sel == Q[q].bin) qi = q;
+          if (qi >= 0) {
+            double M = Q[0].M;
+#pragma unroll
+            for (int q = 1; q < kQ; ++q)
+              if (qi == q) M = Q[q].M;
+            const double y = xadd(M, v[0]);
+            const double d = xsub(v[0], xsub(y, M));
+            tie |= fabs(d) == __longlong_as_double(__double_as_longlong(M) - (53LL << 52));
+            rQ = __double_as_longlong(y) - __double_as_longlong(M);
+          }
+        }
+        if (tie) {  // rare: this element and the rest of the chunk take the general path
+          bail = true, bh = has, bsel = sel;
+#pragma unroll
+          for (int l = 0; l < NF; ++l) bv[l] = v[l];
+          break;
+        }
+        if (first)
+#pragma unroll
+          for (int l = 0; l < NF; ++l) BF[l] += rF[l];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          if (qi == q) BQ[q] += rQ;
+      }
+      if (first)
+#pragma unroll
+        for (int l = 0; l < NF; ++l) F[l].B += BF[l];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) Q[q].B += BQ[q];
+      if (bail) {  // the interrupted element through the general steps
+        if (first) {
+#pragma unroll
+          for (int l = 0; l < NF; ++l) step(F[l], bv[l], j, l, c);
+        }
+        if (SEL)
+#pragma unroll
+          for (int q = 0; q < kQ; ++q)
+            if (bsel == Q[q].bin) step(Q[q], bv[0], j, NF + bsel, c);
+        (void)bh;
+        ++j;
+      }
+    }
+    for (; j < j1; ++j) {
       bool has;
       int sel;
       double v[NF];
@@ -452,7 +564,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
   TRB_XS_MARK(2);
   __syncthreads();
   long long* ibuf = reinterpret_cast<long long*>(buf);
-  cta_exscan<long long>(ibuf, L, s.cta_ip, reinterpret_cast<long long*>(wsumd));
+  cta_exscan<long long>(ibuf, L, lmask, s.cta_ip, reinterpret_cast<long long*>(wsumd));
   const int nrec = min(s.nrec, kRecCta);
   for (int l = t; l < L; l += NT) s.cta_cnt[l] = 0;
   __syncthreads();
@@ -527,6 +639,10 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
       double S = 0.0;
       long long ipp = 0;
       bool ok = true;
+      if (s.lane_base[l] == s.lane_base[l + 1] && ip_end == 0) {  // no element anywhere (or only zeros)
+        s.res[l] = 0.0;
+        continue;
+      }
       for (int q = s.lane_base[l]; q < s.lane_base[l + 1]; ++q) {
         const Rec2 rc = all[q];
         S = add_units(S, rc.ip - ipp, ok);
