@@ -63,6 +63,10 @@ METRIC = "frames/sec (1080p, device-timed) motion+segment+track"
 MOTION_BYTES_PER_PX = 8   # frame 1 + evict 1 + insert 1 + u16 sum 2+2 + mask 1
 PATH_BYTES_PER_PX = 12    # + int32 labels
 MORPH_BYTES_PER_PX = 2    # fused 3x3 open: mask in 1 + mask out 1 (halo re-reads are not algorithmic)
+# incremental Mode, the common push (evicted and new sample in one bin): frame 1 + ring evict/insert 2 +
+# bin sum read/write 4 + mode bin read/write 2 + its count 1 + mask 1 + 1 (the mode bin's sum when it
+# differs); a bin change adds the two counters (4 B), a rescan 1 B per bin (not counted)
+MODE_BYTES_PER_PX = 12
 CLIP_FRAMES = 300         # the recipes' clip length (n_frames is part of the recipe)
 
 CONFIGS = {
@@ -75,6 +79,8 @@ CONFIGS = {
     "C4": dict(recipe="C4", streams=1, desc="C4: one 3840x2160 clip, 50 crossing blobs (configs[3])"),
     "C5": dict(recipe="C5", streams=64, desc="C5: independent 1920x1080 C3-recipe camera streams (20 blobs, "
                                               "occlusions/merges), 64 per GPU (configs[4])"),
+    "C5MODE": dict(recipe="C5", streams=64, method=1,
+                   desc="C5 with the Mode background (MotionConfig.method = mode, 32 bins; SURVEY 8(f) row 1)"),
 }
 
 
@@ -356,7 +362,7 @@ def reference_single_thread(clip, steady, mcfg=None):
                                    "tracking": 1e3 * stage[2] / k}}
 
 
-CPU_STEADY = {"C1": 200, "C2": 150, "C2M": 150, "C3": 40, "C4": 12, "C5": 40}
+CPU_STEADY = {"C1": 200, "C2": 150, "C2M": 150, "C3": 40, "C4": 12, "C5": 40, "C5MODE": 10}
 
 
 def reference_main(args, rank, world):
@@ -391,13 +397,13 @@ def reference_main(args, rank, world):
 
 
 # -------------------------------------------------------------------- ours
-def verify_logs(clips, logs, n_frames):
+def verify_logs(clips, logs, n_frames, mcfg=None):
     """The unmodified reference over the same frames: track logs equal."""
     from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG
     from tests import _oracle as O
     fr = [O.ref_frames(c, n_frames)[0] for c in clips]
     c0 = clips[0]
-    ref = O.ref_run_streams_detail(fr, c0.width, c0.height, c0.channels, MOTION_CFG(), SEG_CFG(), TRACKER_CFG(),
+    ref = O.ref_run_streams_detail(fr, c0.width, c0.height, c0.channels, mcfg or MOTION_CFG(), SEG_CFG(), TRACKER_CFG(),
                                    len(clips), bcap=1, lcap=1 << 16)
     return [r["log"].tobytes() == lg.tobytes() for r, lg in zip(ref, logs)], [len(lg) for lg in logs]
 
@@ -422,7 +428,7 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     assert S >= 1, "every rank needs at least one stream"
     c0 = clips[0]
     px = c0.width * c0.height
-    mcfg = MOTION_CFG(morph=cfg.get("morph", 0))
+    mcfg = MOTION_CFG(morph=cfg.get("morph", 0), method=cfg.get("method", 0))
     K, Wm = args.steps, args.warmup
     fill = W_DEFAULT - 1
     e2e_steps = 0 if args.no_e2e else args.e2e_steps
@@ -542,7 +548,7 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     if args.verify_streams and rank == 0 and cfg.get("morph", 0) == 0:
         nv = min(args.verify_streams, S)
         logs = [st.log(s) for s in range(nv)]
-        ok, n_entries = verify_logs(clips[:nv], logs, t)
+        ok, n_entries = verify_logs(clips[:nv], logs, t, mcfg)
         verify = {"streams": nv, "frames": t, "log_entries": n_entries, "identical_to_reference": all(ok)}
         if not all(ok):
             print(f"[bench] VERIFY FAILED: track logs differ from the reference on streams "
@@ -587,10 +593,11 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
             return None
 
     motion_ms = stage_ms[0]
-    mb = (MOTION_BYTES_PER_PX + (2 if cfg.get("morph") else 0)) * S * px
+    mode = cfg.get("method", 0) == 1
+    mb = ((MODE_BYTES_PER_PX if mode else MOTION_BYTES_PER_PX) + (2 if cfg.get("morph") else 0)) * S * px
     ma = mb / (motion_ms / 1e3) / 1e9 if motion_ms > 0 else 0.0
-    roofline_motion = {"bound": "hbm", "kernel": "motion_mean_kernel" + (" + morph_strip_kernel" if cfg.get("morph")
-                                                                         else ""),
+    roofline_motion = {"bound": "hbm", "kernel": ("motion_mode_inc_kernel" if mode else "motion_mean_kernel") +
+                       (" + morph_strip_kernel" if cfg.get("morph") else ""),
                        "achieved": ma, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ma / peak,
                        "traffic": dram_traffic("motion_dram_bytes.json"), "bytes_per_launch": mb,
                        "ms_per_step": motion_ms}
@@ -634,14 +641,14 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if _HOST_AFFINITY:
             os.sched_setaffinity(0, _HOST_AFFINITY)  # the reference baseline gets every host core
-        if name == "C5":
+        if cfg["recipe"] == "C5":
             threads = args.cpu_threads or os.cpu_count() or 1
-            fps, done, secs = run_reference_streams(clips, threads, 2, 0)
+            fps, done, secs = run_reference_streams(clips, threads, 2, 0, mcfg)
             line["cpu_baseline"] = {
                 "value": fps, "unit": "frames/s", "cores": threads, "kind": "reference",
                 "sample": f"{S} C5 streams x 2 steady frames after the {W_DEFAULT - 1}-frame fill on {threads} host "
                           f"threads (nproc {os.cpu_count()}), one stream per thread at a time; {cpu_model()}"}
-            one = reference_single_thread(clips[0], CPU_STEADY["C3"])
+            one = reference_single_thread(clips[0], CPU_STEADY["C3"], mcfg)
             line["cpu_baseline"]["single_thread_one_stream"] = one
         else:
             line["cpu_baseline"] = reference_single_thread(clips[0], CPU_STEADY[name], mcfg if cfg.get("morph")
@@ -655,7 +662,7 @@ def ours_main(args, rank, world, local_rank):
     bind_info = bind_to_gpu_numa_node(local_rank)
     import torch
     torch.cuda.set_device(local_rank)
-    names = ["C1", "C2", "C2M", "C3", "C4", "C5"] if args.config == "all" else [args.config]
+    names = ["C1", "C2", "C2M", "C3", "C4", "C5MODE", "C5"] if args.config == "all" else [args.config]
     for i, name in enumerate(names):
         if name not in CONFIGS:
             raise SystemExit(f"unknown --config {name}")

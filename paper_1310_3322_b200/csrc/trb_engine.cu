@@ -62,6 +62,15 @@ MotionState::MotionState(const trb_motion_config& cfg, int S, int w, int h, int 
   wide_ = cfg.window > 257;  // 255*257 < 2^16
   ring_.alloc(static_cast<size_t>(px_) * cfg.window * S);
   sums_.alloc(static_cast<size_t>(px_) * S * (wide_ ? 4 : 2));
+  // Mode: incremental per-bin counts / sums / mode bin when the counts fit
+  // a byte (W <= 255); TRB_MODE_INC=0 keeps the ring re-read (A/B)
+  const char* e = getenv("TRB_MODE_INC");
+  mode_inc_ = cfg.method == TRB_BG_MODE && cfg.window <= 255 && !(e && atoi(e) == 0);
+  if (mode_inc_) {
+    cnt_.alloc(static_cast<size_t>(px_) * cfg.bins * S);
+    bsum_.alloc(sizeof(uint16_t) * static_cast<size_t>(px_) * cfg.bins * S);
+    mode_.alloc(static_cast<size_t>(px_) * S);
+  }
 }
 
 bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t* tmp, cudaStream_t st,
@@ -87,6 +96,23 @@ bool MotionState::push(const uint8_t* const* frames_dev, uint8_t* mask, uint8_t*
   a.vec_ok = (px_ % 16 == 0) && frames_aligned;
   if (cfg_.method == TRB_BG_MEAN) {
     launch_motion_mean(a, ch_, wide_, S_, st);
+    ++*launches;
+  } else if (mode_inc_) {
+    ModeIncArgs m{};
+    m.frames = frames_dev;
+    m.ring = ring_.as<uint8_t>();
+    m.ring_stride = px_ * W;
+    m.cnt = cnt_.as<uint8_t>();
+    m.bsum = bsum_.as<uint16_t>();
+    m.mode = mode_.as<uint8_t>();
+    m.mask = raw;
+    m.px = px_;
+    m.slot = a.slot;
+    m.full_before = a.full_before;
+    m.emit = a.emit;
+    m.threshold = cfg_.threshold;
+    m.bins = cfg_.bins;
+    launch_motion_mode_inc(m, ch_, S_, st);
     ++*launches;
   } else {
     launch_ring_update(a, ch_, wide_, S_, st);

@@ -87,7 +87,8 @@ class MotionState {
   int64_t px_;
   bool wide_;
   int frames_seen_ = 0;
-  DevBuf ring_, sums_;
+  bool mode_inc_ = false;
+  DevBuf ring_, sums_, cnt_, bsum_, mode_;  // cnt_/bsum_/mode_: incremental Mode state
 };
 
 class CclState {

@@ -32,6 +32,22 @@ struct ModeArgs {
   uint8_t* bg_out;  // when set: write the background image instead of the mask
 };
 
+// Incremental Mode background (window_background Mode, motion.hpp:134-143,
+// maintained per push instead of re-reading the W-sample ring): per pixel
+// and bin the sample count (u8, W <= 255) and sample sum (u16), and the
+// current mode bin.  Planes are bin-major: cnt[s][bin][px], bsum[s][bin][px].
+struct ModeIncArgs {
+  const uint8_t* const* frames;
+  uint8_t* ring;  // as MotionArgs
+  int64_t ring_stride;
+  uint8_t* cnt;
+  uint16_t* bsum;
+  uint8_t* mode;  // [n_streams][px]
+  uint8_t* mask;
+  int64_t px;
+  int slot, full_before, emit, threshold, bins;
+};
+void launch_motion_mode_inc(const ModeIncArgs& a, int channels, int n_streams, cudaStream_t st);
 void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st);
 void launch_ring_update(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st);
 void launch_motion_mode(const ModeArgs& a, int n_streams, cudaStream_t st);

@@ -160,6 +160,85 @@ __global__ void __launch_bounds__(64) motion_mode_kernel(ModeArgs a) {
   a.mask[static_cast<int64_t>(s) * a.px + p] = thr_mask(v, bg, a.threshold);
 }
 
+// Incremental Mode push (one thread per pixel).  The evicted sample leaves
+// its bin, the new one enters its bin; the mode bin m (argmax, strict >, the
+// lowest bin wins ties) changes only if the new sample's bin overtakes it
+// (compare), or if m itself lost a sample to another bin (rescan of the
+// pixel's `bins` counters — bin-major planes, so a warp's rescan loads are
+// coalesced).  Background = rounded mean of the mode bin's samples,
+// (2*sum + cnt) / (2*cnt) as window_background (motion.hpp:142-143); the mask
+// is |v - bg| > threshold (:189-190).  Per push ~12 B/px plus 1 B per bin
+// for the pixels that rescan, instead of the W-byte ring re-read.
+template <int CH>
+__device__ __forceinline__ void mode_inc_pixel(const ModeIncArgs& a, int s, int64_t p, uint32_t v) {
+  // two dependent load rounds (sample / ring / mode bin, then the touched
+  // counters), all arithmetic in registers with the aliasing between the
+  // old, new and mode bins resolved explicitly, then the stores
+  const int64_t px = a.px;
+  uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * px;
+  uint8_t* __restrict__ cnt = a.cnt + static_cast<int64_t>(s) * a.bins * px + p;
+  uint16_t* __restrict__ bsum = a.bsum + static_cast<int64_t>(s) * a.bins * px + p;
+  uint8_t* __restrict__ mode = a.mode + static_cast<int64_t>(s) * px + p;
+  const bool full = a.full_before != 0;
+  const uint32_t old = full ? ring[p] : 0u;
+  int m = *mode;
+  const int bn = static_cast<int>((v * static_cast<uint32_t>(a.bins)) >> 8);
+  const int bo = static_cast<int>((old * static_cast<uint32_t>(a.bins)) >> 8);
+  const bool moved = !full || bo != bn;  // counts change
+  int c_bn = cnt[bn * px], c_m = cnt[m * px];
+  uint32_t s_bn = bsum[bn * px], s_m = bsum[m * px];
+  int c_bo = 0;
+  uint32_t s_bo = 0;
+  if (full && bo != bn) c_bo = cnt[bo * px], s_bo = bsum[bo * px];
+  ring[p] = static_cast<uint8_t>(v);
+  if (!moved) {
+    s_bn = s_bn + v - old;
+  } else {
+    if (full) c_bo -= 1, s_bo -= old;
+    c_bn += 1, s_bn += v;
+  }
+  if (m == bn) c_m = c_bn, s_m = s_bn;
+  if (full && m == bo && bo != bn) c_m = c_bo, s_m = s_bo;
+  if (full && bo != bn && bo == m) {  // the mode bin lost a sample: rescan (new values for bo / bn)
+    int best = 0, bc = -1;
+#pragma unroll 8
+    for (int b = 0; b < a.bins; ++b) {
+      const int c = b == bo ? c_bo : (b == bn ? c_bn : cnt[b * px]);
+      if (c > bc) bc = c, best = b;
+    }
+    m = best, c_m = bc;
+    s_m = m == bo ? s_bo : (m == bn ? s_bn : bsum[m * px]);
+  } else if (moved && bn != m && (c_bn > c_m || (c_bn == c_m && bn < m))) {
+    m = bn, c_m = c_bn, s_m = s_bn;
+  }
+  cnt[bn * px] = static_cast<uint8_t>(c_bn);
+  bsum[bn * px] = static_cast<uint16_t>(s_bn);
+  if (full && bo != bn) cnt[bo * px] = static_cast<uint8_t>(c_bo), bsum[bo * px] = static_cast<uint16_t>(s_bo);
+  *mode = static_cast<uint8_t>(m);
+  if (!a.emit) return;
+  const uint32_t bg = (2 * s_m + static_cast<uint32_t>(c_m)) / (2 * static_cast<uint32_t>(c_m));
+  a.mask[static_cast<int64_t>(s) * px + p] = thr_mask(v, bg, a.threshold);
+}
+
+// kModePix pixels per thread, block-strided (4 measured slower than 1).
+constexpr int kModePix = 1;
+template <int CH>
+__global__ void __launch_bounds__(256) motion_mode_inc_kernel(ModeIncArgs a) {
+  const int s = blockIdx.y;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kModePix + threadIdx.x;
+  uint32_t v[kModePix];
+#pragma unroll
+  for (int k = 0; k < kModePix; ++k) {
+    const int64_t p = base + static_cast<int64_t>(k) * blockDim.x;
+    v[k] = p < a.px ? load1<CH>(a.frames[s], p) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kModePix; ++k) {
+    const int64_t p = base + static_cast<int64_t>(k) * blockDim.x;
+    if (p < a.px) mode_inc_pixel<CH>(a, s, p, v[k]);
+  }
+}
+
 // Ring update only (Mode path): write the new sample, keep the sums.
 template <int CH, typename SumT>
 __global__ void __launch_bounds__(256) ring_update_kernel(MotionArgs a) {
@@ -355,6 +434,13 @@ void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n
     else motion_mean_kernel<3, uint16_t><<<grid, 256, 0, st>>>(a);
   }
   TRB_LAUNCH_CHECK("motion_mean_kernel");
+}
+
+void launch_motion_mode_inc(const ModeIncArgs& a, int channels, int n_streams, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div64(a.px, 256 * kModePix)), n_streams);
+  if (channels == 1) motion_mode_inc_kernel<1><<<grid, 256, 0, st>>>(a);
+  else motion_mode_inc_kernel<3><<<grid, 256, 0, st>>>(a);
+  TRB_LAUNCH_CHECK("motion_mode_inc_kernel");
 }
 
 void launch_ring_update(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st) {

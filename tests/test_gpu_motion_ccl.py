@@ -289,3 +289,47 @@ def test_morph_device_planes_vs_oracle(gpu, w, h):
             want = np.zeros((h, w), np.uint8)
             O.orc_lib().orc_morph(masks[k].ctypes.data, w, h, op, want.ctypes.data)
             assert np.array_equal(got[k], want), (op, k)
+
+
+@pytest.mark.parametrize("window,bins,levels", [(9, 7, 4), (9, 32, 9), (20, 2, 3), (91, 32, 6), (255, 16, 5),
+                                                (256, 16, 5)])
+def test_motion_mode_incremental_long_runs(gpu, window, bins, levels):
+    """The incremental Mode state (per-bin counts / sums, mode bin; W <= 255)
+    over long runs with many evictions, ties between bins and mode changes,
+    every mask and the final background vs the oracle; W = 256 takes the
+    ring re-read path."""
+    rng = np.random.default_rng(window * 100 + bins)
+    w, h = 29, 13
+    step = 255 // (levels - 1)
+    frames = []
+    base = (rng.integers(0, levels, w * h) * step).astype(np.uint8)
+    for i in range(window + 40):
+        f = base.copy()
+        flip = rng.random(w * h) < 0.35  # moving "objects": many pixels change bin, modes flip
+        f[flip] = (rng.integers(0, levels, int(flip.sum())) * step).astype(np.uint8)
+        if i % 7 == 0:
+            base = f
+        frames.append(f)
+    assert run_motion_pair(gpu, MOTION_CFG(method=1, window=window, bins=bins, threshold=20), w, h, frames) == 41
+
+
+def test_streams_mode_background_clip_vs_oracle(gpu):
+    """Mode background through the batched handle (the incremental kernel)
+    on a moving-blob clip, RGB and gray: masks, labels and track logs equal
+    the oracle pipeline."""
+    from paper_1310_3322_b200.abi import SEG_CFG, TRACKER_CFG
+    from paper_1310_3322_b200.synth import harness_vision_clip, recipe
+    from tests.golden.make_golden import sha
+    for clip, n, mcfg in ((recipe("C1"), 130, MOTION_CFG(method=1, bins=32)),
+                          (harness_vision_clip(), 29, MOTION_CFG(method=1, window=9, bins=16))):
+        frames, _ = O.orc_frames(clip, n)
+        st = gpu.Streams(1, clip.width, clip.height, clip.channels, mcfg, SEG_CFG(), TRACKER_CFG())
+        got = []
+        for t in range(n):
+            st.step_host([frames[t]])
+            if st.has_output:
+                got.append((sha(st.mask(0)), sha(st.labels(0))))
+        st.synchronize()
+        out, log, _ = O.run_pipeline_cpu(clip, frames, mcfg, SEG_CFG(), TRACKER_CFG(), "orc")
+        assert got == [(sha(m), sha(l_)) for _, m, l_, _ in out]
+        assert st.log(0).tobytes() == log.tobytes()
