@@ -13,7 +13,9 @@
 //   mask  [px]    u8 0/1
 // Algorithmic bytes per pixel per frame (Mean, gray): frame 1 + evicted
 // sample 1 + new sample 1 + sum 2+2 + mask 1 = 8.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "trb_kernels.cuh"
 
@@ -120,6 +122,141 @@ __global__ void __launch_bounds__(256) motion_mean_kernel(MotionArgs a) {
     }
   }
   }
+}
+
+// ---- bulk-async variant (gray frames, u16 sums: the C5 workload) ----
+// Persistent CTAs stream tiles of kBulkTile pixels through shared memory
+// with the Blackwell bulk-copy engine: one thread issues cp.async.bulk loads
+// of the next tile's frame / evicted ring samples / sums (completion counted
+// on an mbarrier) while the CTA computes the current tile from shared memory,
+// then bulk-stores the new ring samples (the frame tile itself), sums and
+// mask.  Two stages; a load into a stage waits for the stores that last read
+// it (cp.async.bulk.wait_group.read).
+constexpr int kBulkThreads = 256;
+constexpr int kBulkTile = 16 * kBulkThreads;  // pixels per tile (16 per thread)
+struct BulkStage {
+  alignas(128) uint8_t frame[kBulkTile];
+  alignas(128) uint8_t ring[kBulkTile];
+  alignas(128) uint16_t sums[kBulkTile];
+  alignas(128) uint8_t mask[kBulkTile];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kBulkThreads) motion_mean_bulk_kernel(MotionArgs a, int tiles_per_stream,
+                                                                        int n_tiles) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  BulkStage* stage = reinterpret_cast<BulkStage*>(bulk_smem);
+  __shared__ __align__(8) uint64_t bar[2];
+  const int t = threadIdx.x;
+  auto tile_of = [&](int i, int& s, int64_t& p0, uint32_t& n) {
+    s = i / tiles_per_stream;
+    p0 = static_cast<int64_t>(i - s * tiles_per_stream) * kBulkTile;
+    n = static_cast<uint32_t>(min(static_cast<int64_t>(kBulkTile), a.px - p0));
+  };
+  auto issue = [&](int i, int st) {  // loads of tile i into stage st (one thread)
+    int s;
+    int64_t p0;
+    uint32_t n;
+    tile_of(i, s, p0, n);
+    const uint32_t bytes = n * (a.full_before ? 4u : 3u);
+    mbar_expect_tx(&bar[st], bytes);
+    bulk_load(stage[st].frame, a.frames[s] + p0, n, &bar[st]);
+    if (a.full_before)
+      bulk_load(stage[st].ring, a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * a.px + p0,
+                n, &bar[st]);
+    bulk_load(stage[st].sums, reinterpret_cast<const uint16_t*>(a.sums) + static_cast<int64_t>(s) * a.px + p0, 2 * n,
+              &bar[st]);
+  };
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int k = 0;  // tiles this CTA processed
+  if (t == 0 && static_cast<int>(blockIdx.x) < n_tiles) issue(blockIdx.x, 0);
+  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++k) {
+    const int st = k & 1;
+    if (t == 0) {
+      const int nx = i + gridDim.x;
+      if (nx < n_tiles) {
+        bulk_wait_read0();  // the stores of the previous tile (other stage) have read their smem
+        issue(nx, st ^ 1);
+      }
+    }
+    mbar_wait(&bar[st], (k >> 1) & 1);
+    int s;
+    int64_t p0;
+    uint32_t n;
+    tile_of(i, s, p0, n);
+    BulkStage& S = stage[st];
+    const uint32_t q0 = 16u * t;
+    if (q0 < n) {
+      const uint4 fq = *reinterpret_cast<const uint4*>(S.frame + q0);
+      const uint8_t* v = reinterpret_cast<const uint8_t*>(&fq);
+      uint4 oq = make_uint4(0, 0, 0, 0);
+      if (a.full_before) oq = *reinterpret_cast<const uint4*>(S.ring + q0);
+      const uint8_t* old = reinterpret_cast<const uint8_t*>(&oq);
+      uint4 sq[2];
+      sq[0] = *reinterpret_cast<const uint4*>(S.sums + q0);
+      sq[1] = *reinterpret_cast<const uint4*>(S.sums + q0 + 8);
+      uint16_t* sv = reinterpret_cast<uint16_t*>(sq);
+      uint4 mq;
+      uint8_t* mb = reinterpret_cast<uint8_t*>(&mq);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t sum = static_cast<uint32_t>(sv[j]) - old[j] + v[j];
+        sv[j] = static_cast<uint16_t>(sum);
+        mb[j] = thr_mask(v[j], a.div.div(2u * sum + a.W), a.threshold);
+      }
+      *reinterpret_cast<uint4*>(S.sums + q0) = sq[0];
+      *reinterpret_cast<uint4*>(S.sums + q0 + 8) = sq[1];
+      *reinterpret_cast<uint4*>(S.mask + q0) = mq;
+    }
+    fence_proxy_async();  // this thread's smem writes -> visible to the bulk (async proxy) reads
+    __syncthreads();
+    if (t == 0) {
+      bulk_store(a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * a.px + p0, S.frame, n);
+      bulk_store(reinterpret_cast<uint16_t*>(a.sums) + static_cast<int64_t>(s) * a.px + p0, S.sums, 2 * n);
+      if (a.emit) bulk_store(a.mask + static_cast<int64_t>(s) * a.px + p0, S.mask, n);
+      bulk_commit();
+    }
+  }
+  if (t == 0) bulk_wait0();  // every store has landed before the kernel ends
 }
 
 // Mode estimator (window_background Mode path, motion.hpp:134-143): per
@@ -423,7 +560,37 @@ __global__ void synth_raster_kernel(uint8_t* out, int w, int h, int ch, uint8_t 
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+static int bulk_mode() {  // TRB_MOTION_BULK=0 selects the register-streaming kernel (A/B)
+  static const int m = [] {
+    const char* e = getenv("TRB_MOTION_BULK");
+    return e ? atoi(e) : 1;
+  }();
+  return m;
+}
+
 void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n_streams, cudaStream_t st) {
+  if (channels == 1 && !wide_sums && a.vec_ok && bulk_mode()) {
+    static int grid = 0;
+    const size_t smem = 2 * sizeof(BulkStage);
+    if (!grid) {
+      TRB_CUDA(cudaFuncSetAttribute(motion_mean_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      int per_sm = 0, sms = 0, dev = 0;
+      TRB_CUDA(cudaGetDevice(&dev));
+      TRB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      TRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, motion_mean_bulk_kernel, kBulkThreads, smem));
+      // a few CTAs per SM keep enough bytes in flight (2 stages x 20 KB each)
+      // and leave the SMs' shared memory to the tracker of the previous step,
+      // which runs concurrently (step overlap)
+      const char* e = getenv("TRB_MOTION_BULK_CTAS");
+      grid = std::max(1, std::min(per_sm, e ? atoi(e) : 3)) * sms;  // A/B: 1 -> 63 %, 2 -> 87 %, 3 -> 93 % of the measured copy peak
+    }
+    const int tiles_per_stream = static_cast<int>(ceil_div64(a.px, kBulkTile));
+    const int n_tiles = tiles_per_stream * n_streams;
+    motion_mean_bulk_kernel<<<std::min(grid, n_tiles), kBulkThreads, smem, st>>>(a, tiles_per_stream, n_tiles);
+    TRB_LAUNCH_CHECK("motion_mean_bulk_kernel");
+    return;
+  }
   const int64_t chunks = ceil_div64(a.px, 16);
   dim3 grid(static_cast<unsigned>(ceil_div64(chunks, 256 * kMotionItems)), n_streams);
   if (channels == 1) {
