@@ -2017,14 +2017,21 @@ static size_t check_smem(int K, int W, int H) {
   return b;
 }
 
-// The v2 engine (trb_xsum.cuh) serves gray frames with K + 1 <= xs::kMaxL
-// when TRB_ENGINE=2 (under validation); default: the v1 engine (trb_osum.cuh).
-static bool engine_v2(int K, int CH) {
+// Engine choice.  v2 (trb_xsum.cuh: chunk-classified, no partition) has the
+// lower fixed cost per iteration and wins on small windows (frames up to
+// 640x480: C1 +25 %, C2 +7 % frames/s); v1 (trb_osum.cuh: staged element
+// streams) has the cheaper element walks and wins on 1080p / 4K windows
+// (C3 -20 %, C4 -30 %, C5 -25 % with v2).  Both are bit-exact.  v2 needs
+// gray frames and K + 1 <= xs::kMaxL.  TRB_ENGINE=1 / 2 forces one (A/B).
+static bool engine_v2(int K, int CH, int64_t frame_px) {
   static const int sel = [] {
     const char* e = getenv("TRB_ENGINE");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
-  return sel == 2 && CH == 1 && K + 1 <= xs::kMaxL;
+  const bool ok = CH == 1 && K + 1 <= xs::kMaxL;
+  if (sel == 1) return false;
+  if (sel == 2) return ok;
+  return ok && frame_px <= 640 * 480;
 }
 
 static size_t check_smem_v2(int K, int W, int H) {
@@ -2176,7 +2183,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     d_.scratch = bp_.as<unsigned char>();
     smem_set_ = smem;
   }
-  const bool v2 = engine_v2(K_, ch);
+  const bool v2 = engine_v2(K_, ch, static_cast<int64_t>(w) * h);
   if (v2 && smem2_ == 0) {
     smem2_ = check_smem_v2(K_, w, h);
     prepare_cluster_kernel(track_meanshift2_kernel, smem2_, G);
@@ -2349,7 +2356,7 @@ static void scratch_for(OneArgs& a) {
 
 static void launch_one(const OneArgs& a, size_t smem, cudaStream_t st) {
   const int G = cluster_size();
-  if (engine_v2(a.K, a.CH)) {
+  if (engine_v2(a.K, a.CH, static_cast<int64_t>(a.W) * a.H)) {
     const size_t s2 = check_smem_v2(a.K, a.W, a.H);
     thread_local DevBuf u2;
     u2.alloc(sizeof(double) * V2Smem::u2_doubles(a.W, a.H) * G, false);
