@@ -5,8 +5,9 @@
 //    reference's libm).  Restated from the machine code of
 //    libm.so.6:__hypot (non-FMA kernel, SSE2): constants 2^511 / 2^-459 /
 //    2^-54 / 2^+-600 / 2^54 were read from its rodata.  Pinned against the
-//    live libm by tests/test_exact_host.py (random + adversarial inputs) and
-//    on the device by tests/test_tracker_gpu.py.
+//    live libm by tests/test_host.py (random + adversarial inputs) and
+//    on the device by tests/test_gpu_tracker.py and, on 1e8 samples,
+//    tests/test_gpu_bench_parity.py.
 //  * Mt64: std::mt19937_64 (n=312, m=156) — quantize.hpp seeds it via
 //    Rng(seed) (rng.hpp:12-51).
 //
