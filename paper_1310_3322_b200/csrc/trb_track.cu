@@ -678,6 +678,46 @@ __device__ void meanshift_device(const uint8_t* frame, int fw, int fh, int ch, d
   }
 }
 
+// Staged bin words (written by HistSrc2 in the histogram's phase A): word i
+// of cluster thread gt at words[i * GT + gt], streamed through a ring of
+// kRing 4-byte cp.async slots per thread in shared memory (no register
+// read-ahead: a register a pending load targets stalls every instruction
+// that touches it).
+struct WordStream {
+  static constexpr int kRing = 8;
+  const uint32_t* words;
+  uint32_t* stage;  // [kRing][blockDim.x]
+  int GT, gt;
+  struct Cursor {
+    const uint32_t* p;
+    uint32_t* stage;
+    int GT, w, k;
+    uint32_t cur;
+    __device__ __forceinline__ void start(const WordStream& ws) {
+      stage = ws.stage, GT = ws.GT, w = 0, k = 0, cur = 0;
+      p = ws.words + ws.gt;
+      cp_async_wait<0>();  // nothing of an earlier walk is still landing
+#pragma unroll
+      for (int r = 0; r < kRing - 1; ++r, p += GT) {
+        cp_async4(stage + r * blockDim.x + threadIdx.x, p);
+        cp_async_commit();
+      }
+    }
+    __device__ __forceinline__ int next_bin() {
+      if (k == 0) {
+        cp_async_wait<kRing - 2>();  // word w has landed
+        cur = stage[(w & (kRing - 1)) * blockDim.x + threadIdx.x];
+        cp_async4(stage + ((w + kRing - 1) & (kRing - 1)) * blockDim.x + threadIdx.x, p);
+        cp_async_commit();
+        p += GT, ++w;
+      }
+      const int b = (cur >> (8 * k)) & 0xff;
+      k = (k + 1) & 3;
+      return b;
+    }
+  };
+};
+
 // ------------------------------------------------------ mean-shift, v2
 // The same meanshift_step / histogram_opt (tracking.hpp:79-157) on the
 // chunk-classified engine (trb_xsum.cuh): the K+1 histogram sums run straight
@@ -700,11 +740,18 @@ struct V2Smem {
   double* bct;    // [K]
   int* iscal;     // [16]
   uint8_t* lut;   // [256]
+  uint32_t* ring; // [WordStream::kRing][NT] cp.async staging of bin words
+  uint32_t* words;  // global: this group's staged bin words
   static size_t bytes(int K, int W, int H) {
     const int L = K + 1;
     (void)W, (void)H;
     return sizeof(xs::Shared) + 16 + sizeof(double) * (static_cast<size_t>(L) * NT + L * 32 + 7 * K) +
-           sizeof(float) * L * NT + sizeof(int) * 16 + 256 + 16 * 16;
+           sizeof(float) * L * NT + sizeof(int) * 16 + 256 + sizeof(uint32_t) * WordStream::kRing * NT + 17 * 16;
+  }
+  // bin-word scratch per cluster: the window (<= frame) in 4-element words,
+  // plus read-ahead slack of the rings; split mode: 1/G of it per CTA
+  static __host__ __device__ size_t words_per_cluster(int64_t frame_px, int G) {
+    return static_cast<size_t>(frame_px / 4 + 4 * G * NT) + static_cast<size_t>(WordStream::kRing + 2) * G * NT;
   }
   static __host__ __device__ size_t u2_doubles(int W, int H) { return static_cast<size_t>(W) + H + 1; }  // per CTA
   __device__ void carve(void* base, int K, int W, int H, double* u2_base) {
@@ -730,6 +777,8 @@ struct V2Smem {
     bct = reinterpret_cast<double*>(take(sizeof(double) * K));
     iscal = reinterpret_cast<int*>(take(sizeof(int) * 16));
     lut = reinterpret_cast<uint8_t*>(take(256));
+    ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * WordStream::kRing * NT));
+    words = nullptr;
   }
 };
 
@@ -757,9 +806,21 @@ struct HistSrc2 {
       const double w = s->weight(xx, uy);
       has = w > 0.0;  // if (wgt <= 0.0) continue;
       v[0] = w;
+      if (s->words) {  // stage the bin for the later walks (4-element words, chunk-interleaved)
+        wacc |= static_cast<uint32_t>(sel) << (8 * k);
+        if (++k == 4) *wp = wacc, wp += s->GT, wacc = 0, k = 0;
+      }
       if (++xx == s->ww) xx = 0, ++yy, row += s->fw, uy = s->uy2[yy];
     }
+    __device__ __forceinline__ void finish() {
+      if (s->words && k) *wp = wacc;
+    }
+    uint32_t* wp;
+    uint32_t wacc;
+    int k;
   };
+  uint32_t* words;  // when set: bin words of the thread's chunk are staged here
+  int GT, gt;
   __device__ Cursor begin(int j0) const {
     Cursor c;
     c.s = this;
@@ -767,6 +828,8 @@ struct HistSrc2 {
     c.xx = j0 - c.yy * ww;
     c.row = frame + static_cast<int64_t>(y0 + c.yy) * fw + x0;
     c.uy = uy2[c.yy];
+    c.wp = words ? words + gt : nullptr;
+    c.wacc = 0, c.k = 0;
     return c;
   }
   __device__ void get(int j, bool& has, int& sel, double* v) const {
@@ -800,6 +863,7 @@ struct CentSrc2 {
       xd = xadd(xd, 1.0);
       if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0), row += s->fw;
     }
+    __device__ __forceinline__ void finish() {}
   };
   __device__ Cursor begin(int j0) const {
     Cursor c;
@@ -819,6 +883,79 @@ struct CentSrc2 {
     v[0] = w;
     v[1] = xmul(w, static_cast<double>(x0 + xx));
     v[2] = xmul(w, static_cast<double>(y0 + yy));
+  }
+};
+
+// histogram phase B from the staged bins (same elements as HistSrc2)
+struct HistSrcW {
+  WordStream ws;
+  int ww;
+  const double* ux2;
+  const double* uy2;
+  int epan;
+  struct Cursor {
+    const HistSrcW* s;
+    WordStream::Cursor wc;
+    int xx, yy;
+    double uy;
+    __device__ __forceinline__ void next(bool& has, int& sel, double* v) {
+      sel = wc.next_bin();
+      double w = 1.0;
+      if (s->epan) {
+        const double t = xsub(1.0, xadd(s->ux2[xx], uy));
+        w = (0.0 < t) ? t : 0.0;
+      }
+      has = w > 0.0;
+      v[0] = w;
+      if (++xx == s->ww) xx = 0, ++yy, uy = s->uy2[yy];
+    }
+    __device__ __forceinline__ void finish() {}
+  };
+  __device__ Cursor begin(int j0) const {
+    Cursor c;
+    c.s = this;
+    c.yy = j0 / ww;
+    c.xx = j0 - c.yy * ww;
+    c.uy = uy2[c.yy];
+    c.wc.start(ws);
+    return c;
+  }
+};
+
+// centroid elements from the staged bins (same elements as CentSrc2, which
+// serves the serial fallback's random access)
+struct CentSrcW {
+  WordStream ws;
+  int x0, y0, ww;
+  const double* wsq;
+  CentSrc2 direct;
+  __device__ void get(int j, bool& has, int& sel, double* v) const { direct.get(j, has, sel, v); }
+  struct Cursor {
+    const CentSrcW* s;
+    WordStream::Cursor wc;
+    int xx;
+    double xd, yd;
+    __device__ __forceinline__ void next(bool& has, int& sel, double* v) {
+      const double w = s->wsq[wc.next_bin()];
+      sel = 0;
+      has = w >= 0.0;
+      v[0] = w;
+      v[1] = xmul(w, xd);
+      v[2] = xmul(w, yd);
+      xd = xadd(xd, 1.0);
+      if (++xx == s->ww) xx = 0, xd = static_cast<double>(s->x0), yd = xadd(yd, 1.0);
+    }
+    __device__ __forceinline__ void finish() {}
+  };
+  __device__ Cursor begin(int j0) const {
+    Cursor c;
+    c.s = this;
+    const int yy = j0 / ww;
+    c.xx = j0 - yy * ww;
+    c.xd = static_cast<double>(x0 + c.xx);
+    c.yd = static_cast<double>(y0 + yy);
+    c.wc.start(ws);
+    return c;
   }
 };
 
@@ -842,8 +979,10 @@ __device__ bool window_histogram2(const uint8_t* frame, int fw, int fh, double c
   fill_u2_v2(sm, r, cx, cy, w, h);
   __syncthreads();
   const int ww = r.x1 - r.x0, N = ww * (r.y1 - r.y0);
-  HistSrc2 hs{frame, fw, r.x0, r.y0, ww, sm.ux2, sm.uy2, sm.lut, epan};
-  xs::xsum_run<1, true>(sm.grp, N, K, hs, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap, g_trb_stats);
+  const int GT = sm.grp.size_ * static_cast<int>(blockDim.x), gt = sm.grp.rank_ * static_cast<int>(blockDim.x) + threadIdx.x;
+  HistSrc2 hs{frame, fw, r.x0, r.y0, ww, sm.ux2, sm.uy2, sm.lut, epan, sm.words, GT, gt};
+  HistSrcW hw{WordStream{sm.words, sm.ring, GT, gt}, ww, sm.ux2, sm.uy2, epan};
+  xs::xsum_run<1, true>(sm.grp, N, K, hs, hw, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap, g_trb_stats);
   const double total = sm.xs->res[0];
   if (!(total > 0.0)) {
     __syncthreads();
@@ -900,7 +1039,11 @@ __device__ void meanshift_device2(const uint8_t* frame, int fw, int fh, double& 
     const Win r = clip_window(fw, fh, cx, cy, w, h);
     const int ww = r.x1 - r.x0;
     CentSrc2 cs{frame, fw, r.x0, r.y0, ww, sm.lut, sm.wsq};
-    xs::xsum_run<3, false>(sm.grp, ww * (r.y1 - r.y0), 0, cs, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap,
+    const int GT = sm.grp.size_ * static_cast<int>(blockDim.x);
+    const int gt = sm.grp.rank_ * static_cast<int>(blockDim.x) + threadIdx.x;
+    CentSrcW cw{WordStream{sm.words, sm.ring, GT, gt}, r.x0, r.y0, ww, sm.wsq, cs};
+    // the window is the histogram's (same cx, cy): its staged bins serve both centroid walks
+    xs::xsum_run<3, false>(sm.grp, ww * (r.y1 - r.y0), 0, cw, cw, *sm.xs, sm.buf, sm.ftot, sm.wsum, sm.all_cap,
                            g_trb_stats);
     const double sw = sm.xs->res[0], sx = sm.xs->res[1], sy = sm.xs->res[2];
     __syncthreads();
@@ -1514,6 +1657,10 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(
   V2Smem sm;
   sm.carve(smem_raw, d.K, d.W, d.H, d.u2);
   const int rank = static_cast<int>(cl.block_rank());
+  const int G = static_cast<int>(cl.num_blocks());
+  const size_t wpc = V2Smem::words_per_cluster(static_cast<int64_t>(d.W) * d.H, G);
+  uint32_t* const cl_words = d.words2 + static_cast<size_t>(blockIdx.x / G) * wpc;
+  sm.words = cl_words;
   const int n_work = *d.work_n;
   bool split = false;
   for (;;) {
@@ -1543,9 +1690,10 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(
       to_split = split_class(d, g);
     }
     meanshift_item2(d, q, sm, (split || rank == 0) && threadIdx.x == 0);
-    if (to_split) {
+    if (to_split) {  // this CTA alone from now on, with its 1/G of the cluster's bin words
       split = true;
       sm.grp = Grp::single();
+      sm.words = cl_words + static_cast<size_t>(rank) * (wpc / G);
     }
   }
 }
@@ -1784,6 +1932,7 @@ struct OneArgs {
   size_t scratch_stride;
   int64_t maxN;
   double* u2;  // v2: per-CTA ux2/uy2 slices
+  uint32_t* words;  // v2: staged bin words
 };
 
 // One cluster: meanshift_step or histogram_opt on a single explicit track,
@@ -1793,6 +1942,7 @@ __global__ void __launch_bounds__(NT) track_one2_kernel(OneArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   V2Smem sm;
   sm.carve(smem_raw, a.K, a.W, a.H, a.u2);
+  sm.words = a.words;
   for (int k = threadIdx.x; k < 3 * a.K; k += NT) sm.cen[k] = a.centers[k];
   if (a.target)
     for (int k = threadIdx.x; k < a.K; k += NT) sm.q[k] = a.target[k];
@@ -2192,6 +2342,8 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     if (const char* eg = getenv("TRB_TRACK_CLUSTERS")) grid2_ = std::max(1, std::min(grid2_, atoi(eg)));
     u2_.alloc(sizeof(double) * V2Smem::u2_doubles(w, h) * static_cast<size_t>(grid2_) * G, false);
     d_.u2 = u2_.as<double>();
+    words2_.alloc(sizeof(uint32_t) * V2Smem::words_per_cluster(static_cast<int64_t>(w) * h, G) * grid2_, false);
+    d_.words2 = words2_.as<uint32_t>();
     if (getenv("TRB_VERBOSE"))
       fprintf(stderr, "[trb] tracker v2: %d clusters of %d CTAs, %zu B dynamic smem per CTA\n", grid2_, G, smem2_);
   }
@@ -2358,10 +2510,12 @@ static void launch_one(const OneArgs& a, size_t smem, cudaStream_t st) {
   const int G = cluster_size();
   if (engine_v2(a.K, a.CH, static_cast<int64_t>(a.W) * a.H)) {
     const size_t s2 = check_smem_v2(a.K, a.W, a.H);
-    thread_local DevBuf u2;
+    thread_local DevBuf u2, words;
     u2.alloc(sizeof(double) * V2Smem::u2_doubles(a.W, a.H) * G, false);
+    words.alloc(sizeof(uint32_t) * V2Smem::words_per_cluster(static_cast<int64_t>(a.W) * a.H, G), false);
     OneArgs b = a;
     b.u2 = u2.as<double>();
+    b.words = words.as<uint32_t>();
     prepare_cluster_kernel(track_one2_kernel, s2, G);
     launch_cluster(track_one2_kernel, 1, G, s2, st, b);
     return;

@@ -73,6 +73,7 @@ struct TrackDev {
   size_t scratch_stride;
   int64_t maxN;
   double* u2;  // v2 engine: per-CTA ux2 / uy2 (W + H + 1 doubles each)
+  uint32_t* words2;  // v2 engine: per-cluster staged bin words
 };
 
 class TrackerState {
@@ -110,7 +111,7 @@ class TrackerState {
   trb_tracker_config cfg_;
   int S_, T_, K_;
   int64_t log_cap_;
-  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_, u2_;
+  DevBuf i32_, f64_, lut_, log_, nlog_, matched_, bp_, work_, u2_, words2_;
   TrackDev d_{};
   int64_t matched_cap_ = 0;
   int grid_ = 0, grid2_ = 0;

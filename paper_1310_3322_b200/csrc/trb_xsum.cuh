@@ -312,8 +312,11 @@ __device__ __forceinline__ double apply_tie(double S, long long A, long long B, 
 }
 
 // One run.  Src supplies the elements of thread chunk [j0, j1):
-//   typename Src::Cursor cur = src.begin(j0);  cur.next(has, sel, v)  (v[NF])
+//   typename Src::Cursor cur = src.begin(j0);  cur.next(has, sel, v)  (v[NF]);
+//   cur.finish() after the last element of phase A
 //   src.get(j, has, sel, v)  (random access, serial fallback only)
+// srcA feeds phase A (and the fallback), srcB phase B (e.g. srcA computes
+// each element's bin and stages it, srcB reads the staged words).
 // Lanes: 0..NF-1 fixed (every element with `has` feeds lane l with v[l]);
 // if SEL, NF + b for bins b < K (an element feeds lane NF + sel with v[0]).
 // buf: dynamic shared scratch of L * blockDim.x 8-byte words, ftot: L *
@@ -321,14 +324,14 @@ __device__ __forceinline__ double apply_tie(double S, long long A, long long B, 
 // Results: s.res[l], identical in every CTA of the group, on return.
 // all_cap: Rec2 records that fit in buf (its full allocation, which may
 // exceed this run's L * blockDim.x words).
-template <int NF, bool SEL, class Src>
-__device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s, double* buf, float* ftot,
-                         double* wsumd, int all_cap, unsigned long long* stats) {
+template <int NF, bool SEL, class SrcA, class SrcB>
+__device__ void xsum_run(const Grp& cl, int N, int K, const SrcA& src, const SrcB& srcB, Shared& s, double* buf,
+                         float* ftot, double* wsumd, int all_cap, unsigned long long* stats) {
   const int NT = blockDim.x, t = threadIdx.x;
   const int rank = static_cast<int>(cl.block_rank()), G = static_cast<int>(cl.num_blocks());
   const int GT = G * NT, gt = rank * NT + t;
   const int L = NF + (SEL ? K : 0);
-  const int C = (N + GT - 1) / GT;
+  const int C = ((N + GT - 1) / GT + 3) & ~3;  // a multiple of 4: whole staged 4-element words per thread
   const int j0 = min(N, gt * C), j1 = min(N, j0 + C);
   // relative error of every approximate prefix vs the exact sequential sum:
   // the sequential sum's own drift (N roundings) + the scan's (chunk, warp,
@@ -372,6 +375,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
         acc = xadd(acc, v[0]);
       }
     }
+    cu.finish();
     if (SEL && cur >= 0) buf[(NF + cur) * NT + t] += acc;
 #pragma unroll
     for (int l = 0; l < NF; ++l) buf[l * NT + t] = aF[l];
@@ -436,7 +440,7 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const Src& src, Shared& s,
       }
     }
     if (!first && Q[0].bin < 0) break;
-    auto cu = src.begin(j0);
+    auto cu = srcB.begin(j0);
     int j = j0;
     // common case: every lane of this pass is a safe chunk (no open piece):
     // a lean loop of integer steps; the first tie (or anything else) hands

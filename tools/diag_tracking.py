@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from paper_1310_3322_b200.synth import device_frames  # noqa: E402
 import paper_1310_3322_b200 as trb  # noqa: E402
 from paper_1310_3322_b200 import api  # noqa: E402
 from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
@@ -34,7 +34,7 @@ S = args.streams
 stream = torch.cuda.Stream()
 clips = [recipe("C5", s) for s in range(S)]
 n = 90 + 3 + args.start + args.steps
-frames = bench.make_frames(trb, clips, n, stream)
+frames = device_frames(clips, n, stream.cuda_stream)
 st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
 ptrs = [[frames[s, t].data_ptr() for s in range(S)] for t in range(n)]
 t = 0

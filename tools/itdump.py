@@ -14,7 +14,7 @@ import torch  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402
+from paper_1310_3322_b200.synth import device_frames  # noqa: E402
 import paper_1310_3322_b200 as trb  # noqa: E402
 from paper_1310_3322_b200 import api  # noqa: E402
 from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
@@ -26,7 +26,7 @@ out = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/itdump.npz"
 stream = torch.cuda.Stream()
 clips = [recipe("C5", s) for s in range(S)]
 n = 93 + steps
-frames = bench.make_frames(trb, clips, n, stream)
+frames = device_frames(clips, n, stream.cuda_stream)
 st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
 for t in range(93):
     st.step_device([frames[s, t].data_ptr() for s in range(S)], stream.cuda_stream)

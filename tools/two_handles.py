@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from paper_1310_3322_b200.synth import device_frames  # noqa: E402
 import paper_1310_3322_b200 as trb  # noqa: E402
 from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E402
 from paper_1310_3322_b200.synth import recipe  # noqa: E402
