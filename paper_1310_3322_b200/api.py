@@ -564,6 +564,12 @@ class Streams:
             return
         _check(lib().trb_streams_step_host_async(self._h, ptrs, self._result(result), C.c_void_p(cuda_stream)))
 
+    def num_tracks(self, s: int) -> int:
+        """Live tracks of stream s (Tracker::tracks().size())."""
+        n = C.c_int(0)
+        _check(lib().trb_streams_num_tracks(self._h, s, C.byref(n)))
+        return n.value
+
     def drain_log(self, s: int) -> np.ndarray:
         """The track-log entries of stream s not drained yet (oldest first);
         they are released from the device ring."""

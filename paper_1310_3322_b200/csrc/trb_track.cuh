@@ -115,6 +115,8 @@ class TrackerState {
   TrackDev d_{};
   int64_t matched_cap_ = 0;
   int grid_ = 0, grid2_ = 0;
+  int grid_big_[2] = {0, 0};  // clusters of 16 and of 12 CTAs (few-track frames)
+  PinnedBuf nactive_;         // the previous frame's active-track count (mirror)
   size_t smem_set_ = 0, smem2_ = 0;
 };
 
