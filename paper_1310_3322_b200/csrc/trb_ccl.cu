@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256) ccl_occupancy_kernel(CclArgs a, int vec_o
 }
 
 __global__ void __launch_bounds__(256) ccl_local_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   __shared__ int lab[kTilePx];
   __shared__ int cid[kTilePx];  // compact component id of each local root
   __shared__ uint32_t rowm[kTileH], starts[kTileH];
@@ -352,6 +353,7 @@ __device__ __forceinline__ void ccl_merge_one(const CclArgs& a, int s, int tx, i
 // Only listed (foreground) tiles can own a seam union: the pixel below /
 // right of the seam must be foreground.  Grid-stride over list x 64.
 __global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   const int64_t total = static_cast<int64_t>(*a.tile_count) * 64;
   for (int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gid < total;
        gid += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(256) ccl_merge_kernel(CclArgs a) {
 
 // ---------------------------------------------------------------- resolve
 __global__ void __launch_bounds__(256) ccl_resolve_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   const int s = blockIdx.y;
   const int n = a.nslots[s];
   SlotTable t = slot_base(a, s);
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(256) ccl_resolve_kernel(CclArgs a) {
 
 // ------------------------------------------------------------------- mark
 __global__ void __launch_bounds__(256) ccl_mark_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   const int s = blockIdx.y;
   const int n = a.nslots[s];
   SlotTable t = slot_base(a, s);
@@ -401,6 +405,7 @@ __global__ void __launch_bounds__(256) ccl_mark_kernel(CclArgs a) {
 // Exclusive scan of the per-row survivor counts; one 1024-thread CTA per
 // stream, rows processed in chunks of 1024.
 __global__ void __launch_bounds__(1024) ccl_scan_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   __shared__ int warp_sums[32];
   __shared__ int carry;
   const int s = blockIdx.x;
@@ -440,6 +445,7 @@ __global__ void __launch_bounds__(1024) ccl_scan_kernel(CclArgs a) {
 
 // ----------------------------------------------------------------- assign
 __global__ void __launch_bounds__(256) ccl_assign_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   const int s = blockIdx.y;
   const int n = a.nslots[s];
   SlotTable t = slot_base(a, s);
@@ -484,6 +490,7 @@ __global__ void __launch_bounds__(256) ccl_assign_kernel(CclArgs a) {
 // none now are cleared; untouched background tiles (most of a frame) are
 // skipped — the plane stays zero there from the allocation on.
 __global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a) {
+  pdl_wait();  // launched with launch_pdl: the previous kernel's results first
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -521,22 +528,16 @@ int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   TRB_LAUNCH_CHECK("ccl_occupancy_kernel");
   // persistent CTAs over the foreground-tile list (count known on the device)
   const unsigned list_ctas = static_cast<unsigned>(std::min<int64_t>(n_tiles * S, 148 * 8));
-  ccl_local_kernel<<<list_ctas, 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_local_kernel");
-  ccl_merge_kernel<<<list_ctas, 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_merge_kernel");
+  // the chain below overlaps each launch with its predecessor's drain (PDL)
+  launch_pdl(ccl_local_kernel, dim3(list_ctas), dim3(256), 0, st, a);
+  launch_pdl(ccl_merge_kernel, dim3(list_ctas), dim3(256), 0, st, a);
   // slot kernels: enough CTAs to cover a typical frame, grid-stride beyond
   const unsigned slot_blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div64(a.slot_cap, 256), 64));
-  ccl_resolve_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_resolve_kernel");
-  ccl_mark_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_mark_kernel");
-  ccl_scan_kernel<<<S, 1024, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_scan_kernel");
-  ccl_assign_kernel<<<dim3(slot_blocks, S), 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_assign_kernel");
-  ccl_final_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 32, 256)), S), 256, 0, st>>>(a);
-  TRB_LAUNCH_CHECK("ccl_final_kernel");
+  launch_pdl(ccl_resolve_kernel, dim3(slot_blocks, S), dim3(256), 0, st, a);
+  launch_pdl(ccl_mark_kernel, dim3(slot_blocks, S), dim3(256), 0, st, a);
+  launch_pdl(ccl_scan_kernel, dim3(S), dim3(1024), 0, st, a);
+  launch_pdl(ccl_assign_kernel, dim3(slot_blocks, S), dim3(256), 0, st, a);
+  launch_pdl(ccl_final_kernel, dim3(static_cast<unsigned>(ceil_div64(n_tiles * 32, 256)), S), dim3(256), 0, st, a);
   return 8;
 }
 

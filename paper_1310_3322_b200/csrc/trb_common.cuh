@@ -28,6 +28,28 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define TRB_CUDA(x) ::trb::cuda_check((x), #x)
 #define TRB_LAUNCH_CHECK(name) ::trb::cuda_check(cudaGetLastError(), name)
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while the previous kernel on the stream drains; it must call pdl_wait()
+// before touching memory that kernel reads or writes (the wait returns once
+// the previous grid has completed and its writes are visible).  Saves the
+// launch gap between the short kernels of a frame (CCL chain, tracker chain).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, args...), "cudaLaunchKernelEx (programmatic dependent launch)");
+}
+
 // Tile geometry of the connected-component kernels: a CTA owns a 32x32
 // pixel tile; a tile holds at most 512 components (4-connected
 // checkerboard), which bounds the per-stream slot table at px/2.

@@ -1563,6 +1563,7 @@ __device__ void meanshift_item(const TrackDev& d, int q, TrackSmem& sm, const Tr
 #define TRB_MS_MINBLOCKS 2
 #endif
 __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift_kernel(TrackDev d) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results first
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   TrackSmem sm;
@@ -1652,6 +1653,7 @@ __device__ void meanshift_item2(const TrackDev& d, int q, V2Smem& sm, bool lead)
 }
 
 __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(TrackDev d) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results first
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   V2Smem sm;
@@ -1703,6 +1705,7 @@ __global__ void __launch_bounds__(NT, TRB_MS_MINBLOCKS) track_meanshift2_kernel(
 // geometry and success conditions (:208-234), lost counting and retirement
 // (:197-201) and the log (:203-204).
 __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results first
   __shared__ int sh_n, sh_ncur, sh_next_id, sh_ok;
   __shared__ double sh_min[2][NT / 32];
   const int s = blockIdx.x;
@@ -1865,6 +1868,7 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
 // centres broadcast through DSMEM, then the cluster-parallel target
 // histogram (:230-232) and the gray->bin table.
 __global__ void __launch_bounds__(NT) track_spawn_kernel(TrackDev d) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results first
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Mt64 rng;
 
@@ -2229,22 +2233,32 @@ static int max_clusters(Kern kern, size_t smem, int G) {
 }
 
 template <typename... KArgs, typename... Args>
-static void launch_cluster(void (*kern)(KArgs...), int n_clusters, int G, size_t smem, cudaStream_t st,
-                           Args... args) {
+static void launch_cluster_ex(bool pdl, void (*kern)(KArgs...), int n_clusters, int G, size_t smem, cudaStream_t st,
+                              Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_clusters * G);
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = G;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   TRB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
+
+// pdl: programmatic dependent launch (the kernel must pdl_wait() first)
+template <typename... KArgs, typename... Args>
+static void launch_cluster(void (*kern)(KArgs...), int n_clusters, int G, size_t smem, cudaStream_t st,
+                           Args... args) {
+  launch_cluster_ex(false, kern, n_clusters, G, smem, st, args...);
+}
+
 
 TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, int64_t log_cap)
     : cfg_(cfg), S_(S), T_(track_cap), K_(cfg.k_clusters), log_cap_(log_cap) {
@@ -2379,15 +2393,18 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   dm.G = Gm;
   track_schedule_kernel<<<1, 1024, 0, st>>>(dm);
   TRB_LAUNCH_CHECK("track_schedule_kernel");
-  if (nactive_.p) TRB_CUDA(cudaMemcpyAsync(nactive_.p, d_.work_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  const bool pdl = !after_meanshift;  // (profiling records an event between the kernels)
   if (v2)
-    launch_cluster(track_meanshift2_kernel, grid2_, G, smem2_, st, d_);
+    launch_cluster_ex(pdl, track_meanshift2_kernel, grid2_, G, smem2_, st, d_);
   else
-    launch_cluster(track_meanshift_kernel, gridm, Gm, smem, st, dm);
+    launch_cluster_ex(pdl, track_meanshift_kernel, gridm, Gm, smem, st, dm);
   if (after_meanshift) TRB_CUDA(cudaEventRecord(after_meanshift, st));
-  track_gate_kernel<<<S_, NT, 0, st>>>(d_);
+  if (pdl) launch_pdl(track_gate_kernel, dim3(S_), dim3(NT), 0, st, d_);
+  else track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
-  launch_cluster(track_spawn_kernel, grid_, G, smem, st, d_);
+  launch_cluster_ex(pdl, track_spawn_kernel, grid_, G, smem, st, d_);
+  // (after the chain, so the copy does not break the programmatic launches)
+  if (nactive_.p) TRB_CUDA(cudaMemcpyAsync(nactive_.p, d_.work_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   *launches += 4;
 }
 
