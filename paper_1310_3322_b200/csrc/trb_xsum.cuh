@@ -92,6 +92,9 @@ struct Shared {
   int gcnt[kMaxCluster][kMaxL];
   int gflag[kMaxCluster];
   unsigned wmask[32];           // phase A: lanes present per warp
+  int gbase[kMaxCluster][kMaxL];   // phase C pull: destination base per (source CTA, lane)
+  long long gipc[kMaxCluster][kMaxL];  // integer prefix of the lower CTAs per (source CTA, lane)
+  int goff[kMaxCluster + 1];       // record offsets per source CTA
   int lane_base[kMaxL + 1];
   double res[kMaxL];
   int fail;
@@ -618,19 +621,35 @@ __device__ void xsum_run(const Grp& cl, int N, int K, const SrcA& src, const Src
   if (!failed) {
     // pull every CTA's records into place: lane base + records of the lane in
     // lower CTAs + rank inside the source CTA; integer prefix + lower CTAs' totals
-    for (int r = 0; r < G; ++r) {
-      const Shared* rs = (r == rank) ? &s : cl.map_shared_rank(&s, r);
-      const int n = min(rs->nrec, kRecCta);
-      for (int i = t; i < n; i += NT) {
-        Rec rc = rs->rec[i];
-        const int l = rc.lane;
-        int before = 0;
-        long long ipc = 0;
-        for (int q = 0; q < r; ++q) before += s.gcnt[q][l], ipc += s.gip[q][l];
-        Rec2 g;
-        g.v = rc.v, g.ip = rc.ip + ipc, g.b = rc.b, g.kind = rc.kind, g.pad = 0;
-        all[s.lane_base[l] + before + rc.lrank] = g;
+    // (one flattened pass over every CTA's records: the remote loads of all
+    // CTAs are in flight together)
+    for (int i = t; i < G * L; i += NT) {  // per (source CTA, lane): destination base, carried prefix
+      const int r = i / L, l = i - r * L;
+      int before = 0;
+      long long ipc = 0;
+      for (int q = 0; q < r; ++q) before += s.gcnt[q][l], ipc += s.gip[q][l];
+      s.gbase[r][l] = s.lane_base[l] + before;
+      s.gipc[r][l] = ipc;
+    }
+    if (t == 0) {
+      int o = 0;
+      for (int r = 0; r < G; ++r) {
+        s.goff[r] = o;
+        for (int l = 0; l < L; ++l) o += s.gcnt[r][l];
       }
+      s.goff[G] = o;
+    }
+    __syncthreads();
+    const int total = s.goff[G];
+    for (int k = t; k < total; k += NT) {
+      int r = 0;
+      while (k >= s.goff[r + 1]) ++r;
+      const Shared* rs = (r == rank) ? &s : cl.map_shared_rank(&s, r);
+      const Rec rc = rs->rec[k - s.goff[r]];
+      const int l = rc.lane;
+      Rec2 g;
+      g.v = rc.v, g.ip = rc.ip + s.gipc[r][l], g.b = rc.b, g.kind = rc.kind, g.pad = 0;
+      all[s.gbase[r][l] + rc.lrank] = g;
     }
   }
   __syncthreads();
