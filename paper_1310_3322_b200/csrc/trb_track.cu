@@ -1469,9 +1469,17 @@ __device__ __forceinline__ bool split_class(const TrackDev& d, int64_t g) {
 // Work list of the active tracks, largest window first (longest processing
 // time first keeps the persistent clusters balanced).  One CTA.
 __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
-  __shared__ int cnt[256], off[256];
+  // buckets: [split class][stream group][cost]: all cluster-class tracks come
+  // before every split-class one (a cluster that turns to split mode never
+  // turns back); inside a class, stream group g's tracks before group g+1's
+  // (fewer frames are being read at a time: better L2 locality), costliest
+  // first inside a group
+  constexpr int kMaxGroups = 4;
+  __shared__ int cnt[256 * kMaxGroups], off[256 * kMaxGroups];
+  const int NG = max(1, min(kMaxGroups, d.stream_groups));
+  const int NB = 256 * NG;
   const int t = threadIdx.x;
-  if (t < 256) cnt[t] = 0;
+  for (int i = t; i < NB; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   auto bucket = [&](int item) -> int {
     const int s = item / d.T, i = item - s * d.T;
@@ -1480,12 +1488,12 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     if (d.status[g] != TRB_TRACK_ACTIVE) return -1;
     // estimated cost: previous frame's iteration count x (fixed overhead
     // ~30k px + window area); 4 buckets per octave, small index = costly.
-    // Split-class tracks go after every cluster-class one.
     const unsigned cost =
         static_cast<unsigned>(max(d.iter_floor, d.iters[g])) * static_cast<unsigned>(d.order_fix + max(1, d.w[g] * d.h[g]));
     const int lz = __clz(cost);
     const int sub = lz <= 29 ? static_cast<int>((cost >> (29 - lz)) & 3u) : 0;
-    return (split_class(d, g) ? 128 : 0) + 4 * lz + (3 - sub);
+    const int grp = static_cast<int>(static_cast<int64_t>(s) * NG / d.S);
+    return (split_class(d, g) ? 128 * NG : 0) + 128 * grp + 4 * lz + (3 - sub);
   };
   // only the listed tracks: one warp per stream, lanes over its list
   const int lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
@@ -1497,10 +1505,10 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     }
   }
   __syncthreads();
-  if (wid == 0) {  // exclusive scan of the 256 bucket counts (8 per lane)
-    int v[8], sum = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = cnt[lane * 8 + k], sum += v[k];
+  if (wid == 0) {  // exclusive scan of the bucket counts (NB / 32 per lane)
+    const int per = NB / 32;
+    int sum = 0;
+    for (int k = 0; k < per; ++k) sum += cnt[lane * per + k];
     int incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1508,8 +1516,10 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
       if (lane >= o) incl += y;
     }
     int o = incl - sum;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) off[lane * 8 + k] = o, o += v[k];
+    for (int k = 0; k < per; ++k) {
+      const int v = cnt[lane * per + k];
+      off[lane * per + k] = o, o += v;
+    }
     if (lane == 31) {
       *d.work_n = incl;
       *d.work_head = 0;
@@ -2336,6 +2346,8 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     d_.split_fix = envf("TRB_SPLIT_FIX", 30.0);
     d_.split_perpx = envf("TRB_SPLIT_PERKPX", 14.1) * 1e-3;
     d_.order_fix = static_cast<int>(envf("TRB_ORDER_FIX", 5000.0));  // A/B (4 x 4 runs): 5k px ahead of 10k, 20k, 30k
+    const char* eg2 = getenv("TRB_STREAM_GROUPS");
+    d_.stream_groups = eg2 ? atoi(eg2) : 1;
     const char* ef = getenv("TRB_ITER_FLOOR");
     d_.iter_floor = ef ? std::max(1, atoi(ef)) : 6;  // iteration history is noisy: order mostly by area
     d_.G = G;

@@ -74,6 +74,7 @@ struct TrackDev {
   int64_t maxN;
   double* u2;  // v2 engine: per-CTA ux2 / uy2 (W + H + 1 doubles each)
   uint32_t* words2;  // v2 engine: per-cluster staged bin words
+  int stream_groups;  // schedule: streams in this many contiguous groups, processed group after group
 };
 
 class TrackerState {
