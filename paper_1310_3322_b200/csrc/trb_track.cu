@@ -2027,74 +2027,134 @@ __global__ void __launch_bounds__(NT) quantize_kernel(const int* px, int n, int 
 // thread runs the reference's sequential algorithm with non-contracted
 // __d*_rn arithmetic and the device mt19937_64.  Used by the public free
 // function only; the tracker's samples are pixels (integers: quantize_kernel).
-__global__ void quantize_serial_kernel(const double* __restrict__ px, int64_t n, int k, int iters, uint64_t seed,
-                                       double* __restrict__ centers, double* __restrict__ d2,
-                                       int* __restrict__ assign, double* __restrict__ sum,
-                                       int64_t* __restrict__ count, Mt64* rng) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) quantize_serial_kernel(const double* __restrict__ px, int64_t n, int k,
+                                                              int iters, uint64_t seed, double* __restrict__ centers,
+                                                              double* __restrict__ d2, int* __restrict__ assign,
+                                                              double* __restrict__ sum, int64_t* __restrict__ count,
+                                                              Mt64* rng) {
+  // One CTA.  Everything order-independent runs on all threads (distances,
+  // the running D^2 minimum, assignments, counts, the farthest point with the
+  // lowest index on ties); the order-dependent fp64 sums — the D^2 total, the
+  // pick's running prefix, each cluster's coordinate sums — stay sequential in
+  // point order, one thread per chain (quantize.hpp:52-114's order exactly).
+  __shared__ long long s_pick;
+  __shared__ double s_far[32];
+  __shared__ long long s_fari[32];
+  __shared__ int s_moved;
+  const int t = threadIdx.x, NTq = blockDim.x;
   auto sq_dist3 = [](const double* a, const double* b) {
     const double dr = xsub(a[0], b[0]), dg = xsub(a[1], b[1]), db = xsub(a[2], b[2]);
     return xadd(xadd(xmul(dr, dr), xmul(dg, dg)), xmul(db, db));
   };
-  rng->seed(seed);
-  const int64_t first = rng->uniform_int(0, n - 1);  // k-means++: uniform first centre
-  for (int c = 0; c < 3; ++c) centers[c] = px[3 * first + c];
+  if (t == 0) {
+    rng->seed(seed);
+    const int64_t first = rng->uniform_int(0, n - 1);  // k-means++: uniform first centre
+    for (int c = 0; c < 3; ++c) centers[c] = px[3 * first + c];
+  }
+  __syncthreads();
+  for (int64_t i = t; i < n; i += NTq) d2[i] = __longlong_as_double(0x7ff0000000000000LL);
+  __syncthreads();
+  double* pre = d2 + n;  // running D^2 prefix of the current pass (the pick's acc values)
+  constexpr int kChunk = 4096;
+  __shared__ double s_chunk[kChunk];
+  __shared__ double s_total;
+  __shared__ unsigned long long s_first;
   for (int nc = 1; nc < k; ++nc) {  // D^2-weighted picks
-    double total = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      double best = __longlong_as_double(0x7ff0000000000000LL);
-      for (int c = 0; c < nc; ++c) {
-        const double d = sq_dist3(&px[3 * i], &centers[3 * c]);
-        best = d < best ? d : best;
+    double total = 0.0;  // thread 0's chain
+    for (int64_t base = 0; base < n; base += kChunk) {
+      const int m = n - base < kChunk ? static_cast<int>(n - base) : kChunk;
+      for (int u = t; u < m; u += NTq) {  // min over the centres so far (order-free: the newest one only)
+        const int64_t i = base + u;
+        const double d = sq_dist3(&px[3 * i], &centers[3 * (nc - 1)]);
+        const double b = d < d2[i] ? d : d2[i];
+        d2[i] = b;
+        s_chunk[u] = b;
       }
-      d2[i] = best;
-      total = xadd(total, best);
+      __syncthreads();
+      if (t == 0)  // the sequential total; its partials are exactly the pick loop's acc
+        for (int u = 0; u < m; ++u) s_chunk[u] = total = xadd(total, s_chunk[u]);
+      __syncthreads();
+      for (int u = t; u < m; u += NTq) pre[base + u] = s_chunk[u];
+      __syncthreads();
     }
+    if (t == 0) {
+      s_total = total;
+      s_first = static_cast<unsigned long long>(n - 1);
+    }
+    __syncthreads();
     int64_t pick = 0;
-    if (total > 0.0) {
-      const double r = xmul(rng->uniform(), total);
-      double acc = 0.0;
-      pick = n - 1;
-      for (int64_t i = 0; i < n; ++i) {
-        acc = xadd(acc, d2[i]);
-        if (acc > r) {
-          pick = i;
+    if (s_total > 0.0) {
+      if (t == 0) s_chunk[0] = xmul(rng->uniform(), s_total);
+      __syncthreads();
+      const double r = s_chunk[0];
+      for (int64_t i = t; i < n; i += NTq)  // first i whose prefix exceeds r (else n - 1)
+        if (pre[i] > r) {
+          atomicMin(&s_first, static_cast<unsigned long long>(i));
           break;
         }
-      }
+      __syncthreads();
+      pick = static_cast<int64_t>(s_first);
     }
-    for (int c = 0; c < 3; ++c) centers[3 * nc + c] = px[3 * pick + c];
+    if (t < 3) centers[3 * nc + t] = px[3 * pick + t];
+    __syncthreads();
   }
   for (int it = 0; it < iters; ++it) {  // Lloyd
-    bool moved = false;
-    for (int64_t i = 0; i < n; ++i) assign[i] = q_assign(centers, k, px[3 * i], px[3 * i + 1], px[3 * i + 2]);
-    for (int c = 0; c < 3 * k; ++c) sum[c] = 0.0;
-    for (int c = 0; c < k; ++c) count[c] = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      const int c = assign[i];
-      sum[3 * c] = xadd(sum[3 * c], px[3 * i]);
-      sum[3 * c + 1] = xadd(sum[3 * c + 1], px[3 * i + 1]);
-      sum[3 * c + 2] = xadd(sum[3 * c + 2], px[3 * i + 2]);
-      count[c] += 1;
+    for (int64_t i = t; i < n; i += NTq) assign[i] = q_assign(centers, k, px[3 * i], px[3 * i + 1], px[3 * i + 2]);
+    for (int c = t; c < k; c += NTq) count[c] = 0;
+    __syncthreads();
+    for (int64_t i = t; i < n; i += NTq)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&count[assign[i]]), 1ull);
+    for (int j = t; j < 3 * k; j += NTq) {  // one register chain per (cluster, coordinate), point order
+      const int c = j / 3, q = j - 3 * c;
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i)  // assign[i] is a warp-wide broadcast load
+        if (assign[i] == c) acc = xadd(acc, px[3 * i + q]);
+      sum[j] = acc;
     }
-    for (int c = 0; c < k; ++c) {  // centres update in order (empty ones see the partial update)
-      double nc3[3];
-      if (count[c] == 0) {
-        int64_t far = 0;
-        double far_d = -1.0;
-        for (int64_t i = 0; i < n; ++i) {
+    if (t == 0) s_moved = 0;
+    __syncthreads();
+    for (int c = 0; c < k; ++c) {  // centres update in order (an empty one sees the partial update)
+      if (count[c] == 0) {  // farthest point (first index on ties) from its current centre
+        __syncthreads();  // earlier centres' updates visible
+        double fd = -1.0;
+        long long fi = 0;
+        for (int64_t i = t; i < n; i += NTq) {
           const double d = sq_dist3(&px[3 * i], &centers[3 * assign[i]]);
-          if (d > far_d) far_d = d, far = i;
+          if (d > fd) fd = d, fi = i;
         }
-        for (int q = 0; q < 3; ++q) nc3[q] = px[3 * far + q];
-      } else {
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_down_sync(0xffffffffu, fd, o);
+          const long long oi = __shfl_down_sync(0xffffffffu, fi, o);
+          if (od > fd || (od == fd && oi < fi)) fd = od, fi = oi;
+        }
+        if ((t & 31) == 0) s_far[t >> 5] = fd, s_fari[t >> 5] = fi;
+        __syncthreads();
+        if (t == 0) {
+          double bd = s_far[0];
+          long long bi = s_fari[0];
+          for (int w = 1; w < NTq / 32; ++w)
+            if (s_far[w] > bd || (s_far[w] == bd && s_fari[w] < bi)) bd = s_far[w], bi = s_fari[w];
+          s_pick = bi;
+        }
+        __syncthreads();
+        if (t == 0) {
+          double nc3[3];
+          for (int q = 0; q < 3; ++q) nc3[q] = px[3 * s_pick + q];
+          if (nc3[0] != centers[3 * c] || nc3[1] != centers[3 * c + 1] || nc3[2] != centers[3 * c + 2]) s_moved = 1;
+          for (int q = 0; q < 3; ++q) centers[3 * c + q] = nc3[q];
+        }
+        __syncthreads();
+      } else if (t == 0) {
         const double m = static_cast<double>(count[c]);
+        double nc3[3];
         for (int q = 0; q < 3; ++q) nc3[q] = xdiv(sum[3 * c + q], m);
+        if (nc3[0] != centers[3 * c] || nc3[1] != centers[3 * c + 1] || nc3[2] != centers[3 * c + 2]) s_moved = 1;
+        for (int q = 0; q < 3; ++q) centers[3 * c + q] = nc3[q];
       }
-      if (nc3[0] != centers[3 * c] || nc3[1] != centers[3 * c + 1] || nc3[2] != centers[3 * c + 2]) moved = true;
-      for (int q = 0; q < 3; ++q) centers[3 * c + q] = nc3[q];
     }
-    if (!moved) break;
+    __syncthreads();
+    if (!s_moved) break;
+    __syncthreads();
   }
 }
 
@@ -2650,13 +2710,13 @@ void device_quantize_colors(const double* pixels, int64_t n, int k, int iters, u
     DevBuf dpx, dc, dd2, das, dsum, dcnt, drng;
     dpx.alloc(sizeof(double) * 3 * n, false);
     dc.alloc(sizeof(double) * 3 * k, false);
-    dd2.alloc(sizeof(double) * n, false);
+    dd2.alloc(sizeof(double) * 2 * n, false);  // D^2 + its running prefix
     das.alloc(sizeof(int) * n, false);
     dsum.alloc(sizeof(double) * 3 * k, false);
     dcnt.alloc(sizeof(int64_t) * k, false);
     drng.alloc(sizeof(Mt64), false);
     TRB_CUDA(cudaMemcpyAsync(dpx.p, pixels, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
-    quantize_serial_kernel<<<1, 1, 0, st>>>(dpx.as<double>(), n, k, iters, seed, dc.as<double>(), dd2.as<double>(),
+    quantize_serial_kernel<<<1, 1024, 0, st>>>(dpx.as<double>(), n, k, iters, seed, dc.as<double>(), dd2.as<double>(),
                                             das.as<int>(), dsum.as<double>(), dcnt.as<int64_t>(), drng.as<Mt64>());
     TRB_LAUNCH_CHECK("quantize_serial_kernel");
     TRB_CUDA(cudaMemcpyAsync(centers, dc.p, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost, st));

@@ -49,7 +49,11 @@ def test_quantize_colors_real_valued_vs_oracle(gpu):
     cases = [(clumps[np.arange(60) % 3] + rng.uniform(-5.0, 5.0, (60, 3)), 3, 30, 11),
              (rng.uniform(0.0, 255.0, (40, 3)), 4, 20, 9),
              (rng.uniform(0.0, 255.0, (700, 3)), 16, 20, 123),
-             (np.round(rng.uniform(0, 255, (300, 3))) + 0.5, 8, 20, 77)]
+             (np.round(rng.uniform(0, 255, (300, 3))) + 0.5, 8, 20, 77),
+             # duplicates -> empty clusters (farthest-point re-seed), many samples, large k
+             (np.repeat(rng.uniform(0.0, 255.0, (5, 3)), 40, axis=0) + 0.25, 9, 20, 5),
+             (rng.uniform(0.0, 255.0, (40000, 3)), 24, 15, 31),
+             (clumps[np.arange(20000) % 3] + rng.normal(0.0, 3.0, (20000, 3)), 70, 10, 2)]
     for px, k, iters, seed in cases:
         px = np.ascontiguousarray(px)
         want = np.zeros(3 * k)

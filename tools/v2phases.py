@@ -19,11 +19,12 @@ from paper_1310_3322_b200.abi import MOTION_CFG, SEG_CFG, TRACKER_CFG  # noqa: E
 from paper_1310_3322_b200.synth import device_frames, recipe  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+cfg = sys.argv[2] if len(sys.argv) > 2 else "C5"
 steps = 5
-clips = [recipe("C5", s) for s in range(S)]
+clips = [recipe("C5", s) for s in range(S)] if cfg == "C5" else [recipe(cfg)] * S
 n = 95 + steps
 frames = device_frames(clips, n)
-st = trb.Streams(S, 1920, 1080, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
+st = trb.Streams(S, clips[0].width, clips[0].height, 1, MOTION_CFG(), SEG_CFG(), TRACKER_CFG())
 for t in range(95):
     st.step_device([frames[s, t].data_ptr() for s in range(S)])
 st.synchronize()
