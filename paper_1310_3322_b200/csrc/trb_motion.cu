@@ -306,73 +306,107 @@ __global__ void __launch_bounds__(64) motion_mode_kernel(ModeArgs a) {
 // (2*sum + cnt) / (2*cnt) as window_background (motion.hpp:142-143); the mask
 // is |v - bg| > threshold (:189-190).  Per push ~12 B/px plus 1 B per bin
 // for the pixels that rescan, instead of the W-byte ring re-read.
-template <int CH>
-__device__ __forceinline__ void mode_inc_pixel(const ModeIncArgs& a, int s, int64_t p, uint32_t v) {
-  // two dependent load rounds (sample / ring / mode bin, then the touched
-  // counters), all arithmetic in registers with the aliasing between the
-  // old, new and mode bins resolved explicitly, then the stores
-  const int64_t px = a.px;
-  uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * px;
-  uint8_t* __restrict__ cnt = a.cnt + static_cast<int64_t>(s) * a.bins * px + p;
-  uint16_t* __restrict__ bsum = a.bsum + static_cast<int64_t>(s) * a.bins * px + p;
-  uint8_t* __restrict__ mode = a.mode + static_cast<int64_t>(s) * px + p;
-  const bool full = a.full_before != 0;
-  const uint32_t old = full ? ring[p] : 0u;
-  int m = *mode;
-  const int bn = static_cast<int>((v * static_cast<uint32_t>(a.bins)) >> 8);
-  const int bo = static_cast<int>((old * static_cast<uint32_t>(a.bins)) >> 8);
-  const bool moved = !full || bo != bn;  // counts change
-  int c_bn = cnt[bn * px], c_m = cnt[m * px];
-  uint32_t s_bn = bsum[bn * px], s_m = bsum[m * px];
-  int c_bo = 0;
-  uint32_t s_bo = 0;
-  if (full && bo != bn) c_bo = cnt[bo * px], s_bo = bsum[bo * px];
-  ring[p] = static_cast<uint8_t>(v);
-  if (!moved) {
-    s_bn = s_bn + v - old;
-  } else {
-    if (full) c_bo -= 1, s_bo -= old;
-    c_bn += 1, s_bn += v;
-  }
-  if (m == bn) c_m = c_bn, s_m = s_bn;
-  if (full && m == bo && bo != bn) c_m = c_bo, s_m = s_bo;
-  if (full && bo != bn && bo == m) {  // the mode bin lost a sample: rescan (new values for bo / bn)
-    int best = 0, bc = -1;
-#pragma unroll 8
-    for (int b = 0; b < a.bins; ++b) {
-      const int c = b == bo ? c_bo : (b == bn ? c_bn : cnt[b * px]);
-      if (c > bc) bc = c, best = b;
-    }
-    m = best, c_m = bc;
-    s_m = m == bo ? s_bo : (m == bn ? s_bn : bsum[m * px]);
-  } else if (moved && bn != m && (c_bn > c_m || (c_bn == c_m && bn < m))) {
-    m = bn, c_m = c_bn, s_m = s_bn;
-  }
-  cnt[bn * px] = static_cast<uint8_t>(c_bn);
-  bsum[bn * px] = static_cast<uint16_t>(s_bn);
-  if (full && bo != bn) cnt[bo * px] = static_cast<uint8_t>(c_bo), bsum[bo * px] = static_cast<uint16_t>(s_bo);
-  *mode = static_cast<uint8_t>(m);
-  if (!a.emit) return;
-  const uint32_t bg = (2 * s_m + static_cast<uint32_t>(c_m)) / (2 * static_cast<uint32_t>(c_m));
-  a.mask[static_cast<int64_t>(s) * px + p] = thr_mask(v, bg, a.threshold);
+// P pixels per thread (block-strided, so every load instruction of a warp
+// is one coalesced run), in three rounds per thread: (1) the samples, the
+// evicted ring samples and the mode bins of all P pixels; (2) every touched
+// counter of all P pixels — no store before the last load, so the loads of
+// a round are all in flight together (the kernel is latency-bound: two
+// dependent DRAM round trips per pixel); (3) arithmetic with the aliasing
+// between the old, new and mode bins resolved in registers, the rare
+// rescans, and the stores — counters, mode bin and ring slot only where
+// they change.
+// floor(n / d) for n < 2^17, 1 <= d < 2^9 (the Mode background's rounded
+// mean): a float reciprocal estimate and one correction step each way.
+__device__ __forceinline__ uint32_t div_small(uint32_t n, uint32_t d) {
+  uint32_t q = static_cast<uint32_t>(__fmul_rz(static_cast<float>(n), __frcp_rn(static_cast<float>(d))));
+  if (q * d > n) --q;
+  if ((q + 1) * d <= n) ++q;
+  return q;
 }
 
-// kModePix pixels per thread, block-strided (4 measured slower than 1).
-constexpr int kModePix = 1;
-template <int CH>
+template <int CH, int P>
 __global__ void __launch_bounds__(256) motion_mode_inc_kernel(ModeIncArgs a) {
   const int s = blockIdx.y;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kModePix + threadIdx.x;
-  uint32_t v[kModePix];
+  // (64-bit offsets: 32-bit ones measured 10-25 % slower — extra widening per address)
+  using Off = int64_t;
+  const Off px = a.px;
+  const Off base = static_cast<Off>(blockIdx.x) * 256 * P + threadIdx.x;
+  uint8_t* __restrict__ ring = a.ring + static_cast<int64_t>(s) * a.ring_stride + static_cast<int64_t>(a.slot) * px;
+  uint8_t* __restrict__ cnt = a.cnt + static_cast<int64_t>(s) * a.bins * px;
+  uint16_t* __restrict__ bsum = a.bsum + static_cast<int64_t>(s) * a.bins * px;
+  uint8_t* __restrict__ mode = a.mode + static_cast<int64_t>(s) * px;
+  uint8_t* __restrict__ mask = a.mask + static_cast<int64_t>(s) * px;
+  const uint8_t* __restrict__ frame = a.frames[s];
+  const bool full = a.full_before != 0;
+  const uint32_t nb = static_cast<uint32_t>(a.bins);
+  uint32_t v[P], old[P];
+  uint32_t m[P];
 #pragma unroll
-  for (int k = 0; k < kModePix; ++k) {
-    const int64_t p = base + static_cast<int64_t>(k) * blockDim.x;
-    v[k] = p < a.px ? load1<CH>(a.frames[s], p) : 0;
+  for (int k = 0; k < P; ++k) {
+    const Off p = base + k * 256;
+    v[k] = 0, old[k] = 0, m[k] = 0;
+    if (p < px) {
+      v[k] = load1<CH>(frame, p);
+      if (full) old[k] = ring[p];
+      m[k] = mode[p];
+    }
+  }
+  int c_bn[P], c_m[P], c_bo[P];
+  uint32_t s_bn[P], s_m[P], s_bo[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const Off p = base + k * 256;
+    c_bn[k] = c_m[k] = c_bo[k] = 0;
+    s_bn[k] = s_m[k] = s_bo[k] = 0;
+    if (p < px) {
+      const uint32_t bn = (v[k] * nb) >> 8, bo = (old[k] * nb) >> 8;
+      c_bn[k] = cnt[bn * px + p], s_bn[k] = bsum[bn * px + p];
+      if (m[k] != bn) c_m[k] = cnt[m[k] * px + p], s_m[k] = bsum[m[k] * px + p];
+      if (full && bo != bn && bo != m[k]) c_bo[k] = cnt[bo * px + p], s_bo[k] = bsum[bo * px + p];
+    }
   }
 #pragma unroll
-  for (int k = 0; k < kModePix; ++k) {
-    const int64_t p = base + static_cast<int64_t>(k) * blockDim.x;
-    if (p < a.px) mode_inc_pixel<CH>(a, s, p, v[k]);
+  for (int k = 0; k < P; ++k) {
+    const Off p = base + k * 256;
+    if (p >= px) continue;
+    const uint32_t bn = (v[k] * nb) >> 8, bo = (old[k] * nb) >> 8;
+    const uint32_t m0 = m[k];
+    int cm = c_m[k], cbn = c_bn[k], cbo = c_bo[k];
+    uint32_t sm_ = s_m[k], sbn = s_bn[k], sbo = s_bo[k];
+    if (m0 == bn) cm = cbn, sm_ = sbn;
+    if (full && bo != bn && bo == m0) cbo = cm, sbo = sm_;
+    const bool moved = !full || bo != bn;  // counts change
+    if (!moved) {
+      sbn = sbn + v[k] - old[k];
+    } else {
+      if (full) cbo -= 1, sbo -= old[k];
+      cbn += 1, sbn += v[k];
+    }
+    if (m0 == bn) cm = cbn, sm_ = sbn;
+    if (full && m0 == bo && bo != bn) cm = cbo, sm_ = sbo;
+    uint32_t mm = m0;
+    if (full && bo != bn && bo == m0) {  // the mode bin lost a sample: rescan (new values for bo / bn)
+      uint32_t best = 0;
+      int bc = -1;
+#pragma unroll 8
+      for (uint32_t b = 0; b < nb; ++b) {
+        const int c = b == bo ? cbo : (b == bn ? cbn : cnt[b * px + p]);
+        if (c > bc) bc = c, best = b;
+      }
+      mm = best, cm = bc;
+      sm_ = mm == bo ? sbo : (mm == bn ? sbn : bsum[mm * px + p]);
+    } else if (moved && bn != m0 && (cbn > cm || (cbn == cm && bn < m0))) {
+      mm = bn, cm = cbn, sm_ = sbn;
+    }
+    if (moved) cnt[bn * px + p] = static_cast<uint8_t>(cbn);
+    if (moved || v[k] != old[k]) bsum[bn * px + p] = static_cast<uint16_t>(sbn);
+    if (full && bo != bn) cnt[bo * px + p] = static_cast<uint8_t>(cbo), bsum[bo * px + p] = static_cast<uint16_t>(sbo);
+    if (mm != m0) mode[p] = static_cast<uint8_t>(mm);
+    if (!full || v[k] != old[k]) ring[p] = static_cast<uint8_t>(v[k]);
+    if (a.emit) {
+      const uint32_t bg = div_small(2 * sm_ + static_cast<uint32_t>(cm), 2 * static_cast<uint32_t>(cm));
+      mask[p] = thr_mask(v[k], bg, a.threshold);
+    }
   }
 }
 
@@ -603,10 +637,22 @@ void launch_motion_mean(const MotionArgs& a, int channels, bool wide_sums, int n
   TRB_LAUNCH_CHECK("motion_mean_kernel");
 }
 
+template <int P>
+static void launch_mode_inc_p(const ModeIncArgs& a, int channels, int n_streams, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div64(a.px, 256 * P)), n_streams);
+  if (channels == 1) motion_mode_inc_kernel<1, P><<<grid, 256, 0, st>>>(a);
+  else motion_mode_inc_kernel<3, P><<<grid, 256, 0, st>>>(a);
+}
+
 void launch_motion_mode_inc(const ModeIncArgs& a, int channels, int n_streams, cudaStream_t st) {
-  dim3 grid(static_cast<unsigned>(ceil_div64(a.px, 256 * kModePix)), n_streams);
-  if (channels == 1) motion_mode_inc_kernel<1><<<grid, 256, 0, st>>>(a);
-  else motion_mode_inc_kernel<3><<<grid, 256, 0, st>>>(a);
+  static const int pix = [] {  // pixels per thread (A/B knob)
+    const char* e = getenv("TRB_MODE_PIX");
+    return e ? atoi(e) : 2;  // A/B (C5MODE): 2 ahead of 1, 4, 8
+  }();
+  if (pix == 1) launch_mode_inc_p<1>(a, channels, n_streams, st);
+  else if (pix == 2) launch_mode_inc_p<2>(a, channels, n_streams, st);
+  else if (pix == 8) launch_mode_inc_p<8>(a, channels, n_streams, st);
+  else launch_mode_inc_p<4>(a, channels, n_streams, st);
   TRB_LAUNCH_CHECK("motion_mode_inc_kernel");
 }
 
