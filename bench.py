@@ -596,7 +596,11 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     mode = cfg.get("method", 0) == 1
     mb = ((MODE_BYTES_PER_PX if mode else MOTION_BYTES_PER_PX) + (2 if cfg.get("morph") else 0)) * S * px
     ma = mb / (motion_ms / 1e3) / 1e9 if motion_ms > 0 else 0.0
-    roofline_motion = {"bound": "hbm", "kernel": ("motion_mode_inc_kernel" if mode else "motion_mean_kernel") +
+    # the Mean kernel: motion_mean_bulk_kernel for gray frames with 16-byte
+    # aligned planes (bench frames are), W <= 257 (u16 sums), TRB_MOTION_BULK unset/1
+    bulk = W_DEFAULT <= 257 and os.environ.get("TRB_MOTION_BULK", "1") != "0"
+    mean_kernel = "motion_mean_bulk_kernel" if bulk else "motion_mean_kernel"
+    roofline_motion = {"bound": "hbm", "kernel": ("motion_mode_inc_kernel" if mode else mean_kernel) +
                        (" + morph_strip_kernel" if cfg.get("morph") else ""),
                        "achieved": ma, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ma / peak,
                        "traffic": dram_traffic("motion_dram_bytes.json"), "bytes_per_launch": mb,
