@@ -59,6 +59,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 W_DEFAULT = 91
+HBM_NOMINAL_GBS = 8000.0  # B200 nominal HBM3e (also report against it)
 METRIC = "frames/sec (1080p, device-timed) motion+segment+track"
 MOTION_BYTES_PER_PX = 8   # frame 1 + evict 1 + insert 1 + u16 sum 2+2 + mask 1
 PATH_BYTES_PER_PX = 12    # + int32 labels
@@ -574,6 +575,7 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
         a = MORPH_BYTES_PER_PX * S * px / (morph_ms / 1e3) / 1e9
         roofline_morph = {"bound": "hbm", "kernel": "morph_strip_kernel<open> (erode+dilate fused)", "achieved": a,
                           "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": a / peak,
+                          "frac_nominal_8tbs": a / HBM_NOMINAL_GBS,
                           "bytes_per_launch": MORPH_BYTES_PER_PX * S * px, "ms_per_launch": morph_ms,
                           "note": "back-to-back launches on the step's masks; C2M times it inside the step"}
         del morph_out
@@ -603,6 +605,7 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     roofline_motion = {"bound": "hbm", "kernel": ("motion_mode_inc_kernel" if mode else mean_kernel) +
                        (" + morph_strip_kernel" if cfg.get("morph") else ""),
                        "achieved": ma, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ma / peak,
+                       "frac_nominal_8tbs": ma / HBM_NOMINAL_GBS,
                        "traffic": dram_traffic("motion_dram_bytes.json"), "bytes_per_launch": mb,
                        "ms_per_step": motion_ms}
     ms_ms = stage_ms[2]
@@ -611,6 +614,7 @@ def ours_config(args, name, rank, world, local_rank, bind_info, first):
     dominant = stage_names[int(np.argmax(stage_ms))] if prof_steps else "unknown"
     roofline = {"bound": "hbm", "kernel": "track_meanshift_kernel", "achieved": ms_achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": ms_achieved / peak,
+                "frac_nominal_8tbs": ms_achieved / HBM_NOMINAL_GBS,
                 "traffic": dram_traffic("meanshift_dram_bytes.json"), "bytes_per_launch": track_px,
                 "ms_per_step": ms_ms, "dominant_stage": dominant,
                 "algorithmic_bytes": "SURVEY §8(d): window px x iterations x channels (1 B) of frame reads",
