@@ -437,6 +437,36 @@ __device__ __forceinline__ int bin_of(const uint8_t* frame, int fw, int ch, int 
 }
 
 // Bin every window pixel (cached for the centroid pass) and stably
+// Per-cluster scratch (partitioned weights, bin words) is rewritten every
+// iteration at the same addresses: its stores carry an L2 evict_last policy
+// so the lines stay in L2 between iterations instead of being written back
+// to HBM while the overlapped motion/CCL kernels stream through L2
+// (TRB_SCRATCH_HINT=0 at build time disables it for A/B).
+#ifndef TRB_SCRATCH_HINT
+#define TRB_SCRATCH_HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol = 0;
+#if TRB_SCRATCH_HINT
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+#if TRB_SCRATCH_HINT
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, uint64_t pol) {
+#if TRB_SCRATCH_HINT
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+
 // partition the positive-weight pixels by bin across the cluster:
 // sm.binoff[b] = start of bin b, scratch.vals = weights in (bin, raster)
 // order.  Returns the number of positive-weight pixels.
@@ -461,9 +491,10 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     int xx = j0 % ww, yy = j0 / ww, npos = 0;
     unsigned wacc = 0;
     uint32_t* bw = reinterpret_cast<uint32_t*>(scr.bins) + gt;
+    const uint64_t pol = l2_keep_policy();
     // a 4-pixel word of bins is complete: store it (word-interleaved)
     auto put_word = [&](int /*j*/, bool /*last*/) {
-      *bw = wacc;
+      st_keep(bw, wacc, pol);
       bw += GT;
       wacc = 0;
     };
@@ -561,6 +592,7 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
     const uint32_t cK = static_cast<uint32_t>(sm.cnt[K * NT_ + t]);
     int gT = static_cast<int>(cK >> 20), iT = static_cast<int>(cK & 0xfffffu);
     auto at = [&](int g, int i) { return (static_cast<int64_t>(i >> 1) * GT + g) * 2 + (i & 1); };
+    const uint64_t pol = l2_keep_policy();
     for (int j = j0; j < j1; ++j) {
       const double w = epan_weight(sm, xx, yy, epan);
       const int b = (word >> (8 * (j & 3))) & 0xffu;
@@ -569,10 +601,10 @@ __device__ int partition_window(const uint8_t* frame, int fw, int ch, const Win&
         TRB_CHECK(b < K, "partition scatter", b, j);
         const uint32_t cb = static_cast<uint32_t>(sm.cnt[b * NT_ + t]);
         int g = static_cast<int>(cb >> 20), i = static_cast<int>(cb & 0xfffffu);
-        scr.vals[at(g, i)] = w;
+        st_keep(&scr.vals[at(g, i)], w, pol);
         if (++i == Cv) i = 0, ++g;
         sm.cnt[b * NT_ + t] = static_cast<int>((static_cast<uint32_t>(g) << 20) | static_cast<uint32_t>(i));
-        scr.vals[at(gT, iT)] = w;
+        st_keep(&scr.vals[at(gT, iT)], w, pol);
         if (++iT == Cv) iT = 0, ++gT;
       }
       if (++xx == ww) xx = 0, ++yy;
