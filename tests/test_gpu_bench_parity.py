@@ -8,8 +8,8 @@ restatement:
 * all 64 C5 streams through frame 134 (the bench's 90 fill + warm-up +
   timed + profile frames) — per steady frame the mask and label planes
   (plane_hash digests), the blob tables, and the whole track log;
-* the full 300-frame C3 clip (BASELINE configs[2]) and 60 steady C4 frames
-  (configs[3]) the same way;
+* the full 300-frame C3 clip (BASELINE configs[2]), 8 C5 streams through
+  the whole 300-frame clip, and 60 steady C4 frames (configs[3]) the same way;
 * the glibc hypot replica that decides gating and convergence on 1e8 device
   samples.
 Steps run exactly as bench.py issues them (step_device on device frames,
@@ -112,6 +112,18 @@ def test_c5_all_64_streams_through_bench_frames_vs_reference(gpu):
     per_ref = ref_batches(clips, BENCH_FRAMES)
     compare(per_gpu, per_ref)
     assert sum(len(g["log"]) for g in per_gpu) > 64 * 45  # tracks were live throughout
+
+
+def test_c5_streams_full_300_frame_clips_vs_reference(gpu):
+    """Past the bench's frames: 8 C5 streams (stream seeds 60..67: four of the
+    bench's and four beyond) through the whole 300-frame clip — every steady frame's planes and
+    blob table and the whole track log, as the e2e leg's later frames see."""
+    _need_ref()
+    clips = [recipe("C5", s) for s in range(60, 68)]
+    per_gpu = run_gpu(gpu, clips, 300)
+    per_ref = ref_batches(clips, 300, batch=8, threads=8)
+    compare(per_gpu, per_ref)
+    assert all(len(g["hashes"]) == 210 for g in per_gpu)
 
 
 def test_c3_full_300_frame_clip_vs_reference(gpu):
