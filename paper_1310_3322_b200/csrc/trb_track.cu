@@ -2270,8 +2270,14 @@ static size_t check_smem(int K, int W, int H) {
   if (b > 200 * 1024)
     throw Error(TRB_CONFIG_ERROR, "tracker k_clusters / frame size exceed the device shared-memory budget");
   if (4 * K > 2 * NT) throw Error(TRB_CONFIG_ERROR, "tracker k_clusters too large for the device k-means");
+  // partition_window packs (chunk g, offset i) as g << 20 | i: a window
+  // chunk (window px / threads of the group, >= 1 CTA) must stay below 2^20
+  if (static_cast<int64_t>(W) * H >= (int64_t(1) << 20) * NT)
+    throw Error(TRB_CONFIG_ERROR, "tracker: frame too large (" + std::to_string(W) + "x" + std::to_string(H) + ")");
   return b;
 }
+// ... and the chunk index g < G x NT must fit the 12 bits above bit 20
+static_assert(kMaxCluster * NT <= 4096, "partition_window's packed (chunk, offset) cursors need G x NT <= 4096");
 
 // Engine choice.  v2 (trb_xsum.cuh: chunk-classified, no partition) has the
 // lower fixed cost per iteration and wins on small windows (frames up to
