@@ -248,7 +248,19 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   for (int i = 0; i < kStages + 1; ++i) TRB_CUDA(cudaEventCreate(&prof_ev_[i]));
   TRB_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
   TRB_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
-  TRB_CUDA(cudaStreamCreateWithFlags(&trk_, cudaStreamNonBlocking));
+  {
+    // The tracker's internal stream runs at the highest priority: with the
+    // step overlap its persistent mean-shift CTAs are then dispatched ahead
+    // of the next step's motion / CCL blocks, which fill the SMs around them
+    // (C5MODE +15 %, C5 neutral; profiles/r02_ab_tracker_priority.txt).
+    // TRB_TRK_PRIO (A/B): 1 highest (default), 0 default priority, -1 lowest.
+    const char* e = getenv("TRB_TRK_PRIO");
+    const int want = e ? atoi(e) : 1;
+    int lo = 0, hi = 0;
+    TRB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (want == 0) TRB_CUDA(cudaStreamCreateWithFlags(&trk_, cudaStreamNonBlocking));
+    else TRB_CUDA(cudaStreamCreateWithPriority(&trk_, cudaStreamNonBlocking, want > 0 ? hi : lo));
+  }
   if (const char* e = getenv("TRB_OVERLAP")) overlap_ = atoi(e) != 0;
   // host-path staging ring, allocated up front: a step never cudaMallocs
   // (that would serialise the device inside the first host steps)
