@@ -324,6 +324,64 @@ __device__ __forceinline__ uint32_t div_small(uint32_t n, uint32_t d) {
   return q;
 }
 
+// One pixel's push given its loaded state: sample v, evicted sample old, mode
+// bin m0 and the counters of the new / mode / evicted bins (c_m / s_m valid
+// when m0 != bn, c_bo / s_bo when bo differs from both).  Stores the changed
+// counters (the rare rescan loads the pixel's other bins) and returns the
+// new mode bin with its count and sum.
+struct ModeOut {
+  uint32_t mm;
+  int cm;
+  uint32_t sm;
+};
+__device__ __forceinline__ ModeOut mode_push(uint32_t v, uint32_t old, uint32_t m0, int cbn, uint32_t sbn, int cm,
+                                             uint32_t sm_, int cbo, uint32_t sbo, bool full, uint32_t nb,
+                                             uint8_t* __restrict__ cnt, uint16_t* __restrict__ bsum, int64_t px,
+                                             int64_t p) {
+  const uint32_t bn = (v * nb) >> 8, bo = (old * nb) >> 8;
+  if (m0 == bn) cm = cbn, sm_ = sbn;
+  if (full && bo != bn && bo == m0) cbo = cm, sbo = sm_;
+  const bool moved = !full || bo != bn;  // counts change
+  if (!moved) {
+    sbn = sbn + v - old;
+  } else {
+    if (full) cbo -= 1, sbo -= old;
+    cbn += 1, sbn += v;
+  }
+  if (m0 == bn) cm = cbn, sm_ = sbn;
+  if (full && m0 == bo && bo != bn) cm = cbo, sm_ = sbo;
+  uint32_t mm = m0;
+  if (full && bo != bn && bo == m0) {  // the mode bin lost a sample: rescan (new values for bo / bn)
+    uint32_t best = 0;
+    int bc = -1;
+#pragma unroll 8
+    for (uint32_t b = 0; b < nb; ++b) {
+      const int c = b == bo ? cbo : (b == bn ? cbn : cnt[b * px + p]);
+      if (c > bc) bc = c, best = b;
+    }
+    mm = best, cm = bc;
+    sm_ = mm == bo ? sbo : (mm == bn ? sbn : bsum[mm * px + p]);
+  } else if (moved && bn != m0 && (cbn > cm || (cbn == cm && bn < m0))) {
+    mm = bn, cm = cbn, sm_ = sbn;
+  }
+  if (moved) cnt[bn * px + p] = static_cast<uint8_t>(cbn);
+  if (moved || v != old) bsum[bn * px + p] = static_cast<uint16_t>(sbn);
+  if (full && bo != bn) cnt[bo * px + p] = static_cast<uint8_t>(cbo), bsum[bo * px + p] = static_cast<uint16_t>(sbo);
+  return ModeOut{mm, cm, sm_};
+}
+
+// The touched counters of one pixel (round 2 of the kernels below).
+__device__ __forceinline__ void mode_loads(uint32_t v, uint32_t old, uint32_t m, bool full, uint32_t nb,
+                                           const uint8_t* __restrict__ cnt, const uint16_t* __restrict__ bsum,
+                                           int64_t px, int64_t p, int& c_bn, uint32_t& s_bn, int& c_m,
+                                           uint32_t& s_m, int& c_bo, uint32_t& s_bo) {
+  const uint32_t bn = (v * nb) >> 8, bo = (old * nb) >> 8;
+  c_m = c_bo = 0, s_m = s_bo = 0;
+  c_bn = cnt[bn * px + p], s_bn = bsum[bn * px + p];
+  if (m != bn) c_m = cnt[m * px + p], s_m = bsum[m * px + p];
+  if (full && bo != bn && bo != m) c_bo = cnt[bo * px + p], s_bo = bsum[bo * px + p];
+}
+
 template <int CH, int P>
 __global__ void __launch_bounds__(256) motion_mode_inc_kernel(ModeIncArgs a) {
   const int s = blockIdx.y;
@@ -356,55 +414,18 @@ __global__ void __launch_bounds__(256) motion_mode_inc_kernel(ModeIncArgs a) {
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const Off p = base + k * 256;
-    c_bn[k] = c_m[k] = c_bo[k] = 0;
-    s_bn[k] = s_m[k] = s_bo[k] = 0;
-    if (p < px) {
-      const uint32_t bn = (v[k] * nb) >> 8, bo = (old[k] * nb) >> 8;
-      c_bn[k] = cnt[bn * px + p], s_bn[k] = bsum[bn * px + p];
-      if (m[k] != bn) c_m[k] = cnt[m[k] * px + p], s_m[k] = bsum[m[k] * px + p];
-      if (full && bo != bn && bo != m[k]) c_bo[k] = cnt[bo * px + p], s_bo[k] = bsum[bo * px + p];
-    }
+    if (p < px) mode_loads(v[k], old[k], m[k], full, nb, cnt, bsum, px, p, c_bn[k], s_bn[k], c_m[k], s_m[k], c_bo[k], s_bo[k]);
   }
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const Off p = base + k * 256;
     if (p >= px) continue;
-    const uint32_t bn = (v[k] * nb) >> 8, bo = (old[k] * nb) >> 8;
-    const uint32_t m0 = m[k];
-    int cm = c_m[k], cbn = c_bn[k], cbo = c_bo[k];
-    uint32_t sm_ = s_m[k], sbn = s_bn[k], sbo = s_bo[k];
-    if (m0 == bn) cm = cbn, sm_ = sbn;
-    if (full && bo != bn && bo == m0) cbo = cm, sbo = sm_;
-    const bool moved = !full || bo != bn;  // counts change
-    if (!moved) {
-      sbn = sbn + v[k] - old[k];
-    } else {
-      if (full) cbo -= 1, sbo -= old[k];
-      cbn += 1, sbn += v[k];
-    }
-    if (m0 == bn) cm = cbn, sm_ = sbn;
-    if (full && m0 == bo && bo != bn) cm = cbo, sm_ = sbo;
-    uint32_t mm = m0;
-    if (full && bo != bn && bo == m0) {  // the mode bin lost a sample: rescan (new values for bo / bn)
-      uint32_t best = 0;
-      int bc = -1;
-#pragma unroll 8
-      for (uint32_t b = 0; b < nb; ++b) {
-        const int c = b == bo ? cbo : (b == bn ? cbn : cnt[b * px + p]);
-        if (c > bc) bc = c, best = b;
-      }
-      mm = best, cm = bc;
-      sm_ = mm == bo ? sbo : (mm == bn ? sbn : bsum[mm * px + p]);
-    } else if (moved && bn != m0 && (cbn > cm || (cbn == cm && bn < m0))) {
-      mm = bn, cm = cbn, sm_ = sbn;
-    }
-    if (moved) cnt[bn * px + p] = static_cast<uint8_t>(cbn);
-    if (moved || v[k] != old[k]) bsum[bn * px + p] = static_cast<uint16_t>(sbn);
-    if (full && bo != bn) cnt[bo * px + p] = static_cast<uint8_t>(cbo), bsum[bo * px + p] = static_cast<uint16_t>(sbo);
-    if (mm != m0) mode[p] = static_cast<uint8_t>(mm);
+    const ModeOut o = mode_push(v[k], old[k], m[k], c_bn[k], s_bn[k], c_m[k], s_m[k], c_bo[k], s_bo[k], full, nb, cnt,
+                                bsum, px, p);
+    if (o.mm != m[k]) mode[p] = static_cast<uint8_t>(o.mm);
     if (!full || v[k] != old[k]) ring[p] = static_cast<uint8_t>(v[k]);
     if (a.emit) {
-      const uint32_t bg = div_small(2 * sm_ + static_cast<uint32_t>(cm), 2 * static_cast<uint32_t>(cm));
+      const uint32_t bg = div_small(2 * o.sm + static_cast<uint32_t>(o.cm), 2 * static_cast<uint32_t>(o.cm));
       mask[p] = thr_mask(v[k], bg, a.threshold);
     }
   }
@@ -646,8 +667,11 @@ static void launch_mode_inc_p(const ModeIncArgs& a, int channels, int n_streams,
 
 void launch_motion_mode_inc(const ModeIncArgs& a, int channels, int n_streams, cudaStream_t st) {
   static const int pix = [] {  // pixels per thread (A/B knob)
+    // A/B (C5MODE): 2 ahead of 1, 4, 8; 4 CONSECUTIVE pixels with 32-bit
+    // sample / ring / mode / mask words measured 1.9x slower (the per-pixel
+    // counter accesses then spread over 4x the sectors per warp instruction)
     const char* e = getenv("TRB_MODE_PIX");
-    return e ? atoi(e) : 2;  // A/B (C5MODE): 2 ahead of 1, 4, 8
+    return e ? atoi(e) : 2;
   }();
   if (pix == 1) launch_mode_inc_p<1>(a, channels, n_streams, st);
   else if (pix == 2) launch_mode_inc_p<2>(a, channels, n_streams, st);
