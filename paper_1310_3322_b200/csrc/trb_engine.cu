@@ -262,6 +262,7 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
     else TRB_CUDA(cudaStreamCreateWithPriority(&trk_, cudaStreamNonBlocking, want > 0 ? hi : lo));
   }
   if (const char* e = getenv("TRB_OVERLAP")) overlap_ = atoi(e) != 0;
+  if (const char* e = getenv("TRB_EARLY_MS")) early_ms_ = atoi(e) != 0;
   // host-path staging ring, allocated up front: a step never cudaMallocs
   // (that would serialise the device inside the first host steps)
   for (int i = 0; i < kStaging; ++i) staging_[i].alloc(static_cast<size_t>(px_) * ch_ * S_, false);
@@ -271,6 +272,7 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   }
   for (int i = 0; i < 2; ++i) {
     TRB_CUDA(cudaEventCreateWithFlags(&ccl_ev_[i], cudaEventDisableTiming));
+    TRB_CUDA(cudaEventCreateWithFlags(&mot_ev_[i], cudaEventDisableTiming));
     TRB_CUDA(cudaEventCreateWithFlags(&trk_ev_[i], cudaEventDisableTiming));
   }
 }
@@ -286,6 +288,7 @@ Streams::~Streams() {
   }
   for (int i = 0; i < 2; ++i) {
     if (ccl_ev_[i]) cudaEventDestroy(ccl_ev_[i]);
+    if (mot_ev_[i]) cudaEventDestroy(mot_ev_[i]);
     if (trk_ev_[i]) cudaEventDestroy(trk_ev_[i]);
   }
   if (trk_) cudaStreamDestroy(trk_);
@@ -318,6 +321,9 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
   has_output_ = emitted;
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[1], st));
   const int b = ccl_->next_buffer();
+  // the step's frames (and their pointer table) are ready for the tracker
+  // once the motion kernel has run (it waited for any upload)
+  if (emitted && tracker_ && overlap && early_ms_) TRB_CUDA(cudaEventRecord(mot_ev_[b], st));
   if (emitted) {
     if (trk_pending_[b]) TRB_CUDA(cudaStreamWaitEvent(st, trk_ev_[b], 0));  // its last reader
     ccl_->run(mask_.as<uint8_t>(), st, &launches);
@@ -325,9 +331,12 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
   if (profiling_) TRB_CUDA(cudaEventRecord(prof_ev_[2], st));
   if (emitted && tracker_ && overlap) {
     TRB_CUDA(cudaEventRecord(ccl_ev_[b], st));
-    TRB_CUDA(cudaStreamWaitEvent(trk_, ccl_ev_[b], 0));
+    // mean-shift needs the frames and the track state only: it starts after
+    // the step's motion kernel, beside the CCL; the gate (the blob table's
+    // first reader) waits for the CCL
+    TRB_CUDA(cudaStreamWaitEvent(trk_, early_ms_ ? mot_ev_[b] : ccl_ev_[b], 0));
     tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), trk_, &launches,
-                      nullptr);
+                      nullptr, early_ms_ ? ccl_ev_[b] : nullptr);
     TRB_CUDA(cudaMemcpyAsync(err_host_.p, tracker_->err_word(), sizeof(int32_t), cudaMemcpyDeviceToHost, trk_));
     if (pending_out_) output_(pending_out_, trk_, &launches);  // before CCL(t+2) may reuse this blob table
     TRB_CUDA(cudaEventRecord(trk_ev_[b], trk_));

@@ -180,7 +180,8 @@ class Streams {
   // step overlap: the tracker of step t runs on trk_ while motion + CCL of
   // step t+1 run on the caller's stream (blob tables double-buffered)
   cudaStream_t trk_ = nullptr;
-  cudaEvent_t ccl_ev_[2] = {}, trk_ev_[2] = {};
+  cudaEvent_t ccl_ev_[2] = {}, trk_ev_[2] = {}, mot_ev_[2] = {};
+  bool early_ms_ = true;  // mean-shift waits for the step's motion only, the gate for its CCL (TRB_EARLY_MS=0: both for CCL)
   bool trk_pending_[2] = {false, false};
   int last_trk_ = -1;
   bool overlap_ = true;  // TRB_OVERLAP=0 disables (A/B)

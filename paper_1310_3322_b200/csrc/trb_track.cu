@@ -2413,7 +2413,8 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
 TrackerState::~TrackerState() = default;
 
 void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int ch, const trb_blob* blobs,
-                           int64_t blob_stride, const int32_t* nblobs, cudaStream_t st, int* launches, cudaEvent_t after_meanshift) {
+                           int64_t blob_stride, const int32_t* nblobs, cudaStream_t st, int* launches, cudaEvent_t after_meanshift,
+                           cudaEvent_t blobs_ready) {
   if (matched_cap_ < blob_stride) {
     matched_.alloc(static_cast<size_t>(blob_stride) * S_);
     matched_cap_ = blob_stride;
@@ -2509,7 +2510,8 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   else
     launch_cluster_ex(pdl, track_meanshift_kernel, gridm, Gm, smem, st, dm);
   if (after_meanshift) TRB_CUDA(cudaEventRecord(after_meanshift, st));
-  if (pdl) launch_pdl(track_gate_kernel, dim3(S_), dim3(NT), 0, st, d_);
+  if (blobs_ready) TRB_CUDA(cudaStreamWaitEvent(st, blobs_ready, 0));
+  if (pdl && !blobs_ready) launch_pdl(track_gate_kernel, dim3(S_), dim3(NT), 0, st, d_);
   else track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
   launch_cluster_ex(pdl, track_spawn_kernel, grid_, G, smem, st, d_);

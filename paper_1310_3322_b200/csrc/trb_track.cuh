@@ -82,10 +82,14 @@ class TrackerState {
   TrackerState(const trb_tracker_config& cfg, int S, int track_cap = 256, int64_t log_cap = 1 << 16);
   ~TrackerState();
   // One Tracker::process for every stream.  blobs: device [S][blob_stride].
+  // blobs_ready (optional): `st` waits for it before the gate kernel, the
+  // first reader of the blob table (mean-shift itself needs only the
+  // frames and the track state).
   // after_meanshift (optional) is recorded on `st` right after the
   // mean-shift kernel (per-stage profiling)
   void process(const uint8_t* const* frames_dev, int w, int h, int ch, const trb_blob* blobs, int64_t blob_stride,
-               const int32_t* nblobs, cudaStream_t st, int* launches, cudaEvent_t after_meanshift = nullptr);
+               const int32_t* nblobs, cudaStream_t st, int* launches, cudaEvent_t after_meanshift = nullptr,
+               cudaEvent_t blobs_ready = nullptr);
   // host-side readers (synchronise `st`)
   int num_tracks(int s, cudaStream_t st);
   void tracks(int s, trb_track* out, int cap, cudaStream_t st);
