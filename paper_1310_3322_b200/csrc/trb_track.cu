@@ -286,18 +286,20 @@ struct BinsSrc {
   struct Cursor {
     const BinsSrc* s;
     const double2* p;  // next block to request
-    int j, b, sb, nb, GT, blk;  // current segment b = [sb, nb); blk = block being consumed
+    int j, b, sb, nb, GT, blk;  // current segment b = [sb, nb); blk = ring slot of the block being consumed
     int k;                      // element of the current 2-element block
     double c0, c1;
     __device__ __forceinline__ void next(int /*k*/, bool& start, int& seg, bool& has, double* v) {
       if (k == 0) {
-        cp_async_wait<kRing - 2>();  // block blk has landed
-        const uint4* slot = s->stage + (blk % kRing) * blockDim.x + threadIdx.x;
+        cp_async_wait<kRing - 2>();  // the block in slot blk has landed
+        const uint4* slot = s->stage + blk * blockDim.x + threadIdx.x;
         const double2 d = *reinterpret_cast<const double2*>(slot);
         c0 = d.x, c1 = d.y;
-        cp_async16(s->stage + ((blk + kRing - 1) % kRing) * blockDim.x + threadIdx.x, p);
+        const int refill = blk == 0 ? kRing - 1 : blk - 1;  // (blk + kRing - 1) % kRing
+        cp_async16(s->stage + refill * blockDim.x + threadIdx.x, p);
         cp_async_commit();
-        p += GT, ++blk;
+        p += GT;
+        blk = blk == kRing - 1 ? 0 : blk + 1;
       }
       if (j >= nb) {
         do ++b;
