@@ -1,4 +1,6 @@
 #!/bin/bash
+# HISTORICAL: the experiment this script A/B-tested was reverted (DESIGN.md lists the result);
+# its knob no longer exists in the library.
 # A/B of the split-mode knobs (early split clusters, split threshold) on C5
 cd "$(dirname "$0")/.."
 CFG=${CFG:-C5}

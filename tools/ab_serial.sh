@@ -1,4 +1,6 @@
 #!/bin/bash
+# HISTORICAL: the experiment this script A/B-tested was reverted (DESIGN.md lists the result);
+# its knob no longer exists in the library.
 # serial sums for tiny windows: correctness + threshold sweep
 cd "$(dirname "$0")/.."
 timeout 600 python -m pytest tests/test_gpu_tracker.py tests/test_gpu_streams.py -x -q 2>&1 | tail -2

@@ -1,4 +1,6 @@
 #!/bin/bash
+# HISTORICAL: the experiment this script A/B-tested was reverted (DESIGN.md lists the result);
+# its knob no longer exists in the library.
 # DRAM bytes of the mean-shift kernel with / without the L2 discard of dead scratch, and the bench line
 cd "$(dirname "$0")/.."
 for dc in 1 0; do
