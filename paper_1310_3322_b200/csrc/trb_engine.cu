@@ -236,8 +236,6 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   motion_ = std::make_unique<MotionState>(mc, S, w, h, ch);
   ccl_ = std::make_unique<CclState>(S, w, h, sc);
   if (with_tracker) tracker_ = std::make_unique<TrackerState>(tc, S, track_cap, log_cap);
-  err_host_.alloc(sizeof(int32_t));
-  *err_host_.as<int32_t>() = 0;
   mask_.alloc(static_cast<size_t>(px_) * S);
   if (mc.morph != TRB_MORPH_NONE) mask_tmp_.alloc(static_cast<size_t>(px_) * S * 2);  // raw mask + 2-pass scratch
   // ring of per-step frame-pointer tables: a table is rewritten only after
@@ -337,7 +335,6 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
     TRB_CUDA(cudaStreamWaitEvent(trk_, early_ms_ ? mot_ev_[b] : ccl_ev_[b], 0));
     tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), trk_, &launches,
                       nullptr, early_ms_ ? ccl_ev_[b] : nullptr);
-    TRB_CUDA(cudaMemcpyAsync(err_host_.p, tracker_->err_word(), sizeof(int32_t), cudaMemcpyDeviceToHost, trk_));
     if (pending_out_) output_(pending_out_, trk_, &launches);  // before CCL(t+2) may reuse this blob table
     TRB_CUDA(cudaEventRecord(trk_ev_[b], trk_));
     trk_pending_[b] = true;
@@ -349,7 +346,6 @@ cudaStream_t Streams::run_(const uint8_t* const* frames_dev, cudaStream_t st, bo
     if (emitted && tracker_) {
       tracker_->process(frames_dev, w_, h_, ch_, ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), st, &launches,
                         profiling_ ? prof_ev_[3] : nullptr);
-      TRB_CUDA(cudaMemcpyAsync(err_host_.p, tracker_->err_word(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     }
     if (pending_out_) output_(pending_out_, st, &launches);
     if (!(emitted && tracker_) && profiling_)
@@ -450,7 +446,7 @@ bool is_pinned_host(const void* p) {
 }
 
 void Streams::check_sticky_errors() {
-  const int32_t e = *static_cast<volatile int32_t*>(err_host_.p);
+  const int32_t e = tracker_ ? tracker_->host_errors() : 0;  // the gate kernel's stores (mapped memory)
   if (e & 1) throw Error(TRB_CAPACITY, "tracker: track capacity exceeded (raise trb_streams_options.track_cap)");
   if (e & 2)
     throw Error(TRB_CAPACITY,

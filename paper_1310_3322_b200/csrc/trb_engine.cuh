@@ -57,6 +57,18 @@ struct PinnedBuf {
     TRB_CUDA(cudaMallocHost(&p, bytes ? bytes : 16));
     n = bytes;
   }
+  // mapped pinned memory: kernels store into it directly (its device address)
+  void alloc_mapped(size_t bytes) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    TRB_CUDA(cudaHostAlloc(&p, bytes ? bytes : 16, cudaHostAllocMapped));
+    n = bytes;
+  }
+  void* device_ptr() const {
+    void* d = nullptr;
+    TRB_CUDA(cudaHostGetDevicePointer(&d, p, 0));
+    return d;
+  }
   template <typename T>
   T* as() const {
     return static_cast<T*>(p);
@@ -188,7 +200,6 @@ class Streams {
   DevBuf warp_buf_, warp_ptrs_, invs_dev_;  // warped frames, their pointer table, inverses [slot][S][9]
   PinnedBuf invs_host_;
   PinnedBuf result_pinned_;
-  PinnedBuf err_host_;          // mirror of the tracker's error word
   DevBuf out_dev_;              // packed step output (trb_step_output regions)
   int out_bcap_ = -1, out_lcap_ = -1;
   PinnedBuf out_bounce_;        // pageable trb_step_output targets go through here

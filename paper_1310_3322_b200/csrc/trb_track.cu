@@ -1556,6 +1556,7 @@ __global__ void __launch_bounds__(1024) track_schedule_kernel(TrackDev d) {
     }
     if (lane == 31) {
       *d.work_n = incl;
+      d.host_mirror[0] = incl;  // the host's active-track hint (cluster size)
       *d.work_head = 0;
       *d.spawn_n = 0;  // this frame's spawn list (track_gate_kernel appends)
       *d.spawn_head = 0;
@@ -1834,6 +1835,7 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
           // the step fails (sticky error, raised by the host at the next call)
           d.err[s] |= 1;
           atomicOr(d.err_any, 1);
+          d.host_mirror[1] = 1;
         } else {
           const int64_t g = slot_index(d, s, slot);
           d.used[g] = 1;
@@ -1882,6 +1884,7 @@ __global__ void __launch_bounds__(NT) track_gate_kernel(TrackDev d) {
   if (!fits && t == 0) {
     atomicOr(&d.err[s], 2);
     atomicOr(d.err_any, 2);
+    d.host_mirror[2] = 1;
   }
   trb_track_log_entry* log = d.log + static_cast<int64_t>(s) * d.log_cap;
   if (t == 0) d.step_log_base[s] = base;
@@ -2392,6 +2395,12 @@ TrackerState::TrackerState(const trb_tracker_config& cfg, int S, int track_cap, 
   d_.list = p, d_.id = p + n, d_.w = p + 2 * n, d_.h = p + 3 * n, d_.status = p + 4 * n, d_.lost = p + 5 * n;
   d_.used = p + 6 * n, d_.pending = p + 7 * n, d_.iters = p + 8 * n;
   d_.err_any = p + 9 * n;
+  mirror_.alloc_mapped(4 * sizeof(int32_t));
+  {
+    volatile int32_t* m = static_cast<volatile int32_t*>(mirror_.p);
+    m[0] = -1, m[1] = 0, m[2] = 0;
+  }
+  d_.host_mirror = static_cast<volatile int32_t*>(mirror_.device_ptr());
   double* f = f64_.as<double>();
   d_.cx = f, d_.cy = f + n, d_.centers = f + 2 * n, d_.hist = f + 2 * n + 3 * K_ * n;
   d_.lut = lut_.as<uint8_t>();
@@ -2476,7 +2485,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   }
   // Mean-shift cluster size (v1 engine, frames above 640x480, TRB_CLUSTER
   // unset): when the active tracks are few (the previous frame's queue length,
-  // mirrored into pinned memory; a frame or two stale) a track gets a 16-CTA
+  // stored into mapped host memory by the schedule kernel; a frame or two stale) a track gets a 16-CTA
   // (or 12-CTA) cluster, which shortens every iteration's walks — the
   // sequential iterations of the biggest windows are the step's critical path
   // (C3 +25 %, C4 +57 %, 8 C5 streams +21 %, 16 streams +13 %); with many
@@ -2484,9 +2493,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   int Gm = G;
   int gridm = grid_;
   if (!v2 && !getenv("TRB_CLUSTER") && static_cast<int64_t>(w) * h > 640 * 480) {
-    if (!nactive_.p) {
-      nactive_.alloc(sizeof(int32_t));
-      *nactive_.as<int32_t>() = -1;
+    if (!grid_big_[0]) {
       for (int k = 0; k < 2; ++k) {
         const int g = k == 0 ? 16 : 12;
         prepare_cluster_kernel(track_meanshift_kernel, smem, g);
@@ -2496,7 +2503,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     }
     // measured crossovers (C5 streams, ~5 tracks each, and C4): 16 wins up to
     // ~40 active tracks (S = 4, 8; C4), 12 around 80 (S = 16), 8 from ~160 (S = 32, 64)
-    const int a = *static_cast<volatile int32_t*>(nactive_.p);
+    const int a = static_cast<const volatile int32_t*>(mirror_.p)[0];  // written by a recent schedule kernel
     if (a >= 0 && a <= 48) Gm = 16, gridm = grid_big_[0];
     else if (a >= 0 && a <= 100) Gm = 12, gridm = grid_big_[1];
   }
@@ -2517,8 +2524,6 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
   else track_gate_kernel<<<S_, NT, 0, st>>>(d_);
   TRB_LAUNCH_CHECK("track_gate_kernel");
   launch_cluster_ex(pdl, track_spawn_kernel, grid_, G, smem, st, d_);
-  // (after the chain, so the copy does not break the programmatic launches)
-  if (nactive_.p) TRB_CUDA(cudaMemcpyAsync(nactive_.p, d_.work_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   *launches += 4;
 }
 

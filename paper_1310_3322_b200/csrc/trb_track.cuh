@@ -36,7 +36,11 @@ struct TrackDev {
   int32_t* next_id;
   int32_t* frame_no;
   int32_t* err;  // bit0 track-capacity overflow, bit1 log overflow
-  int32_t* err_any;  // OR of every stream's err (one word the host mirrors each step)
+  int32_t* err_any;  // OR of every stream's err
+  // mapped pinned host words the kernels store into (no per-step D2H copy):
+  // [0] active tracks of the frame (schedule), [1] / [2] track / log
+  // capacity exceeded (gate; sticky)
+  volatile int32_t* host_mirror;
   // per slot [S][T]
   int32_t *id, *w, *h, *status, *lost, *used, *pending;
   int32_t* iters;  // mean-shift iterations of the last frame (scheduling hint)
@@ -106,6 +110,12 @@ class TrackerState {
                  trb_blob* blobs_out, int bcap, int32_t* n_log_out, trb_track_log_entry* log_out, int lcap,
                  cudaStream_t st);
   const int32_t* err_word() const { return d_.err_any; }
+  // the sticky error bits as the kernels left them in host memory (no sync):
+  // 1 track capacity, 2 log capacity
+  int32_t host_errors() const {
+    const volatile int32_t* m = static_cast<const volatile int32_t*>(mirror_.p);
+    return (m[1] ? 1 : 0) | (m[2] ? 2 : 0);
+  }
   int track_cap() const { return T_; }
   int64_t log_cap() const { return log_cap_; }
   int frames_processed(int s, cudaStream_t st);
@@ -121,7 +131,7 @@ class TrackerState {
   int64_t matched_cap_ = 0;
   int grid_ = 0, grid2_ = 0;
   int grid_big_[2] = {0, 0};  // clusters of 16 and of 12 CTAs (few-track frames)
-  PinnedBuf nactive_;         // the previous frame's active-track count (mirror)
+  PinnedBuf mirror_;          // TrackDev::host_mirror (mapped)
   size_t smem_set_ = 0, smem2_ = 0;
 };
 
