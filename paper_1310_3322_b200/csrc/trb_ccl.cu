@@ -138,10 +138,23 @@ __device__ __forceinline__ void tile_unpack(int v, int& s, int& tx, int& ty) {
 // walk — most of a frame is background (C5: ~8 % foreground).
 __global__ void __launch_bounds__(256) ccl_occupancy_kernel(CclArgs a, int vec_ok) {
   const int n_tiles = a.tiles_x * a.tiles_y;
+  const int s = blockIdx.y;
+  {
+    // per-frame resets of this stream's slot counter, row counts and
+    // survivor bitmap (first used by ccl_local / ccl_mark, which wait for
+    // this grid); the tile-list counter was reset by the previous frame's
+    // ccl_final (this kernel appends to it)
+    const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gn = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if (gt == 0) a.nslots[s] = 0;
+    int32_t* rc = a.rowcount + static_cast<int64_t>(s) * a.h;
+    for (int64_t i = gt; i < a.h; i += gn) rc[i] = 0;
+    uint32_t* bm = a.bitmap + static_cast<int64_t>(s) * a.h * a.wpr;
+    for (int64_t i = gt; i < static_cast<int64_t>(a.h) * a.wpr; i += gn) bm[i] = 0u;
+  }
   const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= n_tiles) return;
-  const int s = blockIdx.y;
   const int tile = s * n_tiles + t;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int gy = ty * kTileH + lane, gx0 = tx * kTileW;
@@ -491,6 +504,9 @@ __global__ void __launch_bounds__(256) ccl_assign_kernel(CclArgs a) {
 // skipped — the plane stays zero there from the allocation on.
 __global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a) {
   pdl_wait();  // launched with launch_pdl: the previous kernel's results first
+  // the next frame's tile list starts empty (ccl_local / ccl_merge, its
+  // readers, completed before this grid got past its PDL wait)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.tile_count = 0;
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -518,11 +534,9 @@ __global__ void __launch_bounds__(256) ccl_final_kernel(CclArgs a) {
 
 int launch_ccl(const CclArgs& a, int S, cudaStream_t st) {
   const int64_t n_tiles = static_cast<int64_t>(a.tiles_x) * a.tiles_y;
-  // per-frame resets: slot counters, row counts and survivor bitmap
-  TRB_CUDA(cudaMemsetAsync(a.nslots, 0, sizeof(int32_t) * S, st));
-  TRB_CUDA(cudaMemsetAsync(a.rowcount, 0, sizeof(int32_t) * static_cast<size_t>(a.h) * S, st));
-  TRB_CUDA(cudaMemsetAsync(a.bitmap, 0, sizeof(uint32_t) * static_cast<size_t>(a.h) * a.wpr * S, st));
-  TRB_CUDA(cudaMemsetAsync(a.tile_count, 0, sizeof(int32_t), st));
+  // per-frame resets happen inside the kernels (ccl_occupancy: slot
+  // counters, row counts, survivor bitmap; ccl_final: the tile-list counter
+  // for the next frame) — no memset launches on the chain
   const int vec_occ = (a.w % 16 == 0);
   ccl_occupancy_kernel<<<dim3(static_cast<unsigned>(ceil_div64(n_tiles * 32, 256)), S), 256, 0, st>>>(a, vec_occ);
   TRB_LAUNCH_CHECK("ccl_occupancy_kernel");

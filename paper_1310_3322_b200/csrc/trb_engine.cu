@@ -176,7 +176,7 @@ CclState::CclState(int S, int w, int h, const trb_seg_config& cfg) : S_(S), w_(w
     blobs_[b].alloc(sizeof(trb_blob) * blob_cap_ * S, false);
     nblobs_[b].alloc(sizeof(int32_t) * S);
   }
-  tiles_.alloc(sizeof(int32_t) * (static_cast<size_t>(tx) * ty * S + 1), false);
+  tiles_.alloc(sizeof(int32_t) * (static_cast<size_t>(tx) * ty * S + 1));  // zeroed: the tile-list counter starts at 0 (then ccl_final resets it)
   tile_state_.alloc(static_cast<size_t>(tx) * ty * S);  // zeroed: no tile labelled yet (labels_ is zeroed too)
 
   CclArgs& a = args_;
