@@ -1491,6 +1491,13 @@ __device__ __forceinline__ TrackScratch cluster_scratch(unsigned char* base, siz
   return s;
 }
 
+// Iteration-count hint for the next frame's queue order: this frame's
+// count, or (iter_decay > 0) a decaying maximum over the recent frames, so a
+// track whose count oscillates is scheduled as its expensive frames need.
+__device__ __forceinline__ int iter_hint(int now, int prev, int decay) {
+  return decay > 0 ? max(now, prev - (prev * decay >> 3)) : now;
+}
+
 // Tracks cheap enough to run on one CTA (estimated from the last frame's
 // iteration count: iters x (30 us + 14.1 us per kpx)) whose window fits the
 // CTA's 1/G share of the cluster scratch.
@@ -1595,7 +1602,7 @@ __device__ void meanshift_item(const TrackDev& d, int q, TrackSmem& sm, const Tr
     d.cx[g] = cx;
     d.cy[g] = cy;
     d.status[g] = status;
-    d.iters[g] = sm.iscal[10];  // scheduling hint for the next frame
+    d.iters[g] = iter_hint(sm.iscal[10], d.iters[g], d.iter_decay);  // scheduling hint for the next frame
   }
 }
 
@@ -1693,7 +1700,7 @@ __device__ void meanshift_item2(const TrackDev& d, int q, V2Smem& sm, bool lead)
     d.cx[g] = cx;
     d.cy[g] = cy;
     d.status[g] = status;
-    d.iters[g] = sm.iscal[10];
+    d.iters[g] = iter_hint(sm.iscal[10], d.iters[g], d.iter_decay);
   }
 }
 
@@ -2460,6 +2467,7 @@ void TrackerState::process(const uint8_t* const* frames_dev, int w, int h, int c
     d_.stream_groups = eg2 ? atoi(eg2) : 1;
     const char* ef = getenv("TRB_ITER_FLOOR");
     d_.iter_floor = ef ? std::max(1, atoi(ef)) : 6;  // iteration history is noisy: order mostly by area
+    d_.iter_decay = static_cast<int>(envf("TRB_ITER_DECAY", 2.0));  // hint = max(now, prev - prev*decay/8); A/B: 2 ahead of 0, 1, 4 (C5 +1.2 %)
     d_.G = G;
     if (getenv("TRB_VERBOSE"))
       fprintf(stderr, "[trb] tracker: %d clusters of %d CTAs, split below %.0f us, %zu B dynamic smem per CTA\n",

@@ -69,6 +69,7 @@ struct TrackDev {
   int32_t* spawn_head;
   int G;               // CTAs per cluster
   int iter_floor;      // scheduling: iterations assumed at least
+  int iter_decay;      // scheduling: iteration hint = max(now, prev - prev*decay/8); 0 = this frame's
   double split_us;     // tracks estimated below this (single-CTA us) run in split mode
   double split_fix, split_perpx;  // single-CTA cost model: us per iteration + us per window pixel
   int order_fix;       // queue order: cost = iterations x (order_fix + window px)
