@@ -86,3 +86,34 @@ def test_config_fuzz_vs_reference(gpu, seed):
     got = run_device(gpu, clips, frames, n, mcfg, scfg, tcfg)
     compare(got, ref)
     assert all(len(g["hashes"]) == n - mcfg.window + 1 for g in got)
+
+
+def make_case_1080p(seed):
+    """Full-HD clips (the v1 mean-shift engine, 8-16-CTA clusters) under
+    non-default configurations."""
+    from paper_1310_3322_b200.synth import random_clip
+    rng = np.random.default_rng(1000 + seed)
+    window = int(rng.choice([17, 40, 91]))
+    n = window - 1 + 15
+    clips = [random_clip(1920, 1080, int(rng.integers(6, 20)), 30, 90, bool(rng.integers(0, 2)),
+                         int(rng.integers(1, 1 << 30)), int(rng.integers(1, 1 << 30)), n) for _ in range(2)]
+    mcfg = MOTION_CFG(method=int(rng.integers(0, 2)), window=window, threshold=int(rng.choice([10, 25, 40])),
+                      bins=int(rng.choice([16, 32])))
+    scfg = SEG_CFG(n_blocks=int(rng.choice([1, 4, 9])), connectivity=int(rng.integers(0, 2)),
+                   min_area=int(rng.choice([1, 4, 30])))
+    tcfg = TRACKER_CFG(k_clusters=int(rng.choice([4, 8, 16, 24])), max_iters=int(rng.choice([5, 20])),
+                       eps=float(rng.choice([0.25, 0.5, 1.0])), kmeans_iters=int(rng.choice([5, 20])),
+                       seed=int(rng.integers(0, 1 << 62)))
+    return clips, n, mcfg, scfg, tcfg
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_config_fuzz_1080p_vs_reference(gpu, seed):
+    if not O.ref_available():
+        pytest.fail("oracle/_ref/libteamrec_ref.so missing: build it with make -C oracle where the reference is")
+    clips, n, mcfg, scfg, tcfg = make_case_1080p(seed)
+    frames = [O.ref_frames(c, n)[0] for c in clips]
+    ref = O.ref_run_streams_detail(frames, 1920, 1080, 1, mcfg, scfg, tcfg, 2, bcap=64, lcap=16384)
+    got = run_device(gpu, clips, frames, n, mcfg, scfg, tcfg)
+    compare(got, ref)
+    assert sum(len(g["log"]) for g in got) > 0
