@@ -264,6 +264,16 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   // host-path staging ring, allocated up front: a step never cudaMallocs
   // (that would serialise the device inside the first host steps)
   for (int i = 0; i < kStaging; ++i) staging_[i].alloc(static_cast<size_t>(px_) * ch_ * S_, false);
+  {
+    // the host path's frame-pointer tables never change (stream s of staging
+    // buffer b is at a fixed offset): uploaded once instead of every step
+    std::vector<const uint8_t*> tab(static_cast<size_t>(kStaging) * S_);
+    const size_t fb = static_cast<size_t>(px_) * ch_;
+    for (int i = 0; i < kStaging; ++i)
+      for (int s = 0; s < S_; ++s) tab[static_cast<size_t>(i) * S_ + s] = staging_[i].as<uint8_t>() + fb * s;
+    staging_ptrs_.alloc(sizeof(void*) * tab.size(), false);
+    TRB_CUDA(cudaMemcpy(staging_ptrs_.p, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
+  }
   for (int i = 0; i < kStaging; ++i) {
     TRB_CUDA(cudaEventCreateWithFlags(&copied_[i], cudaEventDisableTiming));
     TRB_CUDA(cudaEventCreateWithFlags(&consumed_[i], cudaEventDisableTiming));
@@ -521,15 +531,12 @@ void Streams::step_host_async(const uint8_t* const* frames, int32_t* result_host
     s = e;
   }
   TRB_CUDA(cudaEventRecord(copied_[b], copy_));
-  std::vector<const uint8_t*> dev(S_);
-  for (int s = 0; s < S_; ++s) dev[s] = stage + fb * s;
-  const int slot = ptr_slot_;
-  const uint8_t* const* dp = upload_ptrs_(dev.data(), st);
+  const uint8_t* const* dp = staging_ptrs_.as<const uint8_t*>() + static_cast<size_t>(b) * S_;
   TRB_CUDA(cudaStreamWaitEvent(st, copied_[b], 0));
   pending_out_ = out;
   cudaStream_t last_reader;
   try {
-    last_reader = run_(dp, st, overlap_, slot_ev_[slot]);
+    last_reader = run_(dp, st, overlap_, nullptr);  // (staging reuse: consumed_[b] below)
   } catch (...) {
     pending_out_ = nullptr;
     throw;

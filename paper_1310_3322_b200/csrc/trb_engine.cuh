@@ -189,6 +189,7 @@ class Streams {
   std::unique_ptr<CclState> ccl_;
   std::unique_ptr<TrackerState> tracker_;
   DevBuf mask_, mask_tmp_, frame_ptrs_, staging_[kStaging];
+  DevBuf staging_ptrs_;  // [kStaging][S] device pointer tables of the staging planes (constant)
   // step overlap: the tracker of step t runs on trk_ while motion + CCL of
   // step t+1 run on the caller's stream (blob tables double-buffered)
   cudaStream_t trk_ = nullptr;
