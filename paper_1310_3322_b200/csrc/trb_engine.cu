@@ -261,6 +261,7 @@ Streams::Streams(int S, int w, int h, int ch, const trb_motion_config& mc, const
   }
   if (const char* e = getenv("TRB_OVERLAP")) overlap_ = atoi(e) != 0;
   if (const char* e = getenv("TRB_EARLY_MS")) early_ms_ = atoi(e) != 0;
+  if (const char* e = getenv("TRB_DIRECT_OUT")) direct_out_ = atoi(e) != 0;
   // host-path staging ring, allocated up front: a step never cudaMallocs
   // (that would serialise the device inside the first host steps)
   for (int i = 0; i < kStaging; ++i) staging_[i].alloc(static_cast<size_t>(px_) * ch_ * S_, false);
@@ -446,13 +447,26 @@ void CUDART_CB copy_result(void* p) {
 }
 }  // namespace
 
-bool is_pinned_host(const void* p) {
+bool is_pinned_host(const void* p) { return pinned_device_alias(p) != nullptr || pinned_unmapped(p); }
+
+// Pinned host memory's device-side address (UVA: normally the same pointer),
+// or nullptr when `p` is not pinned host memory or not mapped for the device.
+void* pinned_device_alias(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+bool pinned_unmapped(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeHost && !a.devicePointer;
 }
 
 void Streams::check_sticky_errors() {
@@ -482,6 +496,22 @@ void Streams::output_(const trb_step_output* out, cudaStream_t rs, int* launches
   int32_t* nl = nb + S_;
   trb_blob* bl = reinterpret_cast<trb_blob*>(base + hdr);
   trb_track_log_entry* lg = reinterpret_cast<trb_track_log_entry*>(base + hdr + bbytes);
+  if (has_output_ && tracker_ && direct_out_) {
+    // the pack kernel stores straight into the caller's pinned buffers
+    // (their device aliases): no copy launches on the step's chain
+    void* d[4] = {nullptr, nullptr, nullptr, nullptr};
+    const void* h[4] = {out->n_blobs, out->n_log, bcap ? out->blobs : nullptr, lcap ? out->log : nullptr};
+    bool ok = true;
+    for (int i = 0; i < 4 && ok; ++i)
+      if (h[i]) ok = (d[i] = pinned_device_alias(h[i])) != nullptr;
+    if (ok) {
+      tracker_->pack_step(ccl_->blobs(), ccl_->blob_cap(), ccl_->nblobs(), d[0] ? static_cast<int32_t*>(d[0]) : nb,
+                          d[2] ? static_cast<trb_blob*>(d[2]) : bl, bcap, d[1] ? static_cast<int32_t*>(d[1]) : nl,
+                          d[3] ? static_cast<trb_track_log_entry*>(d[3]) : lg, lcap, rs);
+      ++*launches;
+      return;
+    }
+  }
   if (!has_output_) {
     TRB_CUDA(cudaMemsetAsync(base, 0, hdr, rs));
   } else if (tracker_) {

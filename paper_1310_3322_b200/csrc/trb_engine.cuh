@@ -76,6 +76,8 @@ struct PinnedBuf {
 };
 
 bool is_pinned_host(const void* p);
+void* pinned_device_alias(const void* p);
+bool pinned_unmapped(const void* p);
 void validate_motion(const trb_motion_config& c);
 void validate_seg(const trb_seg_config& c, int w, int h);
 void validate_tracker(const trb_tracker_config& c);
@@ -194,7 +196,8 @@ class Streams {
   // step t+1 run on the caller's stream (blob tables double-buffered)
   cudaStream_t trk_ = nullptr;
   cudaEvent_t ccl_ev_[2] = {}, trk_ev_[2] = {}, mot_ev_[2] = {};
-  bool early_ms_ = true;  // mean-shift waits for the step's motion only, the gate for its CCL (TRB_EARLY_MS=0: both for CCL)
+  bool early_ms_ = true;
+  bool direct_out_ = true;  // step outputs stored by the pack kernel into the caller's pinned buffers (TRB_DIRECT_OUT=0: copies)  // mean-shift waits for the step's motion only, the gate for its CCL (TRB_EARLY_MS=0: both for CCL)
   bool trk_pending_[2] = {false, false};
   int last_trk_ = -1;
   bool overlap_ = true;  // TRB_OVERLAP=0 disables (A/B)
